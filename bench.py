@@ -1,0 +1,410 @@
+"""Benchmark of the fused VQ hot path on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on): the
+decode-step linears of Llama-7B under QuiP#-style E8 VQ (VQConfig(8, 16, 1),
+whole-tensor 2^16-entry codebook, codes drawn from the 256-entry working set),
+batch 1. A step = one fused VQ GEMV over every linear of all 32 layers (q/k/v
+fused as one 4096x12288 GEMV, o 4096x4096, gate/up fused 4096x22016, down
+11008x4096: 128 launches), replayed as one CUDA graph. The 1.6 GB of codes is
+> L2 (126 MB), so no flush is needed between steps.
+
+value      whole-job algorithmic GB/s (codes + working-set codebook + x + y bytes)
+e2e        the same through VQLinearStack.run with pinned host buffers (H2D of all
+           activations, D2H of all outputs inside the timed region)
+roofline   the dominant kernel (gemv_fast) against MEASURED_PEAKS.json hbm_gbs
+cpu_baseline  the numpy oracle (dequantize + fp32 matmul) on a bounded sample
+extra keys C4 decode attention and C1 GPTVQ GEMV per-call numbers
+
+--impl reference times the reference algorithm's CPU restatement (oracle port)
+on the host cores on the same metric.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused VQ GEMV/attn µs/call & HBM GB/s vs roofline; decode tokens/s Llama-7B"
+LLAMA7B = [("qkv", 4096, 12288), ("o", 4096, 4096), ("gate_up", 4096, 22016), ("down", 11008, 4096)]
+N_LAYERS = 32
+WORK = 256
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(m, n, rows=1, code_bits=16, v=8, work=WORK):
+    codes = (m * n // v) * code_bits // 8
+    books = work * v * 2
+    return codes + books + rows * m * 2 + rows * n * 2
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index=0):
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if self.p is None:
+            return out
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for name, val in zip(names, parts[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+        if sm:
+            out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------------------------------
+# CPU legs (oracle port: the reference's algorithm restated, V/codec.py:391-408 + V/sim.py:133-144)
+
+def cpu_sample(seconds_budget=12.0):
+    """Oracle dequantize + fp32 GEMV of one 4096x4096 q_proj at the workload config, repeated
+    up to ~seconds_budget; returns (GB/s, sample description, cores)."""
+    from oracle import vq_oracle as O
+
+    m, n, v = 4096, 4096, 8
+    codes, books = O.synthetic_codes_books((m, n), v, 16, 1, 1, 0, working_entries=WORK)
+    regions = np.zeros(m * n // v, dtype=np.int64)
+    x = O.synthetic_tensor((m,), 2)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        w = O.dequantize(codes, books, (m, n), v, 1, regions)
+        O.matmul_ref(x, w)
+        reps += 1
+        if time.perf_counter() - t0 > seconds_budget or reps >= 50:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    gbs = algorithmic_bytes(m, n) / dt / 1e9
+    return gbs, f"numpy oracle dequantize+matmul of one 4096x4096 q_proj, {reps} reps, {dt*1e3:.1f} ms each", 1
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    step_bytes = sum(algorithmic_bytes(m, n) for _, m, n in LLAMA7B) * N_LAYERS
+    for _ in range(args.warmup):
+        cpu_sample(seconds_budget=0.5)
+    vals = []
+    for _ in range(args.steps):
+        gbs, sample, cores = cpu_sample(seconds_budget=3.0)
+        vals.append(gbs)
+    value = float(np.median(vals))
+    ms = step_bytes / (value * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "llama7b-decode-linears quip2 VQ<8,16,1> ws256 batch1 (sampled on q_proj)"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------------
+
+def build_stack(torch, dev, rank=0, world=1):
+    from paper_2503_02236_b200.codec import VQConfig
+    from paper_2503_02236_b200.device import DeviceVQTensor
+    from paper_2503_02236_b200.stack import VQLinearStack
+
+    cfg = VQConfig(8, 16, 1)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    weights, bytes_per = [], []
+    for _layer in range(N_LAYERS):
+        for _name, m, n in LLAMA7B:
+            n_loc = n // world
+            s = m * n_loc // 8
+            codes = torch.randint(0, WORK, (1, s), generator=g, device=dev, dtype=torch.int32)
+            books = (torch.randn((1, 1 << 16, 8), generator=g, device=dev) * 0.1).half()
+            w = DeviceVQTensor.from_device_codes(codes, (m, n_loc), cfg, books, layout="plain").relayout("gemv")
+            weights.append(w)
+            bytes_per.append(algorithmic_bytes(m, n_loc))
+    stack = VQLinearStack(weights, rows=1)
+    stack.x.copy_((torch.randn(stack.x.shape, generator=g, device=dev)).half())
+    return stack, bytes_per
+
+
+def time_attention(torch, dev, ops, N):
+    """C4: CQ-4 KV cache decode attention, B16 H32 T4096 C128 (per-call us, GB/s)."""
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    from paper_2503_02236_b200.device import DeviceVQTensor
+
+    B, H, T, C = 16, 32, 4096, 128
+    cfg = VQConfig(2, 8, 1, Sharing.per_channel_group(2))
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    s = B * H * T * C // 2
+    kv = []
+    for _ in range(2):
+        codes = torch.randint(0, 256, (1, s), generator=g, device=dev, dtype=torch.int32)
+        books = (torch.randn((H * 64, 256, 2), generator=g, device=dev) * 0.1).half()
+        kv.append(DeviceVQTensor.from_device_codes(codes, (B, H, T, C), cfg, books).relayout("kv"))
+    q = torch.randn((B, H, C), generator=g, device=dev).half()
+    for _ in range(3):
+        ops.vq_attention(kv[0], kv[1], q, out_dtype=torch.float16)
+    kern = N.last_kernel()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        ops.vq_attention(kv[0], kv[1], q, out_dtype=torch.float16)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    alg = 2 * s + 2 * H * 64 * 256 * 2 * 2 + B * H * C * 2 * 2
+    # dense fp16 baseline at equal shape (flash-attn decode), if importable
+    dense_us = None
+    try:
+        from flash_attn import flash_attn_with_kvcache
+        kd = torch.randn((B, T, H, C), device=dev, dtype=torch.float16)
+        vd = torch.randn((B, T, H, C), device=dev, dtype=torch.float16)
+        qd = q.view(B, 1, H, C)
+        for _ in range(3):
+            flash_attn_with_kvcache(qd, kd, vd)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            flash_attn_with_kvcache(qd, kd, vd)
+        e1.record()
+        torch.cuda.synchronize()
+        dense_us = e0.elapsed_time(e1) * 1e3 / reps
+        del kd, vd
+    except Exception as ex:  # pragma: no cover - optional baseline
+        dense_us = f"unavailable: {type(ex).__name__}"
+    return {"config": "C4 cq4 VQ<2,8,1> cg2 B16 H32 T4096 C128", "kernel": kern, "us_per_call": us,
+            "alg_bytes": alg, "GB_s": alg / us / 1e3, "fp16_flash_attn_us": dense_us}
+
+
+def time_gemv_single(torch, dev, ops, N, label, cfg_args, shape, work=None):
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    from paper_2503_02236_b200.device import DeviceVQTensor
+
+    v, bits, r, sharing = cfg_args
+    cfg = VQConfig(v, bits, r, sharing)
+    m, n = shape
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    from paper_2503_02236_b200.codec import region_count
+    nreg = region_count(shape, cfg)
+    hi = work or (1 << bits)
+    # 32 distinct copies so the cycle exceeds L2
+    ws = []
+    for _ in range(32):
+        codes = torch.randint(0, hi, (r, m * n // v), generator=g, device=dev, dtype=torch.int32)
+        books = (torch.randn((r * nreg, 1 << bits, v), generator=g, device=dev) * 0.1).half()
+        ws.append(DeviceVQTensor.from_device_codes(codes, shape, cfg, books).relayout("gemv"))
+    x = torch.randn((m,), generator=g, device=dev).half()
+    for w in ws[:3]:
+        ops.vq_gemv(w, x, out_dtype=torch.float16)
+    kern = N.last_kernel()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for w in ws:
+        ops.vq_gemv(w, x, out_dtype=torch.float16)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / len(ws)
+    alg = ws[0].algorithmic_bytes(work) + m * 2 + n * 2
+    dense = torch.randn((m, n), device=dev, dtype=torch.float16)
+    xd = x.view(1, m)
+    for _ in range(3):
+        torch.matmul(xd, dense)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        torch.matmul(xd, dense)
+    e1.record()
+    torch.cuda.synchronize()
+    dense_us = e0.elapsed_time(e1) * 1e3 / 20
+    return {"config": label, "kernel": kern, "us_per_call": us, "alg_bytes": alg, "GB_s": alg / us / 1e3,
+            "fp16_cublas_us": dense_us, "note": "eager launches, 32 distinct weights cycled (> L2)"}
+
+
+def run_impl(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2503_02236_b200 import _native as N
+    from paper_2503_02236_b200 import ops
+
+    stack, bytes_per = build_stack(torch, dev, rank, world)
+    step_bytes = sum(bytes_per)
+    stream = torch.cuda.current_stream(dev)
+
+    # per-kernel durations (eager, CUDA events on the launching stream)
+    stack.launch_all()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in stack.weights]
+    lib = N.lib()
+    for i, (s, L) in enumerate(zip(stack._structs, stack.launches)):
+        evs[i][0].record(stream)
+        N.check(lib.vqb_gemv(s, stack.input_view(i).data_ptr(), N.F16, 1, stack.output_view(i).data_ptr(),
+                             N.F16, L, stack._ws.data_ptr(), stack._ws.numel(), stream.cuda_stream))
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    kern = N.last_kernel()
+    durs = [a.elapsed_time(b) * 1e-3 for a, b in evs]
+    kernel_achieved = sum(bytes_per) / sum(durs) / 1e9
+
+    stack.capture()
+    for _ in range(max(args.warmup, 3)):
+        stack.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        stack.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    # e2e through the public API with pinned host buffers
+    hx = torch.empty(stack.x.shape, dtype=stack.x.dtype, pin_memory=True)
+    hx.copy_(stack.x)
+    hy = torch.empty(stack.y.shape, dtype=stack.y.dtype, pin_memory=True)
+    for _ in range(2):
+        stack.run(hx, hy)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(args.steps):
+        stack.run(hx, hy)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(t[0]), float(t[1])
+
+    if rank == 0:
+        hbm, src = peaks()
+        total_bytes = step_bytes * world
+        value = total_bytes / (ms * 1e-3) / 1e9
+        extra = {}
+        if not args.no_extra and world == 1:
+            from paper_2503_02236_b200.codec import Sharing
+            extra["attention_c4"] = time_attention(torch, dev, ops, N)
+            extra["gemv_c1_gptvq2_q_proj"] = time_gemv_single(
+                torch, dev, ops, N, "C1 gptvq2 VQ<4,8,1> tile256 4096x4096 b1", (4, 8, 1, Sharing.per_tile(256, 256)),
+                (4096, 4096))
+            extra["gemv_c2_quip2_q_proj"] = time_gemv_single(
+                torch, dev, ops, N, "C2 quip2 VQ<8,16,1> ws256 4096x4096 b1", (8, 16, 1, Sharing.whole_tensor()),
+                (4096, 4096), work=WORK)
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            gbs, sample, cores = cpu_sample()
+            cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": "llama7b-decode-linears quip2 VQ<8,16,1> ws256 batch1",
+                       "layers": N_LAYERS, "launches_per_step": stack.n_launches,
+                       "parallelism": f"tp{world}" if world > 1 else "single",
+                       "l2": "inputs 1.6 GB/GPU > L2, no flush", "graph": True},
+            "us_per_call": ms * 1e3 / stack.n_launches,
+            "e2e": {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": int(stack.x.numel() * stack.x.element_size()),
+                    "d2h_bytes_per_step": int(stack.y.numel() * stack.y.element_size()),
+                    "ms_per_step": e2e_ms},
+            "roofline": {"bound": "hbm", "achieved": kernel_achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": kernel_achieved / hbm, "traffic": None, "kernel": kern,
+                         "peak_source": src, "kernel_us_mean": 1e6 * float(np.mean(durs))},
+            "cpu_baseline": cpu,
+            "gpu_launches": stack.n_launches * args.steps * 2,
+            "clocks": clk,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_impl(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,183 @@
+/*
+ * vqb.h — C ABI of the B200-native fused vector-quantization kernels.
+ *
+ * This is the drop-in boundary for the reference's fused-kernel operator API
+ * (vqforge, a pure-Python package with no FFI of its own). Each entry point
+ * replaces one reference call; the Python mirror in
+ * paper_2503_02236_b200/_native.py binds them with ctypes, and INTEGRATION.md
+ * shows the binding a vqforge maintainer would add.
+ *
+ *   vqb_dequant      <- vqforge.codec.dequantize                 (pkg/src/vqforge/codec.py:391-408)
+ *   vqb_gemv         <- SimMachine.run_fused_kernel, ComputeOp.gemv (pkg/src/vqforge/sim.py:297-316,
+ *                       executed by _matmul/_mm_block, sim.py:697-775; op at dataflow.py:73-75)
+ *   vqb_gemm         <- SimMachine.run_fused_kernel, ComputeOp.gemm (sim.py:297-316, dataflow.py:68-71)
+ *   vqb_attn_decode  <- SimMachine.run_fused_kernel, ComputeOp.attention_decode
+ *                       (sim.py:491-693, dataflow.py:77-82)
+ *   vqb_repack       <- QuantizedTensor.packed_codes / bitpack.unpack_indices
+ *                       (codec.py:215-218, bitpack.py:31-43): packed stream -> kernel layout
+ *   vqb_query_usage  <- sim.KERNEL_USAGE (sim.py:53-57): real per-kernel resource usage
+ *                       feeding compute_slack (cacheplan.py:27-62)
+ *   vqb_last_error   <- the message of the raised vqforge.errors exception (errors.py:4-25)
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Every pointer named d_* is DEVICE memory owned
+ *    by the caller; the library never allocates or frees caller memory.
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered and
+ *    asynchronous (no host synchronisation) and reentrant.
+ *  - Return 0 on success, or a negative VQB_E* code whose class maps 1:1 onto the
+ *    reference exception hierarchy; vqb_last_error() then holds the message
+ *    (thread-local), keeping the reference's wording (e.g. "code out of range").
+ *  - Weights follow the reference layout: W is (M = input/reduction, N = output)
+ *    and y = x @ W (sim.py:136-144). Sub-vectors run along the last axis
+ *    (codec.py:229-236): along N for weights, along C for the KV cache.
+ */
+#ifndef VQB_H_
+#define VQB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VQB_ABI_VERSION 1
+
+/* ---- status codes (errors.py:4-25) ---- */
+#define VQB_OK 0
+#define VQB_ESHAPE -1     /* ShapeError */
+#define VQB_ECONFIG -2    /* ConfigError */
+#define VQB_ECODERANGE -3 /* CodeRangeError */
+#define VQB_ECAPACITY -4  /* CapacityError */
+#define VQB_EMAPPING -5   /* MappingError */
+#define VQB_ECUDA -10     /* CUDA runtime failure (RuntimeError in Python) */
+
+/* ---- element types ---- */
+#define VQB_F32 0
+#define VQB_F16 1
+#define VQB_BF16 2
+
+/* ---- codebook sharing (codec.py:23-57) ---- */
+#define VQB_SHARE_WHOLE 0
+#define VQB_SHARE_TILE 1
+#define VQB_SHARE_CHANNEL_GROUP 2
+
+/* ---- code-stream layouts ----
+ * PACKED   : the reference stream, level-major, `log2_entries` bits per code,
+ *            LSB-first, byte padded at the end only (bitpack.py:13-28). Any width 1..16.
+ * GEMV_IL  : weight codes interleaved for 128-bit lane loads, per level
+ *            [M/RPL][G][RPL] with G = N/v sub-vectors per row and RPL = 16/code_bytes
+ *            rows per 16-byte load (8 rows of u16 codes, 16 rows of u8 codes).
+ *            Levels are stored one after another (level-major, like the reference).
+ * KV_IL    : KV-cache codes interleaved for the decode-attention kernel (u8 codes,
+ *            G = C/v in {32, 64}), per level and per (b, h) row block of T tokens:
+ *            [T/TPL][32][TPL][GPL] with GPL = G/32 groups per lane (lane l owns groups
+ *            l + 32*j) and TPL = 16/GPL tokens per 16-byte lane load.
+ * PLAIN    : the reference `codes` array (R, S) level-major in the narrowest unsigned
+ *            type: u8 when log2_entries <= 8, else u16.
+ */
+#define VQB_LAYOUT_PACKED 0
+#define VQB_LAYOUT_GEMV_IL 1
+#define VQB_LAYOUT_KV_IL 2
+#define VQB_LAYOUT_PLAIN 3
+
+/* One quantized tensor as the kernels see it (QuantizedTensor, codec.py:180-226). */
+typedef struct VqbTensor {
+  int32_t vector_size;  /* v in {2,4,8,16} */
+  int32_t log2_entries; /* b in [1,16]; K = 2^b entries per codebook */
+  int32_t residuals;    /* R >= 1 */
+  int32_t sharing;      /* VQB_SHARE_* */
+  int32_t tile_rows, tile_cols, group_width;
+  int32_t ndim;         /* 1..4 */
+  int64_t dims[4];      /* tensor shape, last axis split into sub-vectors */
+  int32_t n_regions;    /* regions per level (region_layout, codec.py:135-177) */
+  int32_t layout;       /* VQB_LAYOUT_* of d_codes */
+  const void* d_codes;  /* code stream in `layout` */
+  int64_t codes_bytes;  /* allocated bytes behind d_codes (bounds check) */
+  int32_t codebook_dtype;   /* VQB_F32 / VQB_F16 / VQB_BF16 */
+  const void* d_codebooks;  /* (R*n_regions, K, v) contiguous, level-major (codec.py:208-209) */
+} VqbTensor;
+
+/* Launch knobs from the planner (FusedPlans, sim.py:229-236). Zero-initialise
+ * for defaults. */
+typedef struct VqbLaunch {
+  int32_t n_reg;        /* CachePlan.n_reg: register-resident entries (reserved, 0 on B200) */
+  int32_t n_shared;     /* CachePlan.n_shared: entries resident in shared memory; 0 = planner default */
+  int32_t split_axis;   /* 0 none, 'M', 'R', 'C', 'T' as char codes (DataflowPlan.split_axis) */
+  int32_t split_factor; /* DataflowPlan.split_factor; 0 = kernel default */
+  int32_t fusion_level; /* 0 register, 1 shared (informational on B200) */
+  int32_t grid_limit;   /* max CTAs (0 = SM count x occupancy) */
+  int32_t flags;        /* VQB_FLAG_* */
+} VqbLaunch;
+
+#define VQB_FLAG_FORCE_GENERIC 1 /* use the generic (any-config) kernel */
+
+/* Kernel resource usage (KernelUsage, gpumodel.py:30-36) measured with
+ * cudaFuncGetAttributes on the loaded cubin. */
+typedef struct VqbUsage {
+  int32_t shared_bytes;      /* static + dynamic shared memory per CTA at the default plan */
+  int32_t regs_per_thread;
+  int32_t threads_per_block;
+  int32_t max_blocks_per_sm; /* occupancy at that usage */
+  int32_t sm_count;
+} VqbUsage;
+
+#define VQB_KERNEL_DEQUANT 0
+#define VQB_KERNEL_GEMV 1
+#define VQB_KERNEL_GEMM 2
+#define VQB_KERNEL_ATTN 3
+
+int vqb_abi_version(void);
+const char* vqb_last_error(void);
+/* Name of the last kernel this thread launched ("gemv_fast", "attn_cq", ...):
+ * lets tests and the benchmark prove which path ran. */
+const char* vqb_last_kernel(void);
+
+/* Reconstruct the dense tensor (dequantize, codec.py:391-408): fp32 output is
+ * bit-exact with the reference (accumulation from +0.0f in level order);
+ * fp16/bf16 outputs are RN-even casts of that fp32 value. */
+int vqb_dequant(const VqbTensor* t, void* d_out, int32_t out_dtype, void* stream);
+
+/* Workspace bytes a fused call needs (split partials + arrival counters).
+ * kind = VQB_KERNEL_*; rows = batch rows (GEMV/GEMM) or B*H (attention). */
+int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t rows,
+                            const VqbLaunch* launch);
+
+/* y(rows, N) = x(rows, M) @ dequant(W)(M, N). rows in [1, 8] take the CUDA-core
+ * decode kernel; larger rows should use vqb_gemm. The workspace must be zeroed
+ * once before first use (counters self-reset afterwards). */
+int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows,
+             void* d_y, int32_t y_dtype, const VqbLaunch* launch, void* d_ws,
+             size_t ws_bytes, void* stream);
+
+/* Prefill GEMM: y(rows, N) = x(rows, M) @ dequant(W). Dequantised W tiles are
+ * written to shared memory in the UMMA canonical layout and consumed by
+ * tcgen05.mma with the accumulator in TMEM. x must be fp16 or bf16 matching the
+ * codebook dtype, M % 64 == 0, N % 128 == 0 (otherwise VQB_ESHAPE). */
+int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows,
+             void* d_y, int32_t y_dtype, const VqbLaunch* launch, void* d_ws,
+             size_t ws_bytes, void* stream);
+
+/* Decode attention over a VQ KV cache: out(B,H,C) = softmax(q.K^T / sqrt(C)) V
+ * with K, V (B,H,T,C) quantized tensors (sim.py:491-521, oracle sim.py:145-155). */
+int vqb_attn_decode(const VqbTensor* k, const VqbTensor* v, const void* d_q,
+                    int32_t q_dtype, int32_t B, int32_t H, int32_t T, int32_t C,
+                    void* d_out, int32_t out_dtype, const VqbLaunch* launch,
+                    void* d_ws, size_t ws_bytes, void* stream);
+
+/* Convert a PACKED stream (src, layout must be VQB_LAYOUT_PACKED) into
+ * `dst_layout`, writing into d_dst (dst_bytes available). Bytes needed are
+ * returned by vqb_layout_bytes. */
+int64_t vqb_layout_bytes(const VqbTensor* t, int32_t layout);
+int vqb_repack(const VqbTensor* src, int32_t dst_layout, void* d_dst,
+               int64_t dst_bytes, void* stream);
+
+/* Measured resource usage of a kernel family at its default configuration for
+ * tensor `t` (may be NULL for the family default). */
+int vqb_query_usage(int32_t kind, const VqbTensor* t, VqbUsage* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VQB_H_ */

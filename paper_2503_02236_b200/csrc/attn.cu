@@ -1,0 +1,479 @@
+// attn.cu — fused decode attention over a VQ-compressed (CQ) KV cache.
+//
+// Replaces SimMachine._attention / _attention_naive / _attention_centric
+// (pkg/src/vqforge/sim.py:491-693) for ComputeOp.attention_decode
+// (dataflow.py:77-82). Oracle: reference_compute (sim.py:145-155):
+//   logits = (q . K_t) / sqrt(C); p = softmax(logits); out = sum_t p_t V_t.
+//
+// Fast kernel (channel-group sharing with group_width == v, one residual level,
+// u8 codes, fp16 codebooks, KV_IL layout, C/v in {32, 64}):
+//  * codebook-centric dataflow: work units (h, b, T-chunk) are ordered head-major
+//    and dealt out as contiguous ranges to persistent CTAs, so a CTA loads the K
+//    and V codebooks of a head once (CQ books are per head and shared by all
+//    batch rows and tokens, codec.py:161-165) and reuses them across batch rows.
+//  * K side as a lookup table: the query is fixed per (b, h), so the CTA builds
+//    LUT[e][g] = log2(e)/sqrt(C) * <q_g, K_book_g[e]> once per (b, h); a token's
+//    logit is then sum_g LUT[code_g][g] — one conflict-free LDS.32 + FADD per
+//    code instead of a dequantise-and-dot.
+//  * bank-conflict-free layouts by construction: lane l owns channel groups
+//    g = l + 32j; both the LUT and the V codebook are stored [entry][group] so
+//    lane l always hits bank (l mod 32) whatever its code is.
+//  * per-lane partial logits are reduced across the warp with a 31-shuffle
+//    transpose-reduction that leaves lane l holding token l's logit; softmax is
+//    online (flash-decode) in the exp2 domain; V is dequantised in registers and
+//    fused into fp32 accumulators with fma.rn.f32.f16.
+//  * split-T partials (m, l, acc) per contiguous span are merged by the last
+//    arriving CTA in fixed T order (deterministic), like the reference's split
+//    reduction (sim.py:604-620).
+// Generic path: dequantise K and V to fp32 (vqb_dequant) and run a plain fp32
+// decode attention; covers every other configuration.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vqb {
+
+int launch_dequant(const Geom& g, const VqbTensor* t, void* out, int out_dtype, cudaStream_t st);
+
+constexpr int kAttnWarps = 16;
+constexpr int kAttnThreads = kAttnWarps * 32;
+constexpr int kAttnChunk = 512;  // tokens per work unit
+
+struct AttnArgs {
+  const uint8_t* kc;
+  const uint8_t* vc;
+  const __half* kb;
+  const __half* vb;
+  const void* q;
+  int q_dtype;
+  void* out;
+  int out_dtype;
+  float* part;   // (B*H, NT, C + 3)
+  int* counters; // B*H
+  int B, H, T, NT;
+  float scale_log2;
+};
+
+template <int V, int GPL>
+struct AttnSmem {
+  static constexpr int G = 32 * GPL;
+  static constexpr int C = G * V;
+  static constexpr size_t book_bytes = 256 * (size_t)C * 2;   // [256][G] x V halves
+  static constexpr size_t lut_bytes = 256 * (size_t)G * 4;    // [256][G] fp32
+  static constexpr size_t scratch_bytes = (size_t)kAttnWarps * (C + 2) * 4;
+  static constexpr size_t total = 2 * book_bytes + lut_bytes + scratch_bytes;
+};
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int V, int GPL>
+__global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
+  using SM = AttnSmem<V, GPL>;
+  constexpr int G = SM::G, C = SM::C;
+  constexpr int TPL = 16 / GPL;      // tokens per 16-byte code load
+  constexpr int LPB = 32 / TPL;      // loads per 32-token batch
+  constexpr int EPB = V * 2;         // entry bytes
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* kbook_s = smem;
+  uint8_t* vbook_s = smem + SM::book_bytes;
+  float* lut_s = reinterpret_cast<float*>(smem + 2 * SM::book_bytes);
+  float* scratch = reinterpret_cast<float*>(smem + 2 * SM::book_bytes + SM::lut_bytes);
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lut_base = smem_u32(lut_s);
+  const uint32_t vbook_base = smem_u32(vbook_s);
+  const int BNT = a.B * a.NT;
+  const int U = a.H * BNT;
+  const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+  const int64_t TG = (int64_t)a.T * G;  // code bytes per (b, h)
+
+  int cur_h = -1;
+  for (int u = u0; u < u1;) {
+    const int h = u / BNT;
+    const int b = (u / a.NT) % a.B;
+    const int tc0 = u % a.NT;
+    const int span_end = min(u1, (u / a.NT + 1) * a.NT);
+    const int tc1 = tc0 + (span_end - u);
+    const int bh = b * a.H + h;
+    const int tok0 = tc0 * kAttnChunk;
+    const int tok1 = min(tc1 * kAttnChunk, a.T);
+
+    __syncthreads();  // previous span finished with books / LUT / scratch
+    if (h != cur_h) {
+      // ---- Switch/Load: the K and V codebooks of head h, transposed to [e][g]
+      constexpr int EPL = 16 / EPB;  // entries per 16-byte read
+      constexpr int ITEMS = G * (256 / EPL);
+      for (int it = tid; it < 2 * ITEMS; it += kAttnThreads) {
+        const int which = it / ITEMS;
+        const int item = it - which * ITEMS;
+        const int g = item % G, ec = item / G;
+        const __half* src = (which ? a.vb : a.kb) + ((int64_t)(h * G + g) * 256 + ec * EPL) * V;
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(src));
+        uint8_t* dst = which ? vbook_s : kbook_s;
+        const uint32_t* wp = &w.x;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          uint8_t* d = dst + ((size_t)(ec * EPL + i) * G + g) * EPB;
+          if constexpr (V == 2) *reinterpret_cast<uint32_t*>(d) = wp[i];
+          else *reinterpret_cast<uint2*>(d) = make_uint2(wp[2 * i], wp[2 * i + 1]);
+        }
+      }
+      cur_h = h;
+      __syncthreads();
+    }
+    // ---- LUT for (b, h): LUT[e][g] = scale_log2 * <q_g, Kbook_g[e]>
+    {
+      const int g = tid % G;  // constant per thread since kAttnThreads % G == 0
+      float qv[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        qv[j] = load_as_f32(a.q, a.q_dtype, (int64_t)bh * C + g * V + j) * a.scale_log2;
+      for (int idx = tid; idx < 256 * G; idx += kAttnThreads) {
+        const int e = idx / G;
+        const __half* ent = reinterpret_cast<const __half*>(kbook_s + ((size_t)e * G + g) * EPB);
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < V; ++j) s = fmaf(qv[j], __half2float(ent[j]), s);
+        lut_s[idx] = s;
+      }
+    }
+    __syncthreads();
+
+    // ---- stream the span's tokens: warp w takes 32-token batches w, w+16, ...
+    float m_w = -INFINITY, l_lane = 0.f;
+    float acc[GPL][V];
+#pragma unroll
+    for (int j = 0; j < GPL; ++j)
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+    const uint8_t* kbase = a.kc + (int64_t)bh * TG;
+    const uint8_t* vbase = a.vc + (int64_t)bh * TG;
+    for (int t0 = tok0 + warp * 32; t0 < tok1; t0 += kAttnWarps * 32) {
+      uint4 kcv[LPB], vcv[LPB];
+#pragma unroll
+      for (int i = 0; i < LPB; ++i) {
+        const int64_t off = ((int64_t)(t0 / TPL + i) * 32 + lane) * 16;
+        kcv[i] = ldg_stream(kbase + off);
+        vcv[i] = ldg_stream(vbase + off);
+      }
+      // K phase: per-lane partial logits of the 32 tokens over this lane's groups
+      float s[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t w = (&kcv[k / TPL].x)[((k % TPL) * GPL) / 4];
+        float acc_s = 0.f;
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+          const int byte = ((k % TPL) * GPL + j) % 4;
+          const uint32_t code = (w >> (8 * byte)) & 0xff;
+          acc_s += lds_f32(lut_base + ((code * G + lane + 32 * j) << 2));
+        }
+        s[k] = acc_s;
+      }
+      // transpose-reduce: afterwards s[0] on lane l is the full logit of token l
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+          const float send = upper ? s[i] : s[i + off];
+          const float keep = upper ? s[i + off] : s[i];
+          s[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      const bool valid = (t0 + lane) < tok1;
+      const float z = valid ? s[0] : -INFINITY;
+      float mb = z;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
+      const float m_new = fmaxf(m_w, mb);
+      const float corr = fast_exp2(m_w - m_new);
+      const float p = fast_exp2(z - m_new);
+      l_lane = l_lane * corr + p;
+      m_w = m_new;
+#pragma unroll
+      for (int j = 0; j < GPL; ++j)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[j][i] *= corr;
+      const uint32_t ph = (uint32_t)__half_as_ushort(__float2half_rn(p));
+      // V phase: dequantise V in registers, fused into the fp32 accumulators
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint16_t pk = (uint16_t)__shfl_sync(0xffffffffu, ph, k);
+        const uint32_t w = (&vcv[k / TPL].x)[((k % TPL) * GPL) / 4];
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+          const int byte = ((k % TPL) * GPL + j) % 4;
+          const uint32_t code = (w >> (8 * byte)) & 0xff;
+          const uint32_t addr = vbook_base + (code * G + lane + 32 * j) * EPB;
+          if constexpr (V == 2) {
+            const uint32_t e = lds32(addr);
+            acc[j][0] = fma_h((uint16_t)(e & 0xffff), pk, acc[j][0]);
+            acc[j][1] = fma_h((uint16_t)(e >> 16), pk, acc[j][1]);
+          } else {
+            const uint2 e = lds64(addr);
+            acc[j][0] = fma_h((uint16_t)(e.x & 0xffff), pk, acc[j][0]);
+            acc[j][1] = fma_h((uint16_t)(e.x >> 16), pk, acc[j][1]);
+            acc[j][2] = fma_h((uint16_t)(e.y & 0xffff), pk, acc[j][2]);
+            acc[j][3] = fma_h((uint16_t)(e.y >> 16), pk, acc[j][3]);
+          }
+        }
+      }
+    }
+    // ---- merge the 16 warps of this span
+    float l_w = l_lane;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) l_w += __shfl_xor_sync(0xffffffffu, l_w, off);
+    float* my = scratch + warp * (C + 2);
+    if (lane == 0) {
+      my[0] = m_w;
+      my[1] = l_w;
+    }
+#pragma unroll
+    for (int j = 0; j < GPL; ++j)
+#pragma unroll
+      for (int i = 0; i < V; ++i) my[2 + (lane + 32 * j) * V + i] = acc[j][i];
+    __syncthreads();
+    const bool whole = (tc0 == 0 && tc1 == a.NT);
+    float* rec = a.part + ((int64_t)bh * a.NT + tc0) * (C + 3);
+    if (tid <= C) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, scratch[w * (C + 2)]);
+      float val = 0.f;
+      for (int w = 0; w < kAttnWarps; ++w) {
+        const float mw = scratch[w * (C + 2)];
+        const float sc = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
+        val += sc * (tid < C ? scratch[w * (C + 2) + 2 + tid] : scratch[w * (C + 2) + 1]);
+      }
+      if (tid < C) {
+        rec[3 + tid] = val;
+      } else {
+        rec[0] = M;
+        rec[1] = val;
+        rec[2] = (float)(tc1 - tc0);
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (whole) {
+      if (tid < C) {
+        const float L = __ldcg(rec + 1);
+        store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, __ldcg(rec + 3 + tid) / L);
+      }
+    } else {
+      if (tid == 0) s_last = (atomicAdd(a.counters + bh, tc1 - tc0) + (tc1 - tc0) == a.NT);
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        if (tid < C) {
+          const float* base = a.part + (int64_t)bh * a.NT * (C + 3);
+          float MM = -INFINITY;
+          for (int tc = 0; tc < a.NT;) {
+            const float* r = base + (int64_t)tc * (C + 3);
+            MM = fmaxf(MM, __ldcg(r));
+            tc += (int)__ldcg(r + 2);
+          }
+          float L = 0.f, A = 0.f;
+          for (int tc = 0; tc < a.NT;) {
+            const float* r = base + (int64_t)tc * (C + 3);
+            const float mi = __ldcg(r);
+            const float sc = (mi == -INFINITY) ? 0.f : fast_exp2(mi - MM);
+            L += sc * __ldcg(r + 1);
+            A += sc * __ldcg(r + 3 + tid);
+            tc += (int)__ldcg(r + 2);
+          }
+          store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, A / L);
+        }
+        if (tid == 0) a.counters[bh] = 0;
+      }
+    }
+    u = span_end;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic path: dense fp32 K/V in the workspace
+
+__global__ void __launch_bounds__(256) attn_dense_kernel(const float* __restrict__ k, const float* __restrict__ v,
+                                                         const void* __restrict__ q, int q_dtype, int T, int C,
+                                                         float* __restrict__ logits, void* __restrict__ out,
+                                                         int out_dtype) {
+  const int bh = blockIdx.x;
+  const float* kb = k + (int64_t)bh * T * C;
+  const float* vb = v + (int64_t)bh * T * C;
+  float* lg = logits + (int64_t)bh * T;
+  __shared__ float red[256];
+  const float inv = 1.0f / sqrtf((float)C);
+  float mx = -INFINITY;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < C; ++c) s = fmaf(load_as_f32(q, q_dtype, (int64_t)bh * C + c), kb[(int64_t)t * C + c], s);
+    s *= inv;
+    lg[t] = s;
+    mx = fmaxf(mx, s);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  mx = red[0];
+  __syncthreads();
+  float sum = 0.f;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const float p = expf(lg[t] - mx);
+    lg[t] = p;
+    sum += p;
+  }
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  sum = red[0];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int t = 0; t < T; ++t) acc = fmaf(lg[t], vb[(int64_t)t * C + c], acc);
+    store_from_f32(out, out_dtype, (int64_t)bh * C + c, acc / sum);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+
+static bool attn_fast_ok(const Geom& gk, const Geom& gv, const VqbTensor* k, const VqbTensor* v, int T,
+                         const VqbLaunch* L) {
+  if (L && (L->flags & VQB_FLAG_FORCE_GENERIC)) return false;
+  if (k->layout != VQB_LAYOUT_KV_IL || v->layout != VQB_LAYOUT_KV_IL) return false;
+  if (k->codebook_dtype != VQB_F16 || v->codebook_dtype != VQB_F16) return false;
+  for (const Geom* g : {&gk, &gv}) {
+    if (g->sharing != VQB_SHARE_CHANNEL_GROUP || g->group_width != g->v || g->R != 1 || g->bits != 8) return false;
+    if (!(g->v == 2 || g->v == 4) || !(g->gpr == 32 || g->gpr == 64)) return false;
+  }
+  if (gk.v != gv.v || T % 32 != 0) return false;
+  return true;
+}
+
+static int64_t a256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH) {
+  Geom g;
+  int s = make_geom(k, &g);
+  if (s) return s;
+  const int64_t T = g.dims[2], C = g.cols;
+  const int64_t NT = ceil_div(T, kAttnChunk);
+  const int64_t fast = a256(BH * 4) + BH * NT * (C + 3) * 4;
+  const int64_t generic = a256(2 * BH * T * C * 4) + BH * T * 4;
+  return std::max(fast, generic);
+}
+
+template <int V, int GPL>
+static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
+  auto kern = attn_cq_kernel<V, GPL>;
+  constexpr size_t smem = AttnSmem<V, GPL>::total;
+  static bool configured[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!configured[dev & 63]) {
+    VQB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[dev & 63] = true;
+  }
+  const int U = a.B * a.H * a.NT;
+  int grid = std::min(U, sm_count());
+  if (grid_limit > 0) grid = std::min(grid, grid_limit);
+  kern<<<grid, kAttnThreads, smem, st>>>(a);
+  VQB_LAUNCH_CHECK("attn_cq_kernel");
+  set_kernel("attn_cq");
+  return VQB_OK;
+}
+
+int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_dtype, int B, int H, int T, int C,
+                  void* out, int out_dtype, const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st,
+                  bool* used_fast) {
+  Geom gk, gv;
+  int s = make_geom(k, &gk);
+  if (s) return s;
+  s = make_geom(v, &gv);
+  if (s) return s;
+  if (gk.ndim != 4 || gv.ndim != 4 || gk.dims[0] != B || gk.dims[1] != H || gk.dims[2] != T || gk.dims[3] != C)
+    return set_error(VQB_ESHAPE, "quantized KV shape does not match op axes (%d, %d, %d, %d)", B, H, T, C);
+  for (int i = 0; i < 4; ++i)
+    if (gv.dims[i] != gk.dims[i]) return set_error(VQB_ESHAPE, "K and V shapes differ");
+  if (q_dtype < VQB_F32 || q_dtype > VQB_BF16 || out_dtype < VQB_F32 || out_dtype > VQB_BF16)
+    return set_error(VQB_ECONFIG, "unknown query/output dtype");
+  const int64_t BH = (int64_t)B * H;
+  const int64_t need = attn_ws_bytes(k, BH);
+  if ((int64_t)ws_bytes < need || !ws)
+    return set_error(VQB_ECAPACITY, "attention workspace too small: %zu < %lld", ws_bytes, (long long)need);
+  const bool fast = attn_fast_ok(gk, gv, k, v, T, L);
+  if (used_fast) *used_fast = fast;
+  if (fast) {
+    AttnArgs a;
+    a.kc = reinterpret_cast<const uint8_t*>(k->d_codes);
+    a.vc = reinterpret_cast<const uint8_t*>(v->d_codes);
+    a.kb = reinterpret_cast<const __half*>(k->d_codebooks);
+    a.vb = reinterpret_cast<const __half*>(v->d_codebooks);
+    a.q = q;
+    a.q_dtype = q_dtype;
+    a.out = out;
+    a.out_dtype = out_dtype;
+    a.counters = reinterpret_cast<int*>(ws);
+    a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + a256(BH * 4));
+    a.B = B;
+    a.H = H;
+    a.T = T;
+    a.NT = (int)ceil_div(T, kAttnChunk);
+    a.scale_log2 = 1.4426950408889634f / sqrtf((float)C);
+    const int gl = L ? L->grid_limit : 0;
+    const int gpl = (int)(gk.gpr / 32);
+    if (gk.v == 2 && gpl == 2) return launch_attn_t<2, 2>(a, st, gl);
+    if (gk.v == 2 && gpl == 1) return launch_attn_t<2, 1>(a, st, gl);
+    if (gk.v == 4 && gpl == 1) return launch_attn_t<4, 1>(a, st, gl);
+    return launch_attn_t<4, 2>(a, st, gl);
+  }
+  float* kd = reinterpret_cast<float*>(ws);
+  float* vd = kd + BH * T * C;
+  float* lg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + a256(2 * BH * T * C * 4));
+  s = launch_dequant(gk, k, kd, VQB_F32, st);
+  if (s) return s;
+  s = launch_dequant(gv, v, vd, VQB_F32, st);
+  if (s) return s;
+  attn_dense_kernel<<<(unsigned)BH, 256, 0, st>>>(kd, vd, q, q_dtype, T, C, lg, out, out_dtype);
+  VQB_LAUNCH_CHECK("attn_dense_kernel");
+  set_kernel("attn_generic");
+  return VQB_OK;
+}
+
+int attn_usage(VqbUsage* u) {
+  cudaFuncAttributes at;
+  auto k = attn_cq_kernel<2, 2>;
+  VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
+  constexpr size_t smem = AttnSmem<2, 2>::total;
+  VQB_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  u->shared_bytes = (int)(at.sharedSizeBytes + smem);
+  u->regs_per_thread = at.numRegs;
+  u->threads_per_block = kAttnThreads;
+  int occ = 0;
+  VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kAttnThreads, smem));
+  u->max_blocks_per_sm = occ;
+  return VQB_OK;
+}
+
+}  // namespace vqb
+
+extern "C" int vqb_attn_decode(const VqbTensor* k, const VqbTensor* v, const void* d_q, int32_t q_dtype, int32_t B,
+                               int32_t H, int32_t T, int32_t C, void* d_out, int32_t out_dtype,
+                               const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
+  return vqb::attn_dispatch(k, v, d_q, q_dtype, B, H, T, C, d_out, out_dtype, launch, d_ws, ws_bytes,
+                            reinterpret_cast<cudaStream_t>(stream), nullptr);
+}

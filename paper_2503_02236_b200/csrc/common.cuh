@@ -1,0 +1,186 @@
+// common.cuh — shared device/host helpers for the B200 VQ kernels.
+//
+// Device-side restatement of the reference's tensor addressing:
+//   * region of a sub-vector   : region_layout (pkg/src/vqforge/codec.py:135-177)
+//   * codebook index           : level * n_regions + region (codec.py:208-209)
+//   * packed code stream       : bitpack.pack_indices, LSB-first (bitpack.py:13-28)
+// computed inline from coordinates instead of materialising int64 temporaries.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/vqb.h"
+
+namespace vqb {
+
+// ---------------------------------------------------------------------------
+// error plumbing (host)
+
+int set_error(int code, const char* fmt, ...);
+int cuda_error(cudaError_t e, const char* what);
+int sm_count();
+void set_kernel(const char* name);
+
+#define VQB_CUDA_CHECK(expr)                            \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return ::vqb::cuda_error(_e, #expr); \
+  } while (0)
+
+#define VQB_LAUNCH_CHECK(what)                               \
+  do {                                                       \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) return ::vqb::cuda_error(_e, what); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// tensor geometry, flattened for kernels (passed by value)
+
+struct Geom {
+  int v;          // vector size
+  int bits;       // log2 entries
+  int R;          // residual levels
+  int K;          // entries per codebook
+  int sharing;
+  int tile_rows, tile_cols, group_width;
+  int ndim;
+  int64_t dims[4];
+  int n_regions;
+  int64_t cols;   // last axis
+  int64_t gpr;    // sub-vectors per row (G)
+  int64_t rows;   // product of leading axes
+  int64_t S;      // sub-vectors per level
+  int layout;
+  int code_bytes; // 1 or 2 for PLAIN / IL layouts
+  int64_t d_H;    // dims[1] of a 4-D tensor (heads)
+  int64_t d_T;    // dims[ndim-2] (tokens of a 4-D tensor, rows of the last 2-D slice)
+};
+
+int make_geom(const VqbTensor* t, Geom* g);  // validates, returns VQB_* status
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Region of sub-vector s (row-major sub-vector order), codec.py:135-177.
+__device__ __forceinline__ int region_of(const Geom& g, int64_t s) {
+  if (g.sharing == VQB_SHARE_WHOLE) return 0;
+  const int64_t row = s / g.gpr;
+  const int64_t col = (s - row * g.gpr) * g.v;
+  if (g.sharing == VQB_SHARE_CHANNEL_GROUP) {
+    const int64_t n_groups = g.cols / g.group_width;
+    const int64_t grp = col / g.group_width;
+    if (g.ndim == 4) {
+      const int64_t head = (row / g.d_T) % g.d_H;
+      return (int)(head * n_groups + grp);
+    }
+    return (int)grp;
+  }
+  // tile sharing over the last two axes, shared across leading axes
+  const int64_t r2 = g.d_T;
+  const int64_t n_tc = ceil_div(g.cols, g.tile_cols);
+  const int64_t local_row = row % r2;
+  return (int)((local_row / g.tile_rows) * n_tc + col / g.tile_cols);
+}
+
+// Offset (in codes) of code (level r, sub-vector s) inside an interleaved layout.
+__device__ __forceinline__ int64_t il_offset(const Geom& g, int r, int64_t s) {
+  if (g.layout == VQB_LAYOUT_GEMV_IL) {
+    const int rpl = 16 / g.code_bytes;
+    const int64_t m = s / g.gpr, grp = s - (s / g.gpr) * g.gpr;
+    return (int64_t)r * g.S + ((m / rpl) * g.gpr + grp) * rpl + (m % rpl);
+  }
+  // KV_IL: per (b,h) block of T tokens: [T/TPL][32][TPL][GPL]
+  const int64_t T = g.d_T;
+  const int gpl = (int)(g.gpr / 32);
+  const int tpl = 16 / gpl;
+  const int64_t row = s / g.gpr, grp = s - (s / g.gpr) * g.gpr;
+  const int64_t bh = row / T, t = row - (row / T) * T;
+  const int64_t lane = grp % 32, j = grp / 32;
+  return (int64_t)r * g.S + bh * T * g.gpr +
+         (((t / tpl) * 32 + lane) * tpl + (t % tpl)) * gpl + j;
+}
+
+// Code of level r for sub-vector s, from any layout.
+__device__ __forceinline__ uint32_t code_at(const Geom& g, const void* codes, int r, int64_t s) {
+  if (g.layout == VQB_LAYOUT_PACKED) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(codes);
+    const int64_t bit = ((int64_t)r * g.S + s) * g.bits;
+    const int64_t wi = bit >> 5;
+    const int sh = (int)(bit & 31);
+    uint32_t lo = __ldg(w + wi);
+    uint32_t val = lo >> sh;
+    if (sh + g.bits > 32) val |= __ldg(w + wi + 1) << (32 - sh);
+    return val & ((1u << g.bits) - 1u);
+  }
+  int64_t off = (g.layout == VQB_LAYOUT_PLAIN) ? (int64_t)r * g.S + s : il_offset(g, r, s);
+  if (g.code_bytes == 1) return __ldg(reinterpret_cast<const uint8_t*>(codes) + off);
+  return __ldg(reinterpret_cast<const uint16_t*>(codes) + off);
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T x);
+template <>
+__device__ __forceinline__ float to_f32<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half x) { return __half2float(x); }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+__device__ __forceinline__ float load_as_f32(const void* p, int dtype, int64_t i) {
+  if (dtype == VQB_F32) return __ldg(reinterpret_cast<const float*>(p) + i);
+  if (dtype == VQB_F16) return __half2float(reinterpret_cast<const __half*>(p)[i]);
+  return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+}
+
+__device__ __forceinline__ void store_from_f32(void* p, int dtype, int64_t i, float v) {
+  if (dtype == VQB_F32) reinterpret_cast<float*>(p)[i] = v;
+  else if (dtype == VQB_F16) reinterpret_cast<__half*>(p)[i] = __float2half_rn(v);
+  else reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+}
+
+// fp32 += fp16 * fp16, single rounding (sm_100 FHFMA): products of two halves are
+// exact in fp32, so this is an fp32 FMA on exactly-widened operands.
+__device__ __forceinline__ float fma_h(uint16_t a, uint16_t b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+}  // namespace vqb

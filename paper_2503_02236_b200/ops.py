@@ -1,0 +1,128 @@
+"""Functional torch-facing entry points: vq_dequantize / vq_gemv / vq_gemm / vq_attention.
+
+Every call goes straight to the C ABI (include/vqb.h) on the tensor's device and
+the current CUDA stream; nothing here computes on the host. Shapes follow the
+reference: weights W (M, N) with y = x @ W (pkg/src/vqforge/sim.py:136-144);
+attention q (B, H, C) with K, V (B, H, T, C) (sim.py:145-155).
+"""
+
+import threading
+
+import torch
+
+from . import _native as N
+from .device import DeviceVQTensor, dtype_enum, torch_dtype
+from .errors import ConfigError, ShapeError
+
+# -- workspace arena ----------------------------------------------------------------------------
+# One zero-initialised byte buffer per (device, stream). The kernels keep split
+# arrival counters in its head and reset them themselves, so it is zeroed only
+# when (re)allocated.
+
+_ws = {}
+_ws_lock = threading.Lock()
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    stream = torch.cuda.current_stream(device).cuda_stream
+    key = (device.index, stream)
+    with _ws_lock:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            size = max(int(nbytes), 1 << 20)
+            if buf is not None:
+                size = max(size, 2 * buf.numel())
+            buf = torch.zeros(size, dtype=torch.uint8, device=device)
+            _ws[key] = buf
+        return buf
+
+
+def launch_struct(plans=None, n_shared=None, split_factor=None, split_axis=None, force_generic=False,
+                  grid_limit=0) -> N.VqbLaunch:
+    """VqbLaunch from FusedPlans (sim.py:229-236) and/or explicit knobs."""
+    L = N.VqbLaunch()
+    if plans is not None:
+        cp, fp = plans.cache_plan, plans.dataflow_plan
+        L.n_reg = int(cp.n_reg)
+        L.n_shared = int(cp.n_shared)
+        L.split_axis = ord(fp.split_axis) if fp.split_axis else 0
+        L.split_factor = int(fp.split_factor)
+        L.fusion_level = 0 if plans.fusion_level == "register" else 1
+    if n_shared is not None:
+        L.n_shared = int(n_shared)
+    if split_factor is not None:
+        L.split_factor = int(split_factor)
+    if split_axis is not None:
+        L.split_axis = ord(split_axis) if split_axis else 0
+    if force_generic:
+        L.flags |= N.FLAG_FORCE_GENERIC
+    L.grid_limit = int(grid_limit)
+    return L
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def vq_dequantize(w: DeviceVQTensor, out_dtype=None) -> torch.Tensor:
+    """Dense reconstruction (codec.py:391-408); fp32 output is bit-exact."""
+    dt = torch_dtype(out_dtype or torch.float32)
+    out = torch.empty(w.shape, dtype=dt, device=w.device)
+    N.check(N.lib().vqb_dequant(w.struct(), out.data_ptr(), dtype_enum(dt), _stream(w.device)))
+    return out
+
+
+def _matmul(kind: int, w: DeviceVQTensor, x: torch.Tensor, out_dtype, launch) -> torch.Tensor:
+    if len(w.shape) != 2:
+        raise ShapeError(f"quantized weight must be 2-D, got {w.shape}")
+    m, n = w.shape
+    squeeze = x.dim() == 1
+    x2 = x.reshape(1, -1) if squeeze else x
+    if x2.dim() != 2 or x2.shape[1] != m:
+        raise ShapeError(f"activation {tuple(x.shape)} does not match M={m}")
+    if x2.device != w.device:
+        raise ConfigError(f"activation on {x2.device}, weight on {w.device}")
+    x2 = x2.contiguous()
+    rows = x2.shape[0]
+    od = torch_dtype(out_dtype or torch.float32)
+    y = torch.empty((rows, n), dtype=od, device=w.device)
+    L = launch if launch is not None else N.VqbLaunch()
+    lib = N.lib()
+    s = w.struct()
+    need = N.check(lib.vqb_workspace_bytes(kind, s, rows, L))
+    ws = workspace(need, w.device)
+    fn = lib.vqb_gemv if kind == N.KERNEL_GEMV else lib.vqb_gemm
+    N.check(fn(s, x2.data_ptr(), dtype_enum(x2.dtype), rows, y.data_ptr(), dtype_enum(od), L,
+               ws.data_ptr(), ws.numel(), _stream(w.device)))
+    return y[0] if squeeze else y
+
+
+def vq_gemv(w: DeviceVQTensor, x: torch.Tensor, out_dtype=None, launch=None) -> torch.Tensor:
+    """Decode GEMV y = x @ dequant(W) for x of shape (M,) or (rows<=8, M)."""
+    return _matmul(N.KERNEL_GEMV, w, x, out_dtype, launch)
+
+
+def vq_gemm(w: DeviceVQTensor, x: torch.Tensor, out_dtype=None, launch=None) -> torch.Tensor:
+    """Prefill GEMM y = X @ dequant(W) for X of shape (rows, M)."""
+    return _matmul(N.KERNEL_GEMM, w, x, out_dtype, launch)
+
+
+def vq_attention(k: DeviceVQTensor, v: DeviceVQTensor, q: torch.Tensor, out_dtype=None,
+                 launch=None) -> torch.Tensor:
+    """Decode attention softmax(q K^T / sqrt(C)) V over a VQ KV cache, q (B, H, C)."""
+    if len(k.shape) != 4:
+        raise ShapeError(f"quantized K must be (B, H, T, C), got {k.shape}")
+    b, h, t, c = k.shape
+    if tuple(q.shape) != (b, h, c):
+        raise ShapeError(f"query shape {tuple(q.shape)} != {(b, h, c)}")
+    q = q.contiguous()
+    od = torch_dtype(out_dtype or torch.float32)
+    out = torch.empty((b, h, c), dtype=od, device=k.device)
+    L = launch if launch is not None else N.VqbLaunch()
+    lib = N.lib()
+    ks, vs = k.struct(), v.struct()
+    need = N.check(lib.vqb_workspace_bytes(N.KERNEL_ATTN, ks, b * h, L))
+    ws = workspace(need, k.device)
+    N.check(lib.vqb_attn_decode(ks, vs, q.data_ptr(), dtype_enum(q.dtype), b, h, t, c, out.data_ptr(),
+                                dtype_enum(od), L, ws.data_ptr(), ws.numel(), _stream(k.device)))
+    return out

@@ -1,0 +1,89 @@
+"""Graph-captured execution of a stack of fused VQ GEMVs (a decode step's linears).
+
+``VQLinearStack`` is the public API a serving loop (and bench.py's end-to-end
+leg) calls: it owns the quantized weights, device input/output buffers and one
+CUDA graph that replays every GEMV of the stack, so a decode step costs one
+graph launch instead of one Python->C-ABI round trip per layer.
+"""
+
+import torch
+
+from . import _native as N
+from .device import DeviceVQTensor, dtype_enum
+from .ops import launch_struct, workspace
+
+
+class VQLinearStack:
+    def __init__(self, weights, rows: int = 1, act_dtype=torch.float16, out_dtype=torch.float16,
+                 launches=None):
+        self.weights = list(weights)
+        if not self.weights:
+            raise ValueError("empty stack")
+        self.device = self.weights[0].device
+        self.rows = rows
+        self.act_dtype, self.out_dtype = act_dtype, out_dtype
+        self.launches = list(launches) if launches else [launch_struct() for _ in self.weights]
+        ins = [w.shape[0] for w in self.weights]
+        outs = [w.shape[1] for w in self.weights]
+        self.in_off = [0]
+        for m in ins:
+            self.in_off.append(self.in_off[-1] + rows * m)
+        self.out_off = [0]
+        for n in outs:
+            self.out_off.append(self.out_off[-1] + rows * n)
+        self.x = torch.zeros(self.in_off[-1], dtype=act_dtype, device=self.device)
+        self.y = torch.zeros(self.out_off[-1], dtype=out_dtype, device=self.device)
+        self._structs = [w.struct() for w in self.weights]
+        lib = N.lib()
+        need = max(N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMV, s, rows, L))
+                   for s, L in zip(self._structs, self.launches))
+        self._ws = workspace(need, self.device)
+        self._graph = None
+
+    @property
+    def n_launches(self) -> int:
+        return len(self.weights)
+
+    def input_view(self, i: int) -> torch.Tensor:
+        return self.x[self.in_off[i]:self.in_off[i + 1]].view(self.rows, -1)
+
+    def output_view(self, i: int) -> torch.Tensor:
+        return self.y[self.out_off[i]:self.out_off[i + 1]].view(self.rows, -1)
+
+    def launch_all(self) -> None:
+        """Enqueue every GEMV on the current stream (no host sync)."""
+        lib = N.lib()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        xd, yd = dtype_enum(self.act_dtype), dtype_enum(self.out_dtype)
+        esz_x, esz_y = self.x.element_size(), self.y.element_size()
+        xb, yb = self.x.data_ptr(), self.y.data_ptr()
+        ws, wsn = self._ws.data_ptr(), self._ws.numel()
+        for i, (s, L) in enumerate(zip(self._structs, self.launches)):
+            N.check(lib.vqb_gemv(s, xb + self.in_off[i] * esz_x, xd, self.rows,
+                                 yb + self.out_off[i] * esz_y, yd, L, ws, wsn, stream))
+
+    def capture(self) -> None:
+        """Record launch_all() into a CUDA graph (after one eager warm-up)."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.launch_all()
+            # the side stream needs its own workspace: rebind to the graph stream's arena
+            self._ws = workspace(self._ws.numel(), self.device)
+            self.launch_all()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.launch_all()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self._graph = g
+
+    def replay(self) -> None:
+        if self._graph is None:
+            self.capture()
+        self._graph.replay()
+
+    def run(self, host_x: torch.Tensor, host_y: torch.Tensor) -> None:
+        """End to end: pinned host inputs -> GPU stack -> pinned host outputs."""
+        self.x.copy_(host_x, non_blocking=True)
+        self.replay()
+        host_y.copy_(self.y, non_blocking=True)

@@ -1,0 +1,256 @@
+"""Parity of the CUDA kernels (through the C ABI) against the CPU oracle and the
+reference's golden vectors. Bit-exact for dequantization; the fused ops within
+the stated tolerances:
+
+  * fp32 codebooks + fp32 activations (parity mode, generic kernel): 1e-4
+    rel-to-max — the reference's own contract (verify.py:212-213)
+  * fp16 codebooks + fp16 activations, fp32 accumulation (fast kernels): 1e-3
+    against the oracle run on the same fp16-rounded inputs
+  * attention with fp16 probabilities in the V accumulation: 2e-3
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+from conftest import ATTENTION_CASES, CASES, MATMUL_CASES, Case, O
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL_PARITY = 1e-4
+TOL_F16 = 1e-3
+TOL_ATTN = 2e-3
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda", 0)
+
+
+def _mods():
+    from paper_2503_02236_b200 import _native as N
+    from paper_2503_02236_b200.device import DeviceVQTensor
+    from paper_2503_02236_b200 import ops
+    return N, DeviceVQTensor, ops
+
+
+# ---- dequantization: bit-exact -----------------------------------------------------------------
+
+@pytest.mark.parametrize("layout", ["plain", "packed", "auto"])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_dequant_bit_exact_fp32(name, layout, dev, meta):
+    N, DeviceVQTensor, ops = _mods()
+    c = Case(name)
+    q = c.quantized()
+    if layout == "packed":
+        d = DeviceVQTensor.from_packed(q.packed_codes(), q.shape, q.config, q.codebooks, device=dev,
+                                       codebook_dtype="float32")
+    else:
+        d = DeviceVQTensor.from_quantized(q, device=dev, codebook_dtype="float32", layout=layout)
+    out = ops.vq_dequantize(d).cpu().numpy()
+    assert N.last_kernel() == "dequant"
+    assert sha(out) == meta["dequant"][name]["dequant_sha"]
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_dequant_fp16_books_and_casts(name, dev, meta):
+    N, DeviceVQTensor, ops = _mods()
+    c = Case(name, books_f16=True)
+    d = DeviceVQTensor.from_quantized(c.quantized(), device=dev, codebook_dtype="float16")
+    out = ops.vq_dequantize(d).cpu().numpy()
+    assert sha(out) == meta["dequant"][name]["dequant16_sha"]
+    ref = c.dense()
+    h = ops.vq_dequantize(d, out_dtype=torch.float16).cpu()
+    assert torch.equal(h, torch.from_numpy(ref).half())
+    b = ops.vq_dequantize(d, out_dtype=torch.bfloat16).cpu()
+    assert torch.equal(b, torch.from_numpy(ref).bfloat16())
+
+
+def test_dequant_module_api_matches_reference(meta):
+    from paper_2503_02236_b200.codec import dequantize
+    c = Case("aqlm3")
+    out = dequantize(c.quantized())
+    assert isinstance(out, np.ndarray) and out.dtype == np.float32
+    assert sha(out) == meta["dequant"]["aqlm3"]["dequant_sha"]
+
+
+def test_dequant_code_out_of_range(dev):
+    from paper_2503_02236_b200.errors import CodeRangeError
+    _, DeviceVQTensor, _ = _mods()
+    c = Case("cq2")
+    q = c.quantized()
+    q.codes[0, 3] = q.config.n_entries + 7
+    with pytest.raises(CodeRangeError, match="code out of range"):
+        DeviceVQTensor.from_quantized(q, device=dev)
+
+
+def test_dequant_negative_zero(dev):
+    from paper_2503_02236_b200.codec import Codebook, QuantizedTensor, VQConfig
+    _, DeviceVQTensor, ops = _mods()
+    books = [Codebook(np.array([[-0.0, 1.0], [2.0, -0.0]], np.float32), 0, 0),
+             Codebook(np.array([[-0.0, -0.0], [0.5, -0.0]], np.float32), 1, 0)]
+    q = QuantizedTensor(np.array([[0, 1], [0, 0]], np.int32), (1, 4), VQConfig(2, 1, 2), books, 1)
+    out = ops.vq_dequantize(DeviceVQTensor.from_quantized(q, device=dev, codebook_dtype="float32"))
+    assert not torch.signbit(out).any()
+
+
+# ---- fused GEMV / GEMM ----------------------------------------------------------------------------
+
+def _act(c, kind, extra):
+    m = c.shape[0]
+    return O.synthetic_tensor((m,) if kind == "gemv" else (extra["rows"], m), c.seed + 2)
+
+
+@pytest.mark.parametrize("name,base,kind,extra", MATMUL_CASES)
+def test_matmul_parity_mode(name, base, kind, extra, dev, arrays):
+    """fp32 books + fp32 activations: within the reference's 1e-4 of its own golden output."""
+    N, DeviceVQTensor, ops = _mods()
+    c = Case(base)
+    d = DeviceVQTensor.from_quantized(c.quantized(), device=dev, codebook_dtype="float32")
+    a = torch.from_numpy(_act(c, kind, extra)).to(dev)
+    fn = ops.vq_gemv if kind == "gemv" else ops.vq_gemm
+    y = fn(d, a).cpu().numpy()
+    assert O.rel_err(y, arrays[f"mm_ref_{name}"]) <= TOL_PARITY
+
+
+def _big_weight(shape, v, bits, r, sharing="whole", tile=(0, 0), work=None, seed=0):
+    nreg = O.n_regions_of(shape, v, sharing, tile)
+    codes, books = O.synthetic_codes_books(shape, v, bits, r, nreg, seed, working_entries=work)
+    books = O.round_f16(books)
+    dense = O.dequantize(codes, books, shape, v, nreg, O.region_ids(shape, v, sharing, tile))
+    return codes, books, nreg, dense
+
+
+def _qt(codes, books, nreg, shape, cfg):
+    from paper_2503_02236_b200.codec import Codebook, QuantizedTensor
+    cbs = [Codebook(books[i], i // nreg, i % nreg) for i in range(books.shape[0])]
+    return QuantizedTensor(codes, shape, cfg, cbs, nreg)
+
+
+FAST_GEMV = [
+    # (label, shape, v, bits, R, sharing, tile, working set)
+    ("C2_quip2_q_proj", (4096, 4096), 8, 16, 1, "whole", (0, 0), 256),
+    ("C1_gptvq2_q_proj", (4096, 4096), 4, 8, 1, "tile", (256, 256), None),
+    ("C3_aqlm2x8", (4096, 2048), 8, 8, 2, "whole", (0, 0), None),
+    ("C2_quip2_down", (11008, 1024), 8, 16, 1, "whole", (0, 0), 256),
+    ("quip2_full_table", (512, 1024), 8, 16, 1, "whole", (0, 0), None),  # global tier hits
+]
+
+
+@pytest.mark.parametrize("rows", [1, 2, 4, 8])
+@pytest.mark.parametrize("label,shape,v,bits,r,sharing,tile,work", FAST_GEMV)
+def test_gemv_fast_kernel(label, shape, v, bits, r, sharing, tile, work, rows, dev):
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    sh = Sharing.per_tile(*tile) if sharing == "tile" else Sharing.whole_tensor()
+    cfg = VQConfig(v, bits, r, sh)
+    codes, books, nreg, dense = _big_weight(shape, v, bits, r, sharing, tile, work)
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev)
+    assert d.layout == "gemv"
+    x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))
+    y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half())
+    assert N.last_kernel() == "gemv_fast"
+    ref = O.matmul_ref(x, dense)
+    assert O.rel_err(y.cpu().numpy(), ref) <= TOL_F16
+    # second launch reuses the self-reset split counters
+    y2 = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half())
+    assert torch.equal(y, y2), "split reduction must be deterministic"
+
+
+def test_gemv_fast_fp16_output_and_plans(dev):
+    from paper_2503_02236_b200.codec import VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    shape = (2048, 2048)
+    codes, books, nreg, dense = _big_weight(shape, 8, 16, 1, work=256, seed=3)
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, VQConfig(8, 16, 1)), device=dev)
+    x = O.round_f16(O.synthetic_tensor((shape[0],), 9))
+    xt = torch.from_numpy(x).to(dev).half()
+    ref = O.matmul_ref(x, dense)
+    for f in (1, 2, 8):
+        for n_sh in (0, 64, 256, 1024):
+            L = ops.launch_struct(n_shared=n_sh if n_sh else None, split_factor=f, split_axis="M")
+            y = ops.vq_gemv(d, xt, out_dtype=torch.float16, launch=L)
+            assert N.last_kernel() == "gemv_fast"
+            assert O.rel_err(y.float().cpu().numpy(), ref) <= 2e-3, (f, n_sh)
+
+
+# ---- attention ------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,base", ATTENTION_CASES)
+def test_attention_parity_mode(name, base, dev, arrays):
+    N, DeviceVQTensor, ops = _mods()
+    k, v = Case(base), Case(base, seed_offset=1)
+    kd = DeviceVQTensor.from_quantized(k.quantized(), device=dev, codebook_dtype="float32")
+    vd = DeviceVQTensor.from_quantized(v.quantized(), device=dev, codebook_dtype="float32")
+    b, h, t, c = k.shape
+    q = torch.from_numpy(O.synthetic_tensor((b, h, c), k.seed + 2)).to(dev)
+    out = ops.vq_attention(kd, vd, q).cpu().numpy()
+    assert N.last_kernel() == "attn_generic"
+    assert O.rel_err(out, arrays[f"at_ref_{name}"]) <= TOL_PARITY
+
+
+ATTN_SHAPES = [
+    # (v, gw, shape): CQ-4 / CQ-2 at several contexts, incl. multi-chunk splits
+    (2, 2, (2, 4, 64, 128)),
+    (2, 2, (2, 3, 4096, 128)),
+    (2, 2, (1, 2, 1000 // 32 * 32, 128)),
+    (4, 4, (2, 4, 512, 128)),
+    (4, 4, (3, 2, 2048, 128)),
+    (2, 2, (2, 2, 256, 64)),
+]
+
+
+@pytest.mark.parametrize("v,gw,shape", ATTN_SHAPES)
+def test_attention_fast_kernel(v, gw, shape, dev):
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    cfg = VQConfig(v, 8, 1, Sharing.per_channel_group(gw))
+    nreg = O.n_regions_of(shape, v, "channel_group", group_width=gw)
+    regs = O.region_ids(shape, v, "channel_group", group_width=gw)
+    dense = []
+    devs = []
+    for s in (11, 12):
+        codes, books = O.synthetic_codes_books(shape, v, 8, 1, nreg, s)
+        books = O.round_f16(books)
+        dense.append(O.dequantize(codes, books, shape, v, nreg, regs))
+        devs.append(DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev))
+    assert devs[0].layout == "kv"
+    b, h, t, c = shape
+    q = O.synthetic_tensor((b, h, c), 13)
+    ref = O.attention_ref(q, dense[0], dense[1])
+    for grid in (0, 7):
+        L = ops.launch_struct(grid_limit=grid)
+        out = ops.vq_attention(devs[0], devs[1], torch.from_numpy(q).to(dev), launch=L)
+        assert N.last_kernel() == "attn_cq"
+        assert O.rel_err(out.cpu().numpy(), ref) <= TOL_ATTN, grid
+
+
+def test_attention_known_answer_single_token(dev):
+    """T = 1 (generic path): the output is the V row (T/test_sim.py:91-98)."""
+    from paper_2503_02236_b200.codec import Codebook, QuantizedTensor, Sharing, VQConfig
+    _, DeviceVQTensor, ops = _mods()
+    cfg = VQConfig(2, 1, 1, Sharing.per_channel_group(2))
+    kb = [Codebook(np.ones((2, 2), np.float32), 0, g) for g in range(2)]
+    vb = [Codebook(np.array([[0, 1], [2, 3]], np.float32) + 4 * g, 0, g) for g in range(2)]
+    codes = np.zeros((1, 2), np.int32)
+    kq = QuantizedTensor(codes, (1, 1, 1, 4), cfg, kb, 2)
+    vq = QuantizedTensor(codes, (1, 1, 1, 4), cfg, vb, 2)
+    out = ops.vq_attention(DeviceVQTensor.from_quantized(kq, device=dev, codebook_dtype="float32"),
+                           DeviceVQTensor.from_quantized(vq, device=dev, codebook_dtype="float32"),
+                           torch.ones((1, 1, 4), device=dev))
+    assert torch.allclose(out.cpu()[0, 0], torch.tensor([0.0, 1.0, 4.0, 5.0]))
+
+
+def test_shape_errors(dev):
+    from paper_2503_02236_b200.errors import ShapeError
+    N, DeviceVQTensor, ops = _mods()
+    c = Case("quip2")
+    d = DeviceVQTensor.from_quantized(c.quantized(), device=dev)
+    with pytest.raises(ShapeError):
+        ops.vq_gemv(d, torch.zeros(c.shape[0] + 1, device=dev, dtype=torch.float16))
