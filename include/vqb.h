@@ -96,6 +96,8 @@ typedef struct VqbTensor {
   int64_t codes_bytes;  /* allocated bytes behind d_codes (bounds check) */
   int32_t codebook_dtype;   /* VQB_F32 / VQB_F16 / VQB_BF16 */
   const void* d_codebooks;  /* (R*n_regions, K, v) contiguous, level-major (codec.py:208-209) */
+  int32_t max_code;         /* largest code in the stream if known (from the upload-time range
+                               check / profiling), else -1; lets a kernel drop its global tier */
 } VqbTensor;
 
 /* Launch knobs from the planner (FusedPlans, sim.py:229-236). Zero-initialise
@@ -111,6 +113,8 @@ typedef struct VqbLaunch {
 } VqbLaunch;
 
 #define VQB_FLAG_FORCE_GENERIC 1 /* use the generic (any-config) kernel */
+#define VQB_FLAG_NO_SHARED 2     /* no shared-memory tier: every lookup from global/L2 ("GC") */
+#define VQB_FLAG_NO_PDL 4        /* launch without programmatic dependent launch */
 
 /* Kernel resource usage (KernelUsage, gpumodel.py:30-36) measured with
  * cudaFuncGetAttributes on the loaded cubin. */
@@ -138,6 +142,10 @@ const char* vqb_last_kernel(void);
  * fp16/bf16 outputs are RN-even casts of that fp32 value. */
 int vqb_dequant(const VqbTensor* t, void* d_out, int32_t out_dtype, void* stream);
 
+/* Workspace bytes a fused call needs. The first VQB_WS_COUNTER_BYTES of every
+ * workspace hold split-arrival counters: zero them once when the workspace is
+ * allocated; kernels reset them after use and never write anything else there. */
+#define VQB_WS_COUNTER_BYTES 65536
 /* Workspace bytes a fused call needs (split partials + arrival counters).
  * kind = VQB_KERNEL_*; rows = batch rows (GEMV/GEMM) or B*H (attention). */
 int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t rows,

@@ -55,6 +55,7 @@ class VqbTensor(ctypes.Structure):
         ("codes_bytes", ctypes.c_int64),
         ("codebook_dtype", ctypes.c_int32),
         ("d_codebooks", ctypes.c_void_p),
+        ("max_code", ctypes.c_int32),
     ]
 
 

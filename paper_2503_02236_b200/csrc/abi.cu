@@ -126,9 +126,8 @@ int make_geom(const VqbTensor* t, Geom* g) {
       if (g->bits > 8) return set_error(VQB_ECONFIG, "KV_IL layout needs codes of at most 8 bits");
       if (g->gpr != 32 && g->gpr != 64)
         return set_error(VQB_ESHAPE, "KV_IL layout needs C/v in {32, 64}, got %lld", (long long)g->gpr);
-      const int tpl = 16 / (int)(g->gpr / 32);
-      if (g->dims[2] % tpl != 0)
-        return set_error(VQB_ESHAPE, "KV_IL layout needs T %% %d == 0, got T=%lld", tpl, (long long)g->dims[2]);
+      if (g->dims[2] % 32 != 0)
+        return set_error(VQB_ESHAPE, "KV_IL layout needs T %% 32 == 0, got T=%lld", (long long)g->dims[2]);
       need = (int64_t)g->R * g->S;
       break;
     }

@@ -6,22 +6,25 @@
 //   logits = (q . K_t) / sqrt(C); p = softmax(logits); out = sum_t p_t V_t.
 //
 // Fast kernel (channel-group sharing with group_width == v, one residual level,
-// u8 codes, fp16 codebooks, KV_IL layout, C/v in {32, 64}):
-//  * codebook-centric dataflow: work units (h, b, T-chunk) are ordered head-major
-//    and dealt out as contiguous ranges to persistent CTAs, so a CTA loads the K
-//    and V codebooks of a head once (CQ books are per head and shared by all
-//    batch rows and tokens, codec.py:161-165) and reuses them across batch rows.
-//  * K side as a lookup table: the query is fixed per (b, h), so the CTA builds
+// u8 codes, fp16 codebooks, KV_IL layout, C/v in {32, 64}, T % 32 == 0):
+//  * codebook-centric dataflow: work units (h, b, 512-token chunk) are ordered
+//    head-major and dealt out as contiguous ranges to persistent CTAs (one per
+//    SM), so a CTA loads the K and V codebooks of a head once (CQ books are per
+//    head, shared by all batch rows and tokens, codec.py:161-165) and reuses
+//    them for every batch row of that head.
+//  * K side as a lookup table: q is fixed per (b, h), so the CTA builds
 //    LUT[e][g] = log2(e)/sqrt(C) * <q_g, K_book_g[e]> once per (b, h); a token's
-//    logit is then sum_g LUT[code_g][g] — one conflict-free LDS.32 + FADD per
-//    code instead of a dequantise-and-dot.
-//  * bank-conflict-free layouts by construction: lane l owns channel groups
-//    g = l + 32j; both the LUT and the V codebook are stored [entry][group] so
-//    lane l always hits bank (l mod 32) whatever its code is.
-//  * per-lane partial logits are reduced across the warp with a 31-shuffle
-//    transpose-reduction that leaves lane l holding token l's logit; softmax is
-//    online (flash-decode) in the exp2 domain; V is dequantised in registers and
-//    fused into fp32 accumulators with fma.rn.f32.f16.
+//    logit is sum_g LUT[code_g][g]: one LDS.32 + FADD per code, no dequantise.
+//  * bank-conflict-free by construction: lane l owns channel groups g = l + 32j;
+//    the LUT and the V book are stored [entry][group], so lane l always hits bank
+//    (l mod 32) whatever its code is. With a 256-byte row the shared address is
+//    a single PRMT of the code byte and the lane's column (plus the region base).
+//  * select-free logit reduction: the KV_IL layout stores token (i ^ l) in lane
+//    l's slot i, so the 32x32 transpose-reduction across the warp is 31
+//    shuffle+add pairs with no selects, leaving lane l with token l's logit.
+//  * online softmax (flash-decode) in the exp2 domain; V is dequantised in
+//    registers and fused into fp32 accumulators with fma.rn.f32.f16.
+//  * the next 32-token batch's codes are loaded while the current one computes.
 //  * split-T partials (m, l, acc) per contiguous span are merged by the last
 //    arriving CTA in fixed T order (deterministic), like the reference's split
 //    reduction (sim.py:604-620).
@@ -35,7 +38,7 @@ namespace vqb {
 
 int launch_dequant(const Geom& g, const VqbTensor* t, void* out, int out_dtype, cudaStream_t st);
 
-constexpr int kAttnWarps = 16;
+constexpr int kAttnWarps = 12;  // 12 x 32 threads leave 168 registers for the double-buffered code stream
 constexpr int kAttnThreads = kAttnWarps * 32;
 constexpr int kAttnChunk = 512;  // tokens per work unit
 
@@ -58,10 +61,14 @@ template <int V, int GPL>
 struct AttnSmem {
   static constexpr int G = 32 * GPL;
   static constexpr int C = G * V;
-  static constexpr size_t book_bytes = 256 * (size_t)C * 2;   // [256][G] x V halves
-  static constexpr size_t lut_bytes = 256 * (size_t)G * 4;    // [256][G] fp32
-  static constexpr size_t scratch_bytes = (size_t)kAttnWarps * (C + 2) * 4;
-  static constexpr size_t total = 2 * book_bytes + lut_bytes + scratch_bytes;
+  static constexpr int EPB = 2 * V;                        // fp16 entry bytes
+  static constexpr size_t region = 65536;                  // 64 KB-aligned regions
+  static constexpr size_t lut_off = 0;                     // [256][G] fp32
+  static constexpr size_t vbook_off = region;              // [256][G] x V halves
+  static constexpr size_t kbook_off = 2 * region;          // [256][G] x V halves
+  static constexpr size_t scratch_off = 3 * region;        // warps x (C + 2) fp32
+  static constexpr size_t total = scratch_off + ((size_t)kAttnWarps * (C + 2) + C + 1) * 4 + 16;
+  static_assert(256 * G * 4 <= region && 256 * G * EPB <= region, "region overflow");
 };
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -70,29 +77,153 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// Shared address of row `code` (byte k of `w`) in a table with ROWB-byte rows,
+// at column `col` of a region starting at `base`. With 256-byte rows and a
+// 64 KB-aligned base this is ONE prmt: [col, code, base>>16 (2 bytes)].
+template <int ROWB, bool PRMT>
+__device__ __forceinline__ uint32_t row_addr(uint32_t w, int k, uint32_t colbase, uint32_t col, uint32_t base) {
+  if constexpr (PRMT && ROWB == 256) {
+    return prmt(w, colbase, 0x7604u | ((uint32_t)k << 4));
+  } else {
+    const uint32_t code = (w >> (8 * k)) & 0xffu;
+    return base + code * ROWB + col;
+  }
+}
+
+template <int V, int GPL, bool PRMT>
+__device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int tok0, int tok1, uint32_t lut_base,
+                                                 uint32_t vbook_base, float& m_w, float& l_lane,
+                                                 float (&acc)[GPL][V]) {
+  using SM = AttnSmem<V, GPL>;
+  constexpr int G = SM::G, EPB = SM::EPB;
+  constexpr int Q = 2 * GPL;  // 16-byte loads per lane per 32-token batch
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t TG = (int64_t)a.T * G;
+  const uint8_t* kbase = a.kc + (int64_t)bh * TG;
+  const uint8_t* vbase = a.vc + (int64_t)bh * TG;
+  // per-lane columns (and, for the single-prmt form, the region's high address bytes)
+  uint32_t colK[GPL], colV[GPL], cbK[GPL], cbV[GPL];
+#pragma unroll
+  for (int j = 0; j < GPL; ++j) {
+    colK[j] = (uint32_t)(lane + 32 * j) * 4;
+    colV[j] = (uint32_t)(lane + 32 * j) * EPB;
+    cbK[j] = (lut_base & 0xffff0000u) | colK[j];
+    cbV[j] = (vbook_base & 0xffff0000u) | colV[j];
+  }
+  auto load = [&](uint4 (&kc)[Q], uint4 (&vc)[Q], int t0) {
+    const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      kc[q] = ldg_stream(kbase + off + q * 512);
+      vc[q] = ldg_stream(vbase + off + q * 512);
+    }
+  };
+  auto batch = [&](const uint4 (&kc)[Q], const uint4 (&vc)[Q]) {
+    // K phase: lane partial logits for the 32 slots (slot i = token i ^ lane)
+    auto partial = [&](int i) {
+      float acc_s = 0.f;
+#pragma unroll
+      for (int j = 0; j < GPL; ++j) {
+        const int byte = i * GPL + j;
+        const uint32_t w = (&kc[byte / 16].x)[(byte % 16) / 4];
+        const float lv = lds_f32(row_addr<G * 4, PRMT>(w, byte % 4, cbK[j], colK[j], lut_base));
+        acc_s = (j == 0) ? lv : acc_s + lv;
+      }
+      return acc_s;
+    };
+    // select-free transpose-reduction: afterwards s[0] on lane l is token l's logit.
+    // The first (offset 16) step is fused into the partial computation so only 16
+    // partial logits are ever live.
+    float s[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float lo = partial(i), hi = partial(i + 16);
+      s[i] = lo + __shfl_xor_sync(0xffffffffu, hi, 16);
+    }
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < off; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i + off], off);
+    const float z = s[0];
+    float mb = z;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
+    const float m_new = fmaxf(m_w, mb);
+    const float corr = fast_exp2(m_w - m_new);
+    const float p = fast_exp2(z - m_new);
+    l_lane = l_lane * corr + p;
+    m_w = m_new;
+#pragma unroll
+    for (int j = 0; j < GPL; ++j)
+#pragma unroll
+      for (int c = 0; c < V; ++c) acc[j][c] *= corr;
+    const uint32_t ph = (uint32_t)__half_as_ushort(__float2half_rn(p));
+    // V phase: slot i holds token i ^ lane, whose probability lives on that lane
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const uint16_t pk = (uint16_t)__shfl_sync(0xffffffffu, ph, i ^ lane);
+#pragma unroll
+      for (int j = 0; j < GPL; ++j) {
+        const int byte = i * GPL + j;
+        const uint32_t w = (&vc[byte / 16].x)[(byte % 16) / 4];
+        const uint32_t addr = row_addr<G * EPB, PRMT>(w, byte % 4, cbV[j], colV[j], vbook_base);
+        if constexpr (V == 2) {
+          const uint32_t e = lds32(addr);
+          acc[j][0] = fma_h((uint16_t)(e & 0xffff), pk, acc[j][0]);
+          acc[j][1] = fma_h((uint16_t)(e >> 16), pk, acc[j][1]);
+        } else {
+          const uint2 e = lds64(addr);
+          acc[j][0] = fma_h((uint16_t)(e.x & 0xffff), pk, acc[j][0]);
+          acc[j][1] = fma_h((uint16_t)(e.x >> 16), pk, acc[j][1]);
+          acc[j][2] = fma_h((uint16_t)(e.y & 0xffff), pk, acc[j][2]);
+          acc[j][3] = fma_h((uint16_t)(e.y >> 16), pk, acc[j][3]);
+        }
+      }
+    }
+  };
+  // warp w takes 32-token batches w, w+12, ... of the span, double-buffered
+  int t0 = tok0 + warp * 32;
+  if (t0 >= tok1) return;
+  constexpr int STRIDE = kAttnWarps * 32;
+  uint4 ka[Q], va[Q], kb[Q], vb[Q];
+  load(ka, va, t0);
+  for (; t0 < tok1; t0 += 2 * STRIDE) {
+    const bool has_b = t0 + STRIDE < tok1;
+    if (has_b) load(kb, vb, t0 + STRIDE);
+    batch(ka, va);
+    if (has_b) {
+      if (t0 + 2 * STRIDE < tok1) load(ka, va, t0 + 2 * STRIDE);
+      batch(kb, vb);
+    }
+  }
+}
+
 template <int V, int GPL>
 __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   using SM = AttnSmem<V, GPL>;
-  constexpr int G = SM::G, C = SM::C;
-  constexpr int TPL = 16 / GPL;      // tokens per 16-byte code load
-  constexpr int LPB = 32 / TPL;      // loads per 32-token batch
-  constexpr int EPB = V * 2;         // entry bytes
+  constexpr int G = SM::G, C = SM::C, EPB = SM::EPB;
 
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* kbook_s = smem;
-  uint8_t* vbook_s = smem + SM::book_bytes;
-  float* lut_s = reinterpret_cast<float*>(smem + 2 * SM::book_bytes);
-  float* scratch = reinterpret_cast<float*>(smem + 2 * SM::book_bytes + SM::lut_bytes);
-  __shared__ int s_last;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* kbook_s = smem + SM::kbook_off;
+  uint8_t* vbook_s = smem + SM::vbook_off;
+  float* lut_s = reinterpret_cast<float*>(smem + SM::lut_off);
+  float* scratch = reinterpret_cast<float*>(smem + SM::scratch_off);
+  int* s_last = reinterpret_cast<int*>(smem + SM::total - 16);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lut_base = smem_u32(lut_s);
   const uint32_t vbook_base = smem_u32(vbook_s);
+  const bool aligned = (lut_base & 0xffffu) == 0;  // single-prmt addressing possible
   const int BNT = a.B * a.NT;
   const int U = a.H * BNT;
   const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
-  const int64_t TG = (int64_t)a.T * G;  // code bytes per (b, h)
 
   int cur_h = -1;
   for (int u = u0; u < u1;) {
@@ -146,88 +277,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     }
     __syncthreads();
 
-    // ---- stream the span's tokens: warp w takes 32-token batches w, w+16, ...
     float m_w = -INFINITY, l_lane = 0.f;
     float acc[GPL][V];
 #pragma unroll
     for (int j = 0; j < GPL; ++j)
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
-    const uint8_t* kbase = a.kc + (int64_t)bh * TG;
-    const uint8_t* vbase = a.vc + (int64_t)bh * TG;
-    for (int t0 = tok0 + warp * 32; t0 < tok1; t0 += kAttnWarps * 32) {
-      uint4 kcv[LPB], vcv[LPB];
-#pragma unroll
-      for (int i = 0; i < LPB; ++i) {
-        const int64_t off = ((int64_t)(t0 / TPL + i) * 32 + lane) * 16;
-        kcv[i] = ldg_stream(kbase + off);
-        vcv[i] = ldg_stream(vbase + off);
-      }
-      // K phase: per-lane partial logits of the 32 tokens over this lane's groups
-      float s[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const uint32_t w = (&kcv[k / TPL].x)[((k % TPL) * GPL) / 4];
-        float acc_s = 0.f;
-#pragma unroll
-        for (int j = 0; j < GPL; ++j) {
-          const int byte = ((k % TPL) * GPL + j) % 4;
-          const uint32_t code = (w >> (8 * byte)) & 0xff;
-          acc_s += lds_f32(lut_base + ((code * G + lane + 32 * j) << 2));
-        }
-        s[k] = acc_s;
-      }
-      // transpose-reduce: afterwards s[0] on lane l is the full logit of token l
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < off; ++i) {
-          const float send = upper ? s[i] : s[i + off];
-          const float keep = upper ? s[i + off] : s[i];
-          s[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-      }
-      const bool valid = (t0 + lane) < tok1;
-      const float z = valid ? s[0] : -INFINITY;
-      float mb = z;
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
-      const float m_new = fmaxf(m_w, mb);
-      const float corr = fast_exp2(m_w - m_new);
-      const float p = fast_exp2(z - m_new);
-      l_lane = l_lane * corr + p;
-      m_w = m_new;
-#pragma unroll
-      for (int j = 0; j < GPL; ++j)
-#pragma unroll
-        for (int i = 0; i < V; ++i) acc[j][i] *= corr;
-      const uint32_t ph = (uint32_t)__half_as_ushort(__float2half_rn(p));
-      // V phase: dequantise V in registers, fused into the fp32 accumulators
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const uint16_t pk = (uint16_t)__shfl_sync(0xffffffffu, ph, k);
-        const uint32_t w = (&vcv[k / TPL].x)[((k % TPL) * GPL) / 4];
-#pragma unroll
-        for (int j = 0; j < GPL; ++j) {
-          const int byte = ((k % TPL) * GPL + j) % 4;
-          const uint32_t code = (w >> (8 * byte)) & 0xff;
-          const uint32_t addr = vbook_base + (code * G + lane + 32 * j) * EPB;
-          if constexpr (V == 2) {
-            const uint32_t e = lds32(addr);
-            acc[j][0] = fma_h((uint16_t)(e & 0xffff), pk, acc[j][0]);
-            acc[j][1] = fma_h((uint16_t)(e >> 16), pk, acc[j][1]);
-          } else {
-            const uint2 e = lds64(addr);
-            acc[j][0] = fma_h((uint16_t)(e.x & 0xffff), pk, acc[j][0]);
-            acc[j][1] = fma_h((uint16_t)(e.x >> 16), pk, acc[j][1]);
-            acc[j][2] = fma_h((uint16_t)(e.y & 0xffff), pk, acc[j][2]);
-            acc[j][3] = fma_h((uint16_t)(e.y >> 16), pk, acc[j][3]);
-          }
-        }
-      }
-    }
-    // ---- merge the 16 warps of this span
+    if (aligned) attn_stream_span<V, GPL, true>(a, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc);
+    else attn_stream_span<V, GPL, false>(a, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc);
+
+    // ---- merge the warps of this span
     float l_w = l_lane;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) l_w += __shfl_xor_sync(0xffffffffu, l_w, off);
@@ -253,7 +312,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
         const float sc = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
         val += sc * (tid < C ? scratch[w * (C + 2) + 2 + tid] : scratch[w * (C + 2) + 1]);
       }
-      if (tid < C) {
+      if (whole) {
+        scratch[kAttnWarps * (C + 2) + tid] = val;  // the span is the whole (b, h): no partials
+      } else if (tid < C) {
         rec[3 + tid] = val;
       } else {
         rec[0] = M;
@@ -261,17 +322,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
         rec[2] = (float)(tc1 - tc0);
       }
     }
-    __threadfence();
     __syncthreads();
     if (whole) {
       if (tid < C) {
-        const float L = __ldcg(rec + 1);
-        store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, __ldcg(rec + 3 + tid) / L);
+        const float L = scratch[kAttnWarps * (C + 2) + C];
+        store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, scratch[kAttnWarps * (C + 2) + tid] / L);
       }
     } else {
-      if (tid == 0) s_last = (atomicAdd(a.counters + bh, tc1 - tc0) + (tc1 - tc0) == a.NT);
+      __threadfence();
       __syncthreads();
-      if (s_last) {
+      if (tid == 0) *s_last = (atomicAdd(a.counters + bh, tc1 - tc0) + (tc1 - tc0) == a.NT);
+      __syncthreads();
+      if (*s_last) {
         __threadfence();
         if (tid < C) {
           const float* base = a.part + (int64_t)bh * a.NT * (C + 3);
@@ -359,6 +421,7 @@ static bool attn_fast_ok(const Geom& gk, const Geom& gv, const VqbTensor* k, con
   for (const Geom* g : {&gk, &gv}) {
     if (g->sharing != VQB_SHARE_CHANNEL_GROUP || g->group_width != g->v || g->R != 1 || g->bits != 8) return false;
     if (!(g->v == 2 || g->v == 4) || !(g->gpr == 32 || g->gpr == 64)) return false;
+    if (g->v * g->gpr > 128) return false;  // C <= 128: books fit the 64 KB regions
   }
   if (gk.v != gv.v || T % 32 != 0) return false;
   return true;
@@ -372,8 +435,8 @@ int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH) {
   if (s) return s;
   const int64_t T = g.dims[2], C = g.cols;
   const int64_t NT = ceil_div(T, kAttnChunk);
-  const int64_t fast = a256(BH * 4) + BH * NT * (C + 3) * 4;
-  const int64_t generic = a256(2 * BH * T * C * 4) + BH * T * 4;
+  const int64_t fast = VQB_WS_COUNTER_BYTES + BH * NT * (C + 3) * 4;
+  const int64_t generic = VQB_WS_COUNTER_BYTES + a256(2 * BH * T * C * 4) + BH * T * 4;
   return std::max(fast, generic);
 }
 
@@ -415,7 +478,7 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
   const int64_t need = attn_ws_bytes(k, BH);
   if ((int64_t)ws_bytes < need || !ws)
     return set_error(VQB_ECAPACITY, "attention workspace too small: %zu < %lld", ws_bytes, (long long)need);
-  const bool fast = attn_fast_ok(gk, gv, k, v, T, L);
+  const bool fast = attn_fast_ok(gk, gv, k, v, T, L) && BH * 4 <= VQB_WS_COUNTER_BYTES;
   if (used_fast) *used_fast = fast;
   if (fast) {
     AttnArgs a;
@@ -428,7 +491,7 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.out = out;
     a.out_dtype = out_dtype;
     a.counters = reinterpret_cast<int*>(ws);
-    a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + a256(BH * 4));
+    a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);
     a.B = B;
     a.H = H;
     a.T = T;
@@ -439,11 +502,11 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     if (gk.v == 2 && gpl == 2) return launch_attn_t<2, 2>(a, st, gl);
     if (gk.v == 2 && gpl == 1) return launch_attn_t<2, 1>(a, st, gl);
     if (gk.v == 4 && gpl == 1) return launch_attn_t<4, 1>(a, st, gl);
-    return launch_attn_t<4, 2>(a, st, gl);
+    return set_error(VQB_ECONFIG, "no fast attention instance for this configuration");
   }
-  float* kd = reinterpret_cast<float*>(ws);
+  float* kd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);
   float* vd = kd + BH * T * C;
-  float* lg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + a256(2 * BH * T * C * 4));
+  float* lg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES + a256(2 * BH * T * C * 4));
   s = launch_dequant(gk, k, kd, VQB_F32, st);
   if (s) return s;
   s = launch_dequant(gv, v, vd, VQB_F32, st);

@@ -95,15 +95,17 @@ __device__ __forceinline__ int64_t il_offset(const Geom& g, int r, int64_t s) {
     const int64_t m = s / g.gpr, grp = s - (s / g.gpr) * g.gpr;
     return (int64_t)r * g.S + ((m / rpl) * g.gpr + grp) * rpl + (m % rpl);
   }
-  // KV_IL: per (b,h) block of T tokens: [T/TPL][32][TPL][GPL]
+  // KV_IL: per (b,h), per 32-token batch: [Q = 2*GPL][32 lanes][16 bytes]; lane l owns
+  // groups l + 32j and stores token (i ^ l) of the batch at slot i, byte i*GPL + j
+  // (the XOR order makes the attention kernel's cross-lane logit reduction select-free).
   const int64_t T = g.d_T;
   const int gpl = (int)(g.gpr / 32);
-  const int tpl = 16 / gpl;
   const int64_t row = s / g.gpr, grp = s - (s / g.gpr) * g.gpr;
   const int64_t bh = row / T, t = row - (row / T) * T;
-  const int64_t lane = grp % 32, j = grp / 32;
-  return (int64_t)r * g.S + bh * T * g.gpr +
-         (((t / tpl) * 32 + lane) * tpl + (t % tpl)) * gpl + j;
+  const int lane = (int)(grp % 32), j = (int)(grp / 32);
+  const int slot = (int)(t % 32) ^ lane;
+  const int byte = slot * gpl + j;
+  return (int64_t)r * g.S + bh * T * g.gpr + (t / 32) * 32 * g.gpr + ((byte / 16) * 32 + lane) * 16 + (byte % 16);
 }
 
 // Code of level r for sub-vector s, from any layout.

@@ -5,27 +5,38 @@
 // reference_compute's `a @ dequantize(W)` (sim.py:136-144) within 1e-4 rel-to-max
 // (verify.py:200-215).
 //
-// Fast kernel (B200 design, see DESIGN.md §GEMV):
-//  * codebook cache — the first n_shared entries of every codebook the CTA needs
+// Fast kernel (B200 design, DESIGN.md §GEMV):
+//  * codebook cache — the first n_shared entries of every codebook a CTA needs
 //    live in shared memory REPLICATED 128/EB times (EB = entry bytes): entry e
-//    occupies one 128-byte bank row and lane l reads replica (l mod 128/EB), so a
-//    warp-wide random gather is conflict-free by construction (8 lanes of an
-//    LDS.128 quarter-warp or 16 lanes of an LDS.64 half-warp always hit distinct
-//    bank groups). Entries >= n_shared are read from the global/L2 tier.
-//  * codebook-centric dataflow — a CTA tile is 32*WG sub-vector columns x a part of
-//    M; for tile-shared codebooks (GPTVQ) a 256-row chunk lies inside one codebook
-//    region, so the CTA loads exactly one codebook per chunk; whole-tensor books
-//    are loaded once per persistent CTA. M is split f ways (DataflowPlan
-//    split_factor on "M"), partials reduced deterministically by the last CTA.
-//  * codes stream as 16-byte lane loads (GEMV_IL layout: 8 u16 or 16 u8 codes of
-//    one column for consecutive rows), fully coalesced 512 B per warp load.
-//  * register-level fusion — each lane owns one sub-vector column and multiplies
-//    its looked-up fp16 entry straight into fp32 accumulators with the sm_100
+//    owns one 128-byte bank row and lane l reads replica (l mod 128/EB), so a
+//    warp-wide random gather is conflict-free by construction (the 8 lanes of an
+//    LDS.128 quarter-warp / 16 lanes of an LDS.64 half-warp always hit distinct
+//    bank groups). Entries >= n_shared come from the global/L2 tier; when the
+//    tensor's max code is known to be < n_shared the global tier is compiled out.
+//  * codebook-centric dataflow — work units are (column block of 32*WG
+//    sub-vector columns, 256-row chunk). For tile-shared books (GPTVQ) a chunk
+//    lies inside one codebook region; the next region's book is prefetched and
+//    written into a second shared buffer while the current chunk computes.
+//    Whole-tensor books are loaded once per persistent CTA.
+//  * persistent streaming — grid = occupancy x SMs; CTA i owns a contiguous
+//    range of units, accumulates consecutive chunks of a column block in
+//    registers, and double-buffers the 16-byte code loads of chunk c+1 in
+//    registers while chunk c computes. Spans that do not cover a whole column
+//    block leave a partial; the last arriving CTA sums them in chunk order
+//    (deterministic, like the reference's ordered split reduction, sim.py:735).
+//  * programmatic dependent launch — codebook fill and the first code loads run
+//    before griddepcontrol.wait, overlapping the previous kernel's tail; x, y and
+//    the workspace are only touched after it.
+//  * register-level fusion — a lane owns one sub-vector column and multiplies
+//    the looked-up fp16 entry straight into fp32 accumulators with the sm_100
 //    mixed-precision FMA (fma.rn.f32.f16): no staging, no shuffles.
 //
-// Generic kernel: any VQConfig / sharing / layout / dtype, fp32 math, bit-exact
-// dequantised W (same +0.0f level-order accumulation as vqb_dequant), used for
-// parity mode (fp32 codebooks) and for configurations outside the fast table.
+// Generic kernel: any VQConfig / sharing / layout / dtype, fp32 math on the
+// bit-exact dequantised W, used for parity mode (fp32 codebooks) and for
+// configurations outside the fast table.
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 
 namespace vqb {
@@ -40,155 +51,228 @@ struct GemvFastArgs {
   const __half* x;        // (B, M)
   void* y;
   int y_dtype;
-  float* part;            // (f, B, N) partials when f > 1
-  int* counters;          // n_cblk arrival counters
+  float* part;            // (n_cblk * n_chunks, B, COLS) span partials
+  int* span_len;          // (n_cblk * n_chunks) chunks covered by the partial at that slot
+  int* counters;          // (n_cblk) chunks reduced so far
   int M, N, G, K, n_regions;
   int tile_rows, tile_cols, n_tc;
-  int f, chunks_per_part, n_cblk, n_sh;
+  int n_chunks, n_cblk, n_sh;
 };
 
-template <int V, int CBYTES, int R, int B, int WG, bool TILE>
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER>
 __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a) {
   constexpr int EB = V * 2;              // fp16 entry bytes
   constexpr int REP = 128 / EB;          // replicas per bank row
   constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code load
   constexpr int WM = 8 / WG;             // warps along M
   constexpr int RW = kChunkRows / WM;    // rows per warp per chunk
-  constexpr int LOADS = RW / RPL;        // 16-byte code loads per lane per level
-  constexpr int COLS = 32 * WG * V;      // output columns per CTA tile
+  constexpr int LOADS = RW / RPL;        // 16-byte code loads per lane per level per chunk
+  constexpr int COLS = 32 * WG * V;      // output columns per column block
+  constexpr int NBUF = TILE ? 2 : 1;     // codebook buffers
   static_assert(LOADS >= 1 && RW % 8 == 0, "bad tiling");
 
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WG, wg = warp % WG;
-  uint8_t* books_s = smem;                                   // R * n_sh * 128
-  float* red = reinterpret_cast<float*>(smem + (size_t)R * a.n_sh * 128);  // WM*B*COLS
+  const size_t book_bytes = (size_t)R * a.n_sh * 128;
+  float* red = reinterpret_cast<float*>(smem + NBUF * book_bytes);  // WM * B * COLS
   __shared__ int s_last;
-  const uint32_t books_base = smem_u32(books_s);
+  const uint32_t smem_base = smem_u32(smem);
   const uint32_t rep_off = (uint32_t)(lane % REP) * EB;
 
-  auto fill = [&](int region) {
-    // copy entries [0, n_sh) of each level's codebook into replicated rows
-    for (int r = 0; r < R; ++r) {
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.books) +
-                           ((int64_t)(r * a.n_regions + region) * a.K) * EB;
-      uint8_t* dst = books_s + (size_t)r * a.n_sh * 128;
-      for (int e = tid; e < a.n_sh; e += kGemvThreads) {
-        if constexpr (EB == 16) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + e);
+  pdl_launch_dependents();
+
+  // entry e of level r for `region`: this thread's share, loaded to registers
+  // (issue) and stored replicated (commit) so the load latency can overlap compute.
+  constexpr int MAX_PER_THREAD = 4;  // n_sh * R <= 1024 entries
+  auto book_issue = [&](int region, uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
-          for (int q = 0; q < REP; ++q)
-            *reinterpret_cast<uint4*>(dst + e * 128 + ((q + e) % REP) * EB) = v;
-        } else {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(src) + e);
+    for (int k = 0; k < MAX_PER_THREAD; ++k) {
+      const int idx = tid + k * kGemvThreads;  // over R * n_sh
+      if (idx < R * a.n_sh) {
+        const int r = idx / a.n_sh, e = idx - r * a.n_sh;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.books) +
+                             (((int64_t)(r * a.n_regions + region) * a.K) + e) * EB;
+        if constexpr (EB == 16) buf[k] = __ldg(reinterpret_cast<const uint4*>(src));
+        else {
+          const uint2 t = __ldg(reinterpret_cast<const uint2*>(src));
+          buf[k] = make_uint4(t.x, t.y, 0, 0);
+        }
+      }
+    }
+  };
+  auto book_commit = [&](int bufi, const uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
-          for (int q = 0; q < REP; ++q)
-            *reinterpret_cast<uint2*>(dst + e * 128 + ((q + e) % REP) * EB) = v;
+    for (int k = 0; k < MAX_PER_THREAD; ++k) {
+      const int idx = tid + k * kGemvThreads;
+      if (idx < R * a.n_sh) {
+        const int r = idx / a.n_sh, e = idx - r * a.n_sh;
+        uint8_t* row = smem + bufi * book_bytes + ((size_t)r * a.n_sh + e) * 128;
+#pragma unroll
+        for (int q = 0; q < REP; ++q) {
+          uint8_t* d = row + ((q + e) % REP) * EB;  // rotate so 8/16 threads hit distinct banks
+          if constexpr (EB == 16) *reinterpret_cast<uint4*>(d) = buf[k];
+          else *reinterpret_cast<uint2*>(d) = make_uint2(buf[k].x, buf[k].y);
         }
       }
     }
   };
 
-  int cur_region = -1;
-  if constexpr (!TILE) {
-    fill(0);
-    cur_region = 0;
-    __syncthreads();
-  }
+  const int U = a.n_cblk * a.n_chunks;
+  const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+  bool waited = false;
 
-  const int n_tiles = a.n_cblk * a.f;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int cblk = tile % a.n_cblk;
-    const int part = tile / a.n_cblk;
+  bool book_ready = TILE;  // whole-tensor book: filled once, after the first code loads are issued
+
+  for (int u = u0; u < u1;) {
+    const int cblk = u / a.n_chunks;
+    const int c0 = u - cblk * a.n_chunks;
+    const int c1 = min(a.n_chunks, c0 + (u1 - u));
     const int g = cblk * 32 * WG + wg * 32 + lane;  // this lane's sub-vector column
+    const int col_tile = TILE ? (cblk * COLS) / a.tile_cols : 0;
+
     float acc[B][V];
 #pragma unroll
     for (int b = 0; b < B; ++b)
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
 
-    for (int ch = 0; ch < a.chunks_per_part; ++ch) {
-      const int chunk = part * a.chunks_per_part + ch;
+    auto load_codes = [&](uint4 (&c)[R][LOADS], int chunk) {
       const int m0 = chunk * kChunkRows + wm * RW;
-      // issue the code stream loads first so their latency overlaps the codebook switch
-      uint4 c[R][LOADS];
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int i = 0; i < LOADS; ++i)
-          c[r][i] = ldg_stream(a.codes + r * a.level_bytes +
-                               ((int64_t)(m0 / RPL + i) * a.G + g) * 16);
-      if constexpr (TILE) {
-        const int region = (chunk * kChunkRows / a.tile_rows) * a.n_tc + (cblk * COLS) / a.tile_cols;
-        if (region != cur_region) {
-          __syncthreads();  // every warp is done with the previous codebook
-          fill(region);
-          cur_region = region;
-          __syncthreads();
-        }
-      }
+          c[r][i] = ldg_stream(a.codes + r * a.level_bytes + ((int64_t)(m0 / RPL + i) * a.G + g) * 16);
+    };
+    auto region_of_chunk = [&](int chunk) {
+      return TILE ? (chunk * kChunkRows / a.tile_rows) * a.n_tc + col_tile : 0;
+    };
+
+    // Gather-then-FMA in batches of NB codes so NB independent LDS are in flight
+    // before their first consumer (the LDS latency is otherwise exposed per code).
+    constexpr int NB = (EB == 16) ? 8 : 16;  // 32 registers of entries per batch
+    auto compute = [&](const uint4 (&c)[R][LOADS], int chunk, int bufi) {
+      const int m0 = chunk * kChunkRows + wm * RW;
+      const uint8_t* bsm = smem + bufi * book_bytes + rep_off;
+      const int region = region_of_chunk(chunk);
 #pragma unroll
       for (int i = 0; i < LOADS; ++i) {
-        // activations of this load's RPL rows (same address on every lane: broadcast)
-        uint4 xv[B][RPL / 8];
 #pragma unroll
-        for (int b = 0; b < B; ++b)
+        for (int r = 0; r < R; ++r) {
 #pragma unroll
-          for (int q = 0; q < RPL / 8; ++q)
-            xv[b][q] = __ldg(reinterpret_cast<const uint4*>(a.x + (int64_t)b * a.M + m0 + i * RPL) + q);
+          for (int k0 = 0; k0 < RPL; k0 += NB) {
+            uint32_t e[NB][V / 2];
 #pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-          uint16_t xh[B];
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            const uint32_t w = (&xv[b][k / 8].x)[(k % 8) / 2];
-            xh[b] = (uint16_t)((k & 1) ? (w >> 16) : (w & 0xffff));
-          }
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            uint32_t code;
-            if constexpr (CBYTES == 2) {
-              const uint32_t w = (&c[r][i].x)[k / 2];
-              code = (k & 1) ? (w >> 16) : (w & 0xffff);
-            } else {
-              const uint32_t w = (&c[r][i].x)[k / 4];
-              code = (w >> (8 * (k % 4))) & 0xff;
-            }
-            uint32_t e[V / 2];
-            if (code < (uint32_t)a.n_sh) {
-              const uint32_t addr = books_base + (uint32_t)r * a.n_sh * 128 + (code << 7) + rep_off;
-              if constexpr (EB == 16) {
-                const uint4 q = lds128(addr);
-                e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
+            for (int kk = 0; kk < NB; ++kk) {
+              const int k = k0 + kk;
+              uint32_t code;
+              if constexpr (CBYTES == 2) {
+                const uint32_t w = (&c[r][i].x)[k / 2];
+                code = (k & 1) ? (w >> 16) : (w & 0xffff);
               } else {
-                const uint2 q = lds64(addr);
-                e[0] = q.x; e[1] = q.y;
+                const uint32_t w = (&c[r][i].x)[k / 4];
+                code = (w >> (8 * (k % 4))) & 0xff;
               }
-            } else {
-              const int region = cur_region < 0 ? 0 : cur_region;
-              const uint8_t* gp = reinterpret_cast<const uint8_t*>(a.books) +
-                                  (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
+              bool in_smem = true;
+              if constexpr (GTIER) in_smem = code < (uint32_t)a.n_sh;
+              const uint8_t* src = in_smem
+                  ? bsm + (size_t)r * a.n_sh * 128 + ((size_t)code << 7)
+                  : reinterpret_cast<const uint8_t*>(a.books) +
+                        (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
               if constexpr (EB == 16) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(gp));
-                e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
+                const uint4 q = in_smem ? *reinterpret_cast<const uint4*>(src)
+                                        : __ldg(reinterpret_cast<const uint4*>(src));
+                e[kk][0] = q.x; e[kk][1] = q.y; e[kk][2] = q.z; e[kk][3] = q.w;
               } else {
-                const uint2 q = __ldg(reinterpret_cast<const uint2*>(gp));
-                e[0] = q.x; e[1] = q.y;
+                const uint2 q = in_smem ? *reinterpret_cast<const uint2*>(src)
+                                        : __ldg(reinterpret_cast<const uint2*>(src));
+                e[kk][0] = q.x; e[kk][1] = q.y;
+              }
+            }
+            // activations of these NB rows (same address on every lane: broadcast)
+            uint32_t xw[B][NB / 2];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              const uint4* xp = reinterpret_cast<const uint4*>(a.x + (int64_t)b * a.M + m0 + i * RPL + k0);
+#pragma unroll
+              for (int q = 0; q < NB / 8; ++q) {
+                const uint4 t = __ldg(xp + q);
+                xw[b][4 * q] = t.x; xw[b][4 * q + 1] = t.y; xw[b][4 * q + 2] = t.z; xw[b][4 * q + 3] = t.w;
               }
             }
 #pragma unroll
-            for (int b = 0; b < B; ++b)
+            for (int kk = 0; kk < NB; ++kk) {
 #pragma unroll
-              for (int j = 0; j < V / 2; ++j) {
-                acc[b][2 * j] = fma_h((uint16_t)(e[j] & 0xffff), xh[b], acc[b][2 * j]);
-                acc[b][2 * j + 1] = fma_h((uint16_t)(e[j] >> 16), xh[b], acc[b][2 * j + 1]);
+              for (int b = 0; b < B; ++b) {
+                const uint16_t xh = (uint16_t)((kk & 1) ? (xw[b][kk / 2] >> 16) : (xw[b][kk / 2] & 0xffff));
+#pragma unroll
+                for (int j = 0; j < V / 2; ++j) {
+                  acc[b][2 * j] = fma_h((uint16_t)(e[kk][j] & 0xffff), xh, acc[b][2 * j]);
+                  acc[b][2 * j + 1] = fma_h((uint16_t)(e[kk][j] >> 16), xh, acc[b][2 * j + 1]);
+                }
               }
+            }
           }
         }
+      }
+    };
+
+    // one chunk step: on a codebook switch (tile sharing) the next region's book is
+    // loaded before and stored (into the idle buffer) after this chunk's compute
+    int cur_buf = 0;
+    auto step = [&](const uint4 (&c)[R][LOADS], int chunk) {
+      if constexpr (TILE) {
+        uint4 nb[MAX_PER_THREAD];
+        const bool sw = (chunk + 1 < c1) && region_of_chunk(chunk + 1) != region_of_chunk(chunk);
+        if (sw) book_issue(region_of_chunk(chunk + 1), nb);
+        compute(c, chunk, cur_buf);
+        if (sw) {
+          book_commit(cur_buf ^ 1, nb);
+          __syncthreads();
+          cur_buf ^= 1;
+        }
+      } else {
+        compute(c, chunk, 0);
+      }
+    };
+
+    uint4 ca[R][LOADS], cb[R][LOADS];
+    load_codes(ca, c0);
+    if (!book_ready) {
+      uint4 bb[MAX_PER_THREAD];
+      book_issue(0, bb);
+      book_commit(0, bb);
+      __syncthreads();
+      book_ready = true;
+    }
+    if constexpr (TILE) {
+      uint4 bb[MAX_PER_THREAD];
+      book_issue(region_of_chunk(c0), bb);
+      __syncthreads();  // the previous span is done with both buffers
+      book_commit(0, bb);
+      __syncthreads();
+    }
+    if (!waited) {
+      pdl_wait();  // x / y / workspace may belong to the previous kernel
+      waited = true;
+    }
+    for (int ch = c0; ch < c1; ch += 2) {
+      if (ch + 1 < c1) load_codes(cb, ch + 1);
+      step(ca, ch);
+      if (ch + 1 < c1) {
+        if (ch + 2 < c1) load_codes(ca, ch + 2);
+        step(cb, ch + 1);
       }
     }
 
-    // ---- reduce the WM row-slabs of this tile in a fixed order ----
+    // ---- reduce the WM row-slabs of this span in a fixed order
 #pragma unroll
     for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -196,32 +280,41 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
         red[((size_t)wm * B + b) * COLS + (wg * 32 + lane) * V + j] = acc[b][j];
     __syncthreads();
     const int n0 = cblk * COLS;
+    const bool whole = (c0 == 0 && c1 == a.n_chunks);
+    const int slot = cblk * a.n_chunks + c0;
     for (int o = tid; o < B * COLS; o += kGemvThreads) {
-      const int b = o / COLS, col = o % COLS;
+      const int b = o / COLS, col = o - (o / COLS) * COLS;
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < WM; ++w) s += red[((size_t)w * B + b) * COLS + col];
-      if (a.f == 1) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, s);
-      else a.part[((int64_t)part * B + b) * a.N + n0 + col] = s;
+      if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, s);
+      else a.part[(int64_t)slot * B * COLS + o] = s;
     }
-    if (a.f > 1) {
+    if (!whole) {
+      if (tid == 0) a.span_len[slot] = c1 - c0;
       __threadfence();
       __syncthreads();
-      if (tid == 0) s_last = (atomicAdd(a.counters + cblk, 1) == a.f - 1);
+      if (tid == 0) s_last = (atomicAdd(a.counters + cblk, c1 - c0) + (c1 - c0) == a.n_chunks);
       __syncthreads();
       if (s_last) {
         __threadfence();
         for (int o = tid; o < B * COLS; o += kGemvThreads) {
-          const int b = o / COLS, col = o % COLS;
+          const int b = o / COLS, col = o - (o / COLS) * COLS;
           float s = 0.f;
-          for (int p = 0; p < a.f; ++p) s += __ldcg(a.part + ((int64_t)p * B + b) * a.N + n0 + col);
+          for (int c = 0; c < a.n_chunks;) {
+            const int sl = cblk * a.n_chunks + c;
+            s += __ldcg(a.part + (int64_t)sl * B * COLS + o);
+            c += __ldcg(a.span_len + sl);
+          }
           store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, s);
         }
         if (tid == 0) a.counters[cblk] = 0;  // self-reset for the next launch
       }
     }
-    __syncthreads();  // red / s_last reuse by the next tile
+    __syncthreads();  // red / s_last reuse by the next span
+    u += c1 - c0;
   }
+  if (!waited) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------
@@ -290,8 +383,8 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
 struct FastPlan {
   bool ok = false;
   int V = 0, cbytes = 0, R = 0, WG = 1;
-  bool tile = false;
-  int n_sh = 0, f = 1, n_cblk = 0, n_chunks = 0;
+  bool tile = false, gtier = true;
+  int n_sh = 0, n_cblk = 0, n_chunks = 0;
   size_t smem = 0;
 };
 
@@ -318,22 +411,13 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   int n_sh = (L && L->n_shared > 0) ? L->n_shared : 256;
   n_sh = std::min(n_sh, g.K);
   n_sh = std::min(n_sh, 1024 / g.R);
+  if (L && (L->flags & VQB_FLAG_NO_SHARED)) n_sh = 0;
   p.n_sh = n_sh;
+  p.gtier = !(t->max_code >= 0 && t->max_code < n_sh);
   p.n_cblk = (int)(g.cols / cols_per_cta);
   p.n_chunks = (int)(g.rows / kChunkRows);
-  int f = 0;
-  if (L && L->split_factor > 0 && (L->split_axis == 'M' || L->split_axis == 0) &&
-      p.n_chunks % L->split_factor == 0)
-    f = L->split_factor;
-  if (f == 0) {
-    const int want = 2 * sm_count();
-    f = p.n_chunks;
-    for (int d = 1; d <= p.n_chunks; ++d)
-      if (p.n_chunks % d == 0 && p.n_cblk * d >= want) { f = d; break; }
-  }
-  p.f = f;
   const int WM = 8 / p.WG;
-  p.smem = (size_t)p.R * p.n_sh * 128 + (size_t)WM * rows * cols_per_cta * sizeof(float);
+  p.smem = (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128 + (size_t)WM * rows * cols_per_cta * sizeof(float);
   p.ok = true;
   return p;
 }
@@ -342,58 +426,80 @@ static int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 static int64_t fast_ws_bytes(const FastPlan& p, const Geom& g, int rows) {
   if (!p.ok) return 0;
-  return align256((int64_t)p.n_cblk * sizeof(int)) + (p.f > 1 ? (int64_t)p.f * rows * g.cols * 4 : 0);
+  const int64_t slots = (int64_t)p.n_cblk * p.n_chunks;
+  const int64_t cols = 32 * p.WG * p.V;
+  return VQB_WS_COUNTER_BYTES + align256(slots * 4) + slots * rows * cols * 4;
 }
 
 static int generic_chunk_rows(const Geom& g) { return g.rows > 4096 ? 512 : 256; }
 
 static int64_t generic_ws_bytes(const Geom& g, int rows) {
   const int64_t n_mc = ceil_div(g.rows, generic_chunk_rows(g));
-  return n_mc * rows * g.cols * 4;
+  return VQB_WS_COUNTER_BYTES + n_mc * rows * g.cols * 4;
+}
+
+typedef void (*GemvKernel)(GemvFastArgs);
+
+static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFastArgs& a, cudaStream_t st,
+                              const VqbLaunch* L) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> occ_cache;  // kernel x smem -> occupancy
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void* key = reinterpret_cast<const void*>(
+        reinterpret_cast<uintptr_t>(kernel) ^ ((uintptr_t)p.smem << 20) ^ ((uintptr_t)dev << 56));
+    auto it = occ_cache.find(key);
+    if (it == occ_cache.end()) {
+      // always opt in: static shared memory pushes even a 48 KB dynamic request over the default
+      VQB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kGemvThreads, p.smem));
+      occ_cache[key] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  if (occ < 1) return set_error(VQB_ECAPACITY, "GEMV plan (n_shared=%d) does not fit one CTA per SM", p.n_sh);
+  int grid = std::min(p.n_cblk * p.n_chunks, occ * sm_count());
+  if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemvThreads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (L && (L->flags & VQB_FLAG_NO_PDL)) ? 0 : 1;
+  VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, a));
+  set_kernel("gemv_fast");
+  return VQB_OK;
 }
 
 template <int V, int CBYTES, int R, int WG, bool TILE>
-static int launch_fast_t(const FastPlan& p, GemvFastArgs& a, int rows, cudaStream_t st, int grid_limit) {
-  auto pick = [&](auto kernel) -> int {
-    static bool configured[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (p.smem > 48 * 1024 && !configured[dev & 63]) {
-      VQB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      configured[dev & 63] = true;
-    }
-    int occ = 0;
-    VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kGemvThreads, p.smem));
-    if (occ < 1) return set_error(VQB_ECAPACITY, "GEMV plan (n_shared=%d) does not fit one CTA per SM", p.n_sh);
-    int grid = std::min(p.n_cblk * p.f, occ * sm_count());
-    if (grid_limit > 0) grid = std::min(grid, grid_limit);
-    kernel<<<grid, kGemvThreads, p.smem, st>>>(a);
-    VQB_LAUNCH_CHECK("gemv_fast_kernel");
-    set_kernel("gemv_fast");
-    return VQB_OK;
-  };
+static GemvKernel pick_kernel(int rows, bool gtier) {
+#define VQB_K(B) (gtier ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true> : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false>)
   switch (rows) {
-    case 1: return pick(gemv_fast_kernel<V, CBYTES, R, 1, WG, TILE>);
-    case 2: return pick(gemv_fast_kernel<V, CBYTES, R, 2, WG, TILE>);
-    case 4: return pick(gemv_fast_kernel<V, CBYTES, R, 4, WG, TILE>);
-    default: return pick(gemv_fast_kernel<V, CBYTES, R, 8, WG, TILE>);
+    case 1: return VQB_K(1);
+    case 2: return VQB_K(2);
+    case 4: return VQB_K(4);
+    default: return VQB_K(8);
   }
+#undef VQB_K
 }
 
-static int launch_fast(const FastPlan& p, GemvFastArgs& a, int rows, cudaStream_t st, int grid_limit) {
+static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
   // (V, code bytes, R, WG, tile-shared) combinations covering the BASELINE configs
-  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return launch_fast_t<8, 2, 1, 1, false>(p, a, rows, st, grid_limit);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return launch_fast_t<8, 1, 2, 1, false>(p, a, rows, st, grid_limit);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return launch_fast_t<8, 1, 1, 1, false>(p, a, rows, st, grid_limit);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return launch_fast_t<4, 1, 1, 2, true>(p, a, rows, st, grid_limit);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return launch_fast_t<4, 1, 1, 2, false>(p, a, rows, st, grid_limit);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return launch_fast_t<8, 1, 1, 1, true>(p, a, rows, st, grid_limit);
-  return set_error(VQB_ECONFIG, "no fast GEMV instance for this configuration");
-}
-
-static bool has_fast_instance(const FastPlan& p) {
-  return (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) || (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) ||
-         (p.V == 8 && p.cbytes == 1 && p.R == 1) || (p.V == 4 && p.cbytes == 1 && p.R == 1);
+  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier);
+  return nullptr;
 }
 
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
@@ -406,12 +512,16 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
   if (x_dtype < VQB_F32 || x_dtype > VQB_BF16 || y_dtype < VQB_F32 || y_dtype > VQB_BF16)
     return set_error(VQB_ECONFIG, "unknown activation/output dtype");
   FastPlan p = plan_fast(g, w, rows, x_dtype, L);
-  if (p.ok && !has_fast_instance(p)) p.ok = false;
-  if (used_fast) *used_fast = p.ok;
-  if (p.ok) {
+  GemvKernel kernel = p.ok ? fast_kernel_for(p, rows) : nullptr;
+  if (used_fast) *used_fast = kernel != nullptr;
+  if (kernel) {
     const int64_t need = fast_ws_bytes(p, g, rows);
-    if ((int64_t)ws_bytes < need || (need > 0 && !ws))
+    if ((int64_t)ws_bytes < need || !ws)
       return set_error(VQB_ECAPACITY, "GEMV workspace too small: %zu < %lld", ws_bytes, (long long)need);
+    const int64_t slots = (int64_t)p.n_cblk * p.n_chunks;
+    if ((int64_t)p.n_cblk * 4 > VQB_WS_COUNTER_BYTES)
+      return set_error(VQB_ECAPACITY, "too many GEMV column blocks (%d) for the counter region", p.n_cblk);
+    uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
     GemvFastArgs a;
     a.codes = reinterpret_cast<const uint8_t*>(w->d_codes);
     a.level_bytes = g.S * g.code_bytes;
@@ -419,8 +529,9 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.x = reinterpret_cast<const __half*>(x);
     a.y = y;
     a.y_dtype = y_dtype;
-    a.counters = reinterpret_cast<int*>(ws);
-    a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + align256((int64_t)p.n_cblk * sizeof(int)));
+    a.counters = reinterpret_cast<int*>(wsb);
+    a.span_len = reinterpret_cast<int*>(wsb + VQB_WS_COUNTER_BYTES);
+    a.part = reinterpret_cast<float*>(wsb + VQB_WS_COUNTER_BYTES + align256(slots * 4));
     a.M = (int)g.rows;
     a.N = (int)g.cols;
     a.G = (int)g.gpr;
@@ -429,11 +540,10 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.tile_rows = g.tile_rows;
     a.tile_cols = g.tile_cols;
     a.n_tc = g.sharing == VQB_SHARE_TILE ? (int)ceil_div(g.cols, g.tile_cols) : 1;
-    a.f = p.f;
-    a.chunks_per_part = p.n_chunks / p.f;
+    a.n_chunks = p.n_chunks;
     a.n_cblk = p.n_cblk;
     a.n_sh = p.n_sh;
-    return launch_fast(p, a, rows, st, L ? L->grid_limit : 0);
+    return launch_gemv_kernel(kernel, p, a, st, L);
   }
   // generic: per-chunk partials then an ordered reduction
   const int chunk_rows = generic_chunk_rows(g);
@@ -441,7 +551,7 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
   const int64_t need = generic_ws_bytes(g, rows);
   if ((int64_t)ws_bytes < need || !ws)
     return set_error(VQB_ECAPACITY, "GEMV workspace too small: %zu < %lld", ws_bytes, (long long)need);
-  float* part = reinterpret_cast<float*>(ws);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);
   dim3 grid((unsigned)ceil_div(g.gpr, 128), (unsigned)n_mc, (unsigned)ceil_div(rows, kGenericRowBlock));
   if (grid.z > 65535) return set_error(VQB_ESHAPE, "too many activation rows for the generic GEMV (%d)", rows);
 #define VQB_GEN(CBT, VV) \
@@ -472,13 +582,13 @@ int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
   int s = make_geom(w, &g);
   if (s) return s;
   FastPlan p = plan_fast(g, w, (int)rows, VQB_F16, L);
-  int64_t a = (p.ok && has_fast_instance(p)) ? fast_ws_bytes(p, g, (int)rows) : 0;
+  int64_t a = (p.ok && fast_kernel_for(p, (int)rows)) ? fast_ws_bytes(p, g, (int)rows) : 0;
   return std::max(a, generic_ws_bytes(g, (int)rows));
 }
 
 int gemv_usage(VqbUsage* u) {
   cudaFuncAttributes at;
-  auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false>;
+  auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, true>;
   VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
   const size_t smem = 256 * 128 + 8 * 1 * 256 * 4;
   u->shared_bytes = (int)(at.sharedSizeBytes + smem);

@@ -61,7 +61,7 @@ def auto_layout(shape, config: VQConfig) -> str:
         return "gemv"
     if len(shape) == 4 and b <= 8:
         groups = shape[3] // config.vector_size
-        if groups in (32, 64) and shape[2] % (16 // (groups // 32)) == 0:
+        if groups in (32, 64) and shape[2] % 32 == 0:
             return "kv"
     return "plain"
 
@@ -74,6 +74,7 @@ class DeviceVQTensor:
     codes: torch.Tensor        # uint8 / int16-viewed-as-u16 / uint8 bytes for packed
     layout: str
     codebooks: torch.Tensor    # (R * n_regions, K, v)
+    max_code: int = -1         # largest code present (-1 unknown): lets kernels drop the global tier
 
     # -- construction ------------------------------------------------------------------------
 
@@ -84,6 +85,7 @@ class DeviceVQTensor:
         cfg = q.config
         k = cfg.n_entries
         codes = q.codes
+        hi = -1
         if codes.size:
             lo, hi = int(codes.min()), int(codes.max())
             if lo < 0 or hi >= k:
@@ -97,7 +99,7 @@ class DeviceVQTensor:
         host = np.ascontiguousarray(codes.astype(narrow))
         t = torch.from_numpy(host.view(np.uint8)).to(dev)
         books = torch.from_numpy(q.stacked_entries()).to(dev).to(torch_dtype(codebook_dtype)).contiguous()
-        plain = cls(cfg, tuple(q.shape), q.n_regions, t, "plain", books)
+        plain = cls(cfg, tuple(q.shape), q.n_regions, t, "plain", books, hi)
         if layout == "auto":
             layout = auto_layout(q.shape, cfg)
         return plain if layout == "plain" else plain.relayout(layout)
@@ -127,11 +129,18 @@ class DeviceVQTensor:
         """Wrap codes already on the GPU ((R, S) integer array for ``plain``)."""
         shape = tuple(int(s) for s in shape)
         n_regions = region_count(shape, config)
+        max_code = -1
         if layout == "plain" and codes.dtype not in (torch.uint8,):
+            if codes.numel():
+                lo, hi = int(codes.min()), int(codes.max())
+                if lo < 0 or hi >= config.n_entries:
+                    raise CodeRangeError(f"code out of range: {lo if lo < 0 else hi} not in "
+                                         f"[0, {config.n_entries})")
+                max_code = hi
             narrow = torch.uint8 if config.log2_entries <= 8 else torch.int16
             codes = codes.to(narrow).contiguous().view(torch.uint8)
         return cls(config, shape, n_regions, codes.contiguous().view(torch.uint8), layout,
-                   codebooks.contiguous())
+                   codebooks.contiguous(), max_code)
 
     # -- views -------------------------------------------------------------------------------
 
@@ -178,6 +187,7 @@ class DeviceVQTensor:
         s.codes_bytes = self.codes.numel()
         s.codebook_dtype = _ENUM[self.codebooks.dtype]
         s.d_codebooks = self.codebooks.data_ptr()
+        s.max_code = int(self.max_code)
         return s
 
     def relayout(self, layout: str) -> "DeviceVQTensor":
@@ -191,11 +201,12 @@ class DeviceVQTensor:
         out = torch.empty(need, dtype=torch.uint8, device=self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         N.check(L.vqb_repack(src, _LAYOUTS[layout], out.data_ptr(), need, stream))
-        return DeviceVQTensor(self.config, self.shape, self.n_regions, out, layout, self.codebooks)
+        return DeviceVQTensor(self.config, self.shape, self.n_regions, out, layout, self.codebooks,
+                              self.max_code)
 
     def with_codebook_dtype(self, dtype) -> "DeviceVQTensor":
         d = torch_dtype(dtype)
         if d == self.codebooks.dtype:
             return self
         return DeviceVQTensor(self.config, self.shape, self.n_regions, self.codes, self.layout,
-                              self.codebooks.to(d))
+                              self.codebooks.to(d), self.max_code)

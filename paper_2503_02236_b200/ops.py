@@ -126,3 +126,35 @@ def vq_attention(k: DeviceVQTensor, v: DeviceVQTensor, q: torch.Tensor, out_dtyp
     N.check(lib.vqb_attn_decode(ks, vs, q.data_ptr(), dtype_enum(q.dtype), b, h, t, c, out.data_ptr(),
                                 dtype_enum(od), L, ws.data_ptr(), ws.numel(), _stream(k.device)))
     return out
+
+
+def vq_codes_regions(w: DeviceVQTensor):
+    """(codes (R, S) int64, region id per sub-vector (S,) int64), both on the device.
+
+    Codes come from the GPU repack to the plain layout; region ids restate
+    region_layout (pkg/src/vqforge/codec.py:135-177) with torch index arithmetic.
+    """
+    cfg = w.config
+    plain = w.relayout("plain")
+    s = w.n_subvectors
+    if cfg.log2_entries <= 8:
+        codes = plain.codes[: cfg.residuals * s].view(cfg.residuals, s).to(torch.int64)
+    else:
+        codes = plain.codes[: 2 * cfg.residuals * s].view(torch.int16).view(cfg.residuals, s)
+        codes = codes.to(torch.int64) & 0xFFFF
+    shape = w.shape
+    v = cfg.vector_size
+    per_row = shape[-1] // v
+    idx = torch.arange(s, device=w.device, dtype=torch.int64)
+    row, col = idx // per_row, (idx % per_row) * v
+    sh = cfg.sharing
+    if sh.kind == "whole":
+        regions = torch.zeros_like(idx)
+    elif sh.kind == "channel_group":
+        grp = col // sh.group_width
+        regions = (((row // shape[2]) % shape[1]) * (shape[-1] // sh.group_width) + grp
+                   if len(shape) == 4 else grp)
+    else:
+        n_tc = -(-shape[-1] // sh.tile_cols)
+        regions = ((row % shape[-2]) // sh.tile_rows) * n_tc + col // sh.tile_cols
+    return codes, regions
