@@ -115,6 +115,8 @@ typedef struct VqbLaunch {
 #define VQB_FLAG_FORCE_GENERIC 1 /* use the generic (any-config) kernel */
 #define VQB_FLAG_NO_SHARED 2     /* no shared-memory tier: every lookup from global/L2 ("GC") */
 #define VQB_FLAG_NO_PDL 4        /* launch without programmatic dependent launch */
+#define VQB_FLAG_EXACT_ACCUM 8   /* GEMV: fp32 accumulation of every product (mixed-precision
+                                    FMA, quarter rate) instead of 8-row fp16x2 windows */
 
 /* Kernel resource usage (KernelUsage, gpumodel.py:30-36) measured with
  * cudaFuncGetAttributes on the loaded cubin. */
@@ -183,6 +185,10 @@ int vqb_repack(const VqbTensor* src, int32_t dst_layout, void* d_dst,
 /* Measured resource usage of a kernel family at its default configuration for
  * tensor `t` (may be NULL for the family default). */
 int vqb_query_usage(int32_t kind, const VqbTensor* t, VqbUsage* out);
+
+/* Debug: write the shared-window offset of dynamic shared memory (kernel with no
+ * static shared memory) to d_out[0]. */
+int vqb_debug_smem_base(uint32_t* d_out, void* stream);
 
 #ifdef __cplusplus
 }

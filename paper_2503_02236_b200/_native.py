@@ -35,6 +35,7 @@ _ERRORS = {
 EXPORTS = (
     "vqb_abi_version", "vqb_last_error", "vqb_last_kernel", "vqb_dequant", "vqb_workspace_bytes", "vqb_gemv",
     "vqb_gemm", "vqb_attn_decode", "vqb_layout_bytes", "vqb_repack", "vqb_query_usage",
+    "vqb_debug_smem_base",
 )
 
 
@@ -113,6 +114,8 @@ def lib():
             L.vqb_layout_bytes.restype = i64
             L.vqb_repack.argtypes = [T, i32, vp, i64, vp]
             L.vqb_query_usage.argtypes = [i32, T, P(VqbUsage)]
+            L.vqb_debug_smem_base.argtypes = [vp, vp]
+            L.vqb_debug_smem_base.restype = ctypes.c_int
             for name in ("vqb_dequant", "vqb_gemv", "vqb_gemm", "vqb_attn_decode", "vqb_repack",
                          "vqb_query_usage"):
                 getattr(L, name).restype = ctypes.c_int

@@ -229,6 +229,14 @@ static int dest_geom(const VqbTensor* t, int32_t layout, Geom* g) {
   return make_geom(&d, g);
 }
 
+// Shared-window offset of dynamic shared memory in a kernel without static
+// shared memory: the kernels fold region bases into PRMT-built addresses when
+// this is 64 KB aligned (tested by tests/test_gpu_kernels.py).
+__global__ void smem_base_probe_kernel(uint32_t* out) {
+  extern __shared__ __align__(16) uint8_t dyn[];
+  if (threadIdx.x == 0) out[0] = smem_u32(dyn);
+}
+
 int gemv_usage(VqbUsage* u);
 int attn_usage(VqbUsage* u);
 int gemm_usage(VqbUsage* u);
@@ -283,6 +291,18 @@ int vqb_repack(const VqbTensor* src, int32_t dst_layout, void* d_dst, int64_t ds
   repack_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(gs, src->d_codes, gd, d_dst);
   VQB_LAUNCH_CHECK("repack_kernel");
   set_kernel("repack");
+  return VQB_OK;
+}
+
+int vqb_debug_smem_base(uint32_t* d_out, void* stream) {
+  smem_base_probe_kernel<<<1, 32, 65536 + 1024, reinterpret_cast<cudaStream_t>(stream)>>>(d_out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaErrorInvalidValue) {
+    cudaFuncSetAttribute(smem_base_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    smem_base_probe_kernel<<<1, 32, 65536 + 1024, reinterpret_cast<cudaStream_t>(stream)>>>(d_out);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) return cuda_error(e, "smem_base_probe_kernel");
   return VQB_OK;
 }
 

@@ -6,6 +6,11 @@
 // (verify.py:200-215).
 //
 // Fast kernel (B200 design):
+//  * TMA-staged index stream — a producer warp streams each work unit's codes
+//    (GEMV_IL layout: 512-byte contiguous row-group segments) into a 4-stage
+//    shared-memory ring with cp.async.bulk + mbarrier transaction counts, so a
+//    CTA keeps up to 64 KB of code loads in flight independent of registers;
+//    consumer warps read their 16-byte code words from shared memory.
 //  * codebook cache — the first n_shared entries of every codebook a CTA needs
 //    live in shared memory REPLICATED 128/EB times (EB = entry bytes): entry e
 //    owns one 128-byte bank row and lane l reads replica (l mod 128/EB), so a
@@ -14,17 +19,14 @@
 //    bank groups). Entries >= n_shared come from the global/L2 tier; when the
 //    tensor's max code is known to be < n_shared the global tier is compiled out.
 //  * codebook-centric dataflow — work units are (column block of 32*WG
-//    sub-vector columns, 256-row chunk). For tile-shared books (GPTVQ) a chunk
-//    lies inside one codebook region; the next region's book is prefetched and
-//    written into a second shared buffer while the current chunk computes.
-//    Whole-tensor books are loaded once per persistent CTA.
-//  * persistent streaming — grid = occupancy x SMs; CTA i owns a contiguous
-//    range of units, accumulates consecutive chunks of a column block in
-//    registers, and double-buffers the 16-byte code loads of chunk c+1 in
-//    registers while chunk c computes. Spans that do not cover a whole column
-//    block leave a partial; the last arriving CTA sums them in chunk order
+//    sub-vector columns, 256-row chunk); a tile-shared book (GPTVQ) covers whole
+//    chunks, the next region's book is prefetched while the current chunk
+//    computes; whole-tensor books are loaded once per persistent CTA.
+//  * persistent CTAs own contiguous unit ranges and accumulate consecutive
+//    chunks of a column block in registers; spans that do not cover a whole
+//    column block leave a partial that the last arriving CTA sums in chunk order
 //    (deterministic, like the reference's ordered split reduction, sim.py:735).
-//  * programmatic dependent launch — codebook fill and the first code loads run
+//  * programmatic dependent launch — the code stream and the codebook fill start
 //    before griddepcontrol.wait, overlapping the previous kernel's tail; x, y and
 //    the workspace are only touched after it.
 //  * register-level fusion — a lane owns one sub-vector column and multiplies
@@ -41,8 +43,14 @@
 
 namespace vqb {
 
-constexpr int kGemvThreads = 256;
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kGemvThreads = kConsumers + 32;  // + one producer warp
 constexpr int kChunkRows = 256;
+constexpr int kStages = 4;
+constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
+// bytes of one work unit's codes (= one ring stage): R levels x 256 rows x 32*WG columns
+__host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG) { return R * cbytes * WG * kChunkRows * 32; }
 
 struct GemvFastArgs {
   const uint8_t* codes;   // GEMV_IL, level r at codes + r * level_bytes
@@ -59,41 +67,78 @@ struct GemvFastArgs {
   int n_chunks, n_cblk, n_sh;
 };
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER>
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, bool H2>
 __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a) {
   constexpr int EB = V * 2;              // fp16 entry bytes
   constexpr int REP = 128 / EB;          // replicas per bank row
-  constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code load
-  constexpr int WM = 8 / WG;             // warps along M
+  constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code word
+  constexpr int WM = kConsumerWarps / WG;  // warps along M
   constexpr int RW = kChunkRows / WM;    // rows per warp per chunk
-  constexpr int LOADS = RW / RPL;        // 16-byte code loads per lane per level per chunk
+  constexpr int LOADS = RW / RPL;        // code words per lane per level per chunk
   constexpr int COLS = 32 * WG * V;      // output columns per column block
+  constexpr int NSEG = kChunkRows / RPL; // row-group segments per level per unit
+  constexpr int SEGB = 32 * WG * 16;     // bytes per segment
+  constexpr int LEVB = NSEG * SEGB;      // bytes per level per unit
   constexpr int NBUF = TILE ? 2 : 1;     // codebook buffers
   static_assert(LOADS >= 1 && RW % 8 == 0, "bad tiling");
+  constexpr int STAGEB = R * LEVB;
+  static_assert(STAGEB == stage_bytes(R, CBYTES, WG), "stage size");
+  static_assert(NSEG <= 32, "one segment per producer lane");
 
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WG, wg = warp % WG;
+  uint8_t* stages = smem;                                        // kStages x STAGEB
+  uint8_t* books_s = smem + kStages * STAGEB;                    // NBUF x R x n_sh x 128
   const size_t book_bytes = (size_t)R * a.n_sh * 128;
-  float* red = reinterpret_cast<float*>(smem + NBUF * book_bytes);  // WM * B * COLS
-  __shared__ int s_last;
-  const uint32_t smem_base = smem_u32(smem);
-  const uint32_t rep_off = (uint32_t)(lane % REP) * EB;
+  float* red = reinterpret_cast<float*>(books_s + NBUF * book_bytes);  // WM * COLS
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + WM * COLS);       // full[kStages], empty[kStages]
+  int* s_last = reinterpret_cast<int*>(bars + 2 * kStages);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
 
+  const int U = a.n_cblk * a.n_chunks;
+  const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
   pdl_launch_dependents();
 
-  // entry e of level r for `region`: this thread's share, loaded to registers
-  // (issue) and stored replicated (commit) so the load latency can overlap compute.
-  constexpr int MAX_PER_THREAD = 4;  // n_sh * R <= 1024 entries
+  if (warp == kConsumerWarps) {
+    // ===== producer: stream each unit's code segments into the stage ring =====
+    for (int idx = 0; idx < u1 - u0; ++idx) {
+      const int u = u0 + idx;
+      const int cblk = u / a.n_chunks, chunk = u - cblk * a.n_chunks;
+      const int s = idx % kStages;
+      if (idx >= kStages) mbar_wait(empty0 + 8 * s, ((idx / kStages) + 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * s, STAGEB);
+      __syncwarp();
+      if (lane < NSEG) {
+        const int64_t rg = (int64_t)chunk * NSEG + lane;  // row-group index along M
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          tma_load_1d(smem_u32(stages + s * STAGEB + r * LEVB + lane * SEGB),
+                      a.codes + r * a.level_bytes + (rg * a.G + (int64_t)cblk * 32 * WG) * 16, SEGB,
+                      full0 + 8 * s);
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int wm = warp / WG, wg = warp % WG;
+  const uint32_t rep_off = (uint32_t)(lane % REP) * EB;
+
+  constexpr int MAX_PER_THREAD = (1024 + kConsumers - 1) / kConsumers;  // n_sh * R <= 1024 entries
   auto book_issue = [&](int region, uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
     for (int k = 0; k < MAX_PER_THREAD; ++k) {
-      const int idx = tid + k * kGemvThreads;  // over R * n_sh
+      const int idx = tid + k * kConsumers;
       if (idx < R * a.n_sh) {
         const int r = idx / a.n_sh, e = idx - r * a.n_sh;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(a.books) +
@@ -109,10 +154,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   auto book_commit = [&](int bufi, const uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
     for (int k = 0; k < MAX_PER_THREAD; ++k) {
-      const int idx = tid + k * kGemvThreads;
+      const int idx = tid + k * kConsumers;
       if (idx < R * a.n_sh) {
         const int r = idx / a.n_sh, e = idx - r * a.n_sh;
-        uint8_t* row = smem + bufi * book_bytes + ((size_t)r * a.n_sh + e) * 128;
+        uint8_t* row = books_s + bufi * book_bytes + ((size_t)r * a.n_sh + e) * 128;
 #pragma unroll
         for (int q = 0; q < REP; ++q) {
           uint8_t* d = row + ((q + e) % REP) * EB;  // rotate so 8/16 threads hit distinct banks
@@ -122,20 +167,35 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
       }
     }
   };
+  auto csync = [&]() { named_bar_sync(1, kConsumers); };
 
-  const int U = a.n_cblk * a.n_chunks;
-  const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
-  const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
-  bool waited = false;
+  if constexpr (!TILE) {
+    uint4 bb[MAX_PER_THREAD];
+    book_issue(0, bb);
+    book_commit(0, bb);
+  }
+  pdl_wait();  // x / y / workspace may belong to the previous kernel
+  csync();
 
-  bool book_ready = TILE;  // whole-tensor book: filled once, after the first code loads are issued
-
+  int idx = 0;
+  int cur_buf = 0;
   for (int u = u0; u < u1;) {
     const int cblk = u / a.n_chunks;
     const int c0 = u - cblk * a.n_chunks;
     const int c1 = min(a.n_chunks, c0 + (u1 - u));
-    const int g = cblk * 32 * WG + wg * 32 + lane;  // this lane's sub-vector column
+    const int g_local = wg * 32 + lane;
     const int col_tile = TILE ? (cblk * COLS) / a.tile_cols : 0;
+    auto region_of_chunk = [&](int chunk) {
+      return TILE ? (chunk * kChunkRows / a.tile_rows) * a.n_tc + col_tile : 0;
+    };
+    if constexpr (TILE) {
+      uint4 bb[MAX_PER_THREAD];
+      book_issue(region_of_chunk(c0), bb);
+      csync();  // the previous span is done with both buffers
+      book_commit(0, bb);
+      cur_buf = 0;
+      csync();
+    }
 
     float acc[B][V];
 #pragma unroll
@@ -143,181 +203,155 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
 
-    auto load_codes = [&](uint4 (&c)[R][LOADS], int chunk) {
-      const int m0 = chunk * kChunkRows + wm * RW;
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int i = 0; i < LOADS; ++i)
-          c[r][i] = ldg_stream(a.codes + r * a.level_bytes + ((int64_t)(m0 / RPL + i) * a.G + g) * 16);
-    };
-    auto region_of_chunk = [&](int chunk) {
-      return TILE ? (chunk * kChunkRows / a.tile_rows) * a.n_tc + col_tile : 0;
-    };
-
-    // Gather-then-FMA in batches of NB codes so NB independent LDS are in flight
-    // before their first consumer (the LDS latency is otherwise exposed per code).
-    constexpr int NB = (EB == 16) ? 8 : 16;  // 32 registers of entries per batch
-    auto compute = [&](const uint4 (&c)[R][LOADS], int chunk, int bufi) {
-      const int m0 = chunk * kChunkRows + wm * RW;
-      const uint8_t* bsm = smem + bufi * book_bytes + rep_off;
+    for (int chunk = c0; chunk < c1; ++chunk, ++idx) {
+      const int s = idx % kStages;
+      uint4 nb[MAX_PER_THREAD];
+      bool sw = false;
+      if constexpr (TILE) {
+        sw = (chunk + 1 < c1) && region_of_chunk(chunk + 1) != region_of_chunk(chunk);
+        if (sw) book_issue(region_of_chunk(chunk + 1), nb);
+      }
+      mbar_wait(full0 + 8 * s, (idx / kStages) & 1);
+      const uint8_t* st = stages + s * STAGEB;
+      const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
       const int region = region_of_chunk(chunk);
+      const int m0 = chunk * kChunkRows + wm * RW;
 #pragma unroll
       for (int i = 0; i < LOADS; ++i) {
+        uint4 cw[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < R; ++r)
+          cw[r] = *reinterpret_cast<const uint4*>(st + r * LEVB + (wm * LOADS + i) * SEGB + g_local * 16);
+        uint4 xv[B][RPL / 8];
 #pragma unroll
-          for (int k0 = 0; k0 < RPL; k0 += NB) {
-            uint32_t e[NB][V / 2];
+        for (int b = 0; b < B; ++b)
 #pragma unroll
-            for (int kk = 0; kk < NB; ++kk) {
-              const int k = k0 + kk;
-              uint32_t code;
-              if constexpr (CBYTES == 2) {
-                const uint32_t w = (&c[r][i].x)[k / 2];
-                code = (k & 1) ? (w >> 16) : (w & 0xffff);
-              } else {
-                const uint32_t w = (&c[r][i].x)[k / 4];
-                code = (w >> (8 * (k % 4))) & 0xff;
-              }
-              bool in_smem = true;
-              if constexpr (GTIER) in_smem = code < (uint32_t)a.n_sh;
-              const uint8_t* src = in_smem
-                  ? bsm + (size_t)r * a.n_sh * 128 + ((size_t)code << 7)
-                  : reinterpret_cast<const uint8_t*>(a.books) +
-                        (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
-              if constexpr (EB == 16) {
-                const uint4 q = in_smem ? *reinterpret_cast<const uint4*>(src)
-                                        : __ldg(reinterpret_cast<const uint4*>(src));
-                e[kk][0] = q.x; e[kk][1] = q.y; e[kk][2] = q.z; e[kk][3] = q.w;
-              } else {
-                const uint2 q = in_smem ? *reinterpret_cast<const uint2*>(src)
-                                        : __ldg(reinterpret_cast<const uint2*>(src));
-                e[kk][0] = q.x; e[kk][1] = q.y;
-              }
+          for (int q = 0; q < RPL / 8; ++q)
+            xv[b][q] = __ldg(reinterpret_cast<const uint4*>(a.x + (int64_t)b * a.M + m0 + i * RPL) + q);
+        uint32_t hw[B][V / 2];  // fp16x2 window accumulators (H2 path)
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int j = 0; j < V / 2; ++j) hw[b][j] = 0u;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+          uint16_t xh[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const uint32_t w = (&xv[b][k / 8].x)[(k % 8) / 2];
+            xh[b] = (uint16_t)((k & 1) ? (w >> 16) : (w & 0xffff));
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            uint32_t code;
+            if constexpr (CBYTES == 2) {
+              const uint32_t w = (&cw[r].x)[k / 2];
+              code = (k & 1) ? (w >> 16) : (w & 0xffff);
+            } else {
+              const uint32_t w = (&cw[r].x)[k / 4];
+              code = (w >> (8 * (k % 4))) & 0xff;
             }
-            // activations of these NB rows (same address on every lane: broadcast)
-            uint32_t xw[B][NB / 2];
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-              const uint4* xp = reinterpret_cast<const uint4*>(a.x + (int64_t)b * a.M + m0 + i * RPL + k0);
-#pragma unroll
-              for (int q = 0; q < NB / 8; ++q) {
-                const uint4 t = __ldg(xp + q);
-                xw[b][4 * q] = t.x; xw[b][4 * q + 1] = t.y; xw[b][4 * q + 2] = t.z; xw[b][4 * q + 3] = t.w;
-              }
+            bool in_smem = true;
+            if constexpr (GTIER) in_smem = code < (uint32_t)a.n_sh;
+            uint32_t e[V / 2];
+            const uint8_t* src = in_smem ? bsm + (size_t)r * a.n_sh * 128 + ((size_t)code << 7)
+                                         : reinterpret_cast<const uint8_t*>(a.books) +
+                                               (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
+            if constexpr (EB == 16) {
+              const uint4 q = in_smem ? *reinterpret_cast<const uint4*>(src) : __ldg(reinterpret_cast<const uint4*>(src));
+              e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
+            } else {
+              const uint2 q = in_smem ? *reinterpret_cast<const uint2*>(src) : __ldg(reinterpret_cast<const uint2*>(src));
+              e[0] = q.x; e[1] = q.y;
             }
-#pragma unroll
-            for (int kk = 0; kk < NB; ++kk) {
+            if constexpr (H2) {
+              // packed fp16x2 FMA into an 8-row fp16 window (full-rate HFMA2; the
+              // mixed-precision FHFMA issues at a quarter of that rate on sm_100)
 #pragma unroll
               for (int b = 0; b < B; ++b) {
-                const uint16_t xh = (uint16_t)((kk & 1) ? (xw[b][kk / 2] >> 16) : (xw[b][kk / 2] & 0xffff));
+                const uint32_t x2 = (uint32_t)xh[b] * 0x10001u;
+#pragma unroll
+                for (int j = 0; j < V / 2; ++j) hw[b][j] = hfma2(e[j], x2, hw[b][j]);
+              }
+            } else {
+#pragma unroll
+              for (int b = 0; b < B; ++b)
 #pragma unroll
                 for (int j = 0; j < V / 2; ++j) {
-                  acc[b][2 * j] = fma_h((uint16_t)(e[kk][j] & 0xffff), xh, acc[b][2 * j]);
-                  acc[b][2 * j + 1] = fma_h((uint16_t)(e[kk][j] >> 16), xh, acc[b][2 * j + 1]);
+                  acc[b][2 * j] = fma_h((uint16_t)(e[j] & 0xffff), xh[b], acc[b][2 * j]);
+                  acc[b][2 * j + 1] = fma_h((uint16_t)(e[j] >> 16), xh[b], acc[b][2 * j + 1]);
                 }
-              }
+            }
+          }
+          if constexpr (H2) {
+            if ((k & 7) == 7) {  // flush the window into the fp32 accumulators (exact widening)
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int j = 0; j < V / 2; ++j) {
+                  acc[b][2 * j] = fma_h((uint16_t)(hw[b][j] & 0xffff), kHalfOne, acc[b][2 * j]);
+                  acc[b][2 * j + 1] = fma_h((uint16_t)(hw[b][j] >> 16), kHalfOne, acc[b][2 * j + 1]);
+                  hw[b][j] = 0u;
+                }
             }
           }
         }
       }
-    };
-
-    // one chunk step: on a codebook switch (tile sharing) the next region's book is
-    // loaded before and stored (into the idle buffer) after this chunk's compute
-    int cur_buf = 0;
-    auto step = [&](const uint4 (&c)[R][LOADS], int chunk) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
       if constexpr (TILE) {
-        uint4 nb[MAX_PER_THREAD];
-        const bool sw = (chunk + 1 < c1) && region_of_chunk(chunk + 1) != region_of_chunk(chunk);
-        if (sw) book_issue(region_of_chunk(chunk + 1), nb);
-        compute(c, chunk, cur_buf);
         if (sw) {
           book_commit(cur_buf ^ 1, nb);
-          __syncthreads();
+          csync();
           cur_buf ^= 1;
         }
-      } else {
-        compute(c, chunk, 0);
-      }
-    };
-
-    uint4 ca[R][LOADS], cb[R][LOADS];
-    load_codes(ca, c0);
-    if (!book_ready) {
-      uint4 bb[MAX_PER_THREAD];
-      book_issue(0, bb);
-      book_commit(0, bb);
-      __syncthreads();
-      book_ready = true;
-    }
-    if constexpr (TILE) {
-      uint4 bb[MAX_PER_THREAD];
-      book_issue(region_of_chunk(c0), bb);
-      __syncthreads();  // the previous span is done with both buffers
-      book_commit(0, bb);
-      __syncthreads();
-    }
-    if (!waited) {
-      pdl_wait();  // x / y / workspace may belong to the previous kernel
-      waited = true;
-    }
-    for (int ch = c0; ch < c1; ch += 2) {
-      if (ch + 1 < c1) load_codes(cb, ch + 1);
-      step(ca, ch);
-      if (ch + 1 < c1) {
-        if (ch + 2 < c1) load_codes(ca, ch + 2);
-        step(cb, ch + 1);
       }
     }
 
-    // ---- reduce the WM row-slabs of this span in a fixed order
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        red[((size_t)wm * B + b) * COLS + (wg * 32 + lane) * V + j] = acc[b][j];
-    __syncthreads();
+    // ---- reduce the WM row-slabs of this span in a fixed order, one batch row at a time
     const int n0 = cblk * COLS;
     const bool whole = (c0 == 0 && c1 == a.n_chunks);
     const int slot = cblk * a.n_chunks + c0;
-    for (int o = tid; o < B * COLS; o += kGemvThreads) {
-      const int b = o / COLS, col = o - (o / COLS) * COLS;
-      float s = 0.f;
 #pragma unroll
-      for (int w = 0; w < WM; ++w) s += red[((size_t)w * B + b) * COLS + col];
-      if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, s);
-      else a.part[(int64_t)slot * B * COLS + o] = s;
+    for (int b = 0; b < B; ++b) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) red[(size_t)wm * COLS + g_local * V + j] = acc[b][j];
+      csync();
+      for (int col = tid; col < COLS; col += kConsumers) {
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < WM; ++w) sum += red[(size_t)w * COLS + col];
+        if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, sum);
+        else a.part[((int64_t)slot * B + b) * COLS + col] = sum;
+      }
+      csync();
     }
     if (!whole) {
       if (tid == 0) a.span_len[slot] = c1 - c0;
       __threadfence();
-      __syncthreads();
-      if (tid == 0) s_last = (atomicAdd(a.counters + cblk, c1 - c0) + (c1 - c0) == a.n_chunks);
-      __syncthreads();
-      if (s_last) {
+      csync();
+      if (tid == 0) *s_last = (atomicAdd(a.counters + cblk, c1 - c0) + (c1 - c0) == a.n_chunks);
+      csync();
+      if (*s_last) {
         __threadfence();
-        for (int o = tid; o < B * COLS; o += kGemvThreads) {
+        for (int o = tid; o < B * COLS; o += kConsumers) {
           const int b = o / COLS, col = o - (o / COLS) * COLS;
-          float s = 0.f;
+          float sum = 0.f;
           for (int c = 0; c < a.n_chunks;) {
             const int sl = cblk * a.n_chunks + c;
-            s += __ldcg(a.part + (int64_t)sl * B * COLS + o);
+            sum += __ldcg(a.part + (int64_t)sl * B * COLS + o);
             c += __ldcg(a.span_len + sl);
           }
-          store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, s);
+          store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, sum);
         }
         if (tid == 0) a.counters[cblk] = 0;  // self-reset for the next launch
       }
     }
-    __syncthreads();  // red / s_last reuse by the next span
+    csync();  // red / s_last reuse by the next span
     u += c1 - c0;
   }
-  if (!waited) pdl_wait();
 }
 
-// ---------------------------------------------------------------------------
 // generic path
 
 constexpr int kGenericRowBlock = 4;
@@ -383,7 +417,7 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
 struct FastPlan {
   bool ok = false;
   int V = 0, cbytes = 0, R = 0, WG = 1;
-  bool tile = false, gtier = true;
+  bool tile = false, gtier = true, h2 = true;
   int n_sh = 0, n_cblk = 0, n_chunks = 0;
   size_t smem = 0;
 };
@@ -414,10 +448,12 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   if (L && (L->flags & VQB_FLAG_NO_SHARED)) n_sh = 0;
   p.n_sh = n_sh;
   p.gtier = !(t->max_code >= 0 && t->max_code < n_sh);
+  p.h2 = !(L && (L->flags & VQB_FLAG_EXACT_ACCUM));
   p.n_cblk = (int)(g.cols / cols_per_cta);
   p.n_chunks = (int)(g.rows / kChunkRows);
-  const int WM = 8 / p.WG;
-  p.smem = (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128 + (size_t)WM * rows * cols_per_cta * sizeof(float);
+  const int WM = kConsumerWarps / p.WG;
+  p.smem = (size_t)kStages * stage_bytes(p.R, p.cbytes, p.WG) + (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128 +
+           (size_t)WM * cols_per_cta * sizeof(float) + 2 * kStages * 8 + 16;
   p.ok = true;
   return p;
 }
@@ -454,7 +490,7 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
     auto it = occ_cache.find(key);
     if (it == occ_cache.end()) {
       // always opt in: static shared memory pushes even a 48 KB dynamic request over the default
-      VQB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      VQB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
       VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kGemvThreads, p.smem));
       occ_cache[key] = occ;
     } else {
@@ -480,8 +516,12 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
 }
 
 template <int V, int CBYTES, int R, int WG, bool TILE>
-static GemvKernel pick_kernel(int rows, bool gtier) {
-#define VQB_K(B) (gtier ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true> : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false>)
+static GemvKernel pick_kernel(int rows, bool gtier, bool h2) {
+#define VQB_K(B)                                                                        \
+  (gtier ? (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, true>                  \
+               : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, false>)                \
+         : (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, true>                 \
+               : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, false>))
   switch (rows) {
     case 1: return VQB_K(1);
     case 2: return VQB_K(2);
@@ -493,12 +533,12 @@ static GemvKernel pick_kernel(int rows, bool gtier) {
 
 static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
   // (V, code bytes, R, WG, tile-shared) combinations covering the BASELINE configs
-  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier);
+  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier, p.h2);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier, p.h2);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier, p.h2);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier, p.h2);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier, p.h2);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier, p.h2);
   return nullptr;
 }
 
@@ -588,9 +628,9 @@ int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
 
 int gemv_usage(VqbUsage* u) {
   cudaFuncAttributes at;
-  auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, true>;
+  auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, true, true>;
   VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
-  const size_t smem = 256 * 128 + 8 * 1 * 256 * 4;
+  const size_t smem = kStages * stage_bytes(1, 2, 1) + 256 * 128 + kConsumerWarps * 256 * 4 + 2 * kStages * 8 + 16;
   u->shared_bytes = (int)(at.sharedSizeBytes + smem);
   u->regs_per_thread = at.numRegs;
   u->threads_per_block = kGemvThreads;

@@ -172,12 +172,14 @@ def test_gemv_fast_fp16_output_and_plans(dev):
     x = O.round_f16(O.synthetic_tensor((shape[0],), 9))
     xt = torch.from_numpy(x).to(dev).half()
     ref = O.matmul_ref(x, dense)
-    for f in (1, 2, 8):
+    for grid in (0, 5, 37):
         for n_sh in (0, 64, 256, 1024):
-            L = ops.launch_struct(n_shared=n_sh if n_sh else None, split_factor=f, split_axis="M")
-            y = ops.vq_gemv(d, xt, out_dtype=torch.float16, launch=L)
-            assert N.last_kernel() == "gemv_fast"
-            assert O.rel_err(y.float().cpu().numpy(), ref) <= 2e-3, (f, n_sh)
+            for flags in (0, 4, 8):  # default / no PDL / exact fp32 accumulation
+                L = ops.launch_struct(n_shared=n_sh if n_sh else None, grid_limit=grid)
+                L.flags = flags
+                y = ops.vq_gemv(d, xt, out_dtype=torch.float16, launch=L)
+                assert N.last_kernel() == "gemv_fast"
+                assert O.rel_err(y.float().cpu().numpy(), ref) <= 2e-3, (grid, n_sh, flags)
 
 
 # ---- attention ------------------------------------------------------------------------------------

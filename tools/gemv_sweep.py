@@ -60,6 +60,9 @@ def main():
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     dev = torch.device("cuda", 0)
+    probe = torch.zeros(4, dtype=torch.int32, device=dev)
+    N.check(N.lib().vqb_debug_smem_base(probe.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    print(json.dumps({"dynamic_smem_base": int(probe[0])}), flush=True)
     cfg, work = CFGS[args.cfg]
     g = torch.Generator(device=dev)
     g.manual_seed(0)
