@@ -1,21 +1,451 @@
-// gemm.cu — prefill GEMM entry point (placeholder until the tcgen05 kernel lands):
-// routes to the generic fused kernel so the API is complete and parity-correct.
+// gemm.cu — prefill GEMM with VQ dequantisation fused into the tcgen05 operand
+// pipeline: Y(rows, N) = X(rows, M) @ dequant(W)(M, N).
+//
+// Replaces SimMachine._matmul/_mm_block (pkg/src/vqforge/sim.py:697-775) for
+// ComputeOp.gemm (dataflow.py:68-71); oracle reference_compute `a @ w`
+// (sim.py:136-144).
+//
+// B200 design. One CTA computes a 256 x 128 tile of Y with
+// two 128 x 128 fp32 accumulators in TMEM (256 of the 512 columns):
+//  * warp 0 — TMA producer: X tiles (256 rows x 64 K, fp16/bf16) are loaded with
+//    cp.async.bulk.tensor (SWIZZLE_128B) into a 4-stage ring; this is exactly the
+//    UMMA K-major SW128 canonical layout, so no reshuffle is needed.
+//  * warps 2-5 — dequantisation producers (the paper's "shared" fusion level:
+//    tcgen05 reads operands only from shared memory / TMEM): each lane takes one
+//    16-byte code word (8 K-rows of one 8-column sub-vector group, GEMV_IL layout),
+//    looks each code up in the replicated, bank-conflict-free shared codebook
+//    (csrc/gemv.cu) and stores the 16-byte fp16 entry straight into the UMMA
+//    MN-major SW128 layout of the W tile: one LDS.128 -> one STS.128 per code,
+//    both conflict-free. A proxy fence then hands the tile to the async proxy.
+//  * warp 1 — a single thread issues tcgen05.mma.cta_group::1.kind::f16
+//    (M=128, N=128, K=16) for both accumulators and commits each stage back to
+//    the producers through an mbarrier; the final commit releases the epilogue.
+//  * epilogue (warps 2-5 again, one TMEM lane quarter each): tcgen05.ld 32x32b,
+//    convert, store.
+#include <cuda.h>
+
+#include <mutex>
+
 #include "common.cuh"
 
 namespace vqb {
+
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast);
 
-int gemm_usage(VqbUsage* u) {
-  *u = VqbUsage{};
+constexpr int kGemmThreads = 192;   // 6 warps
+constexpr int kTileM = 256;         // rows (two 128-row accumulators)
+constexpr int kTileN = 128;         // output columns (16 sub-vector groups of 8)
+constexpr int kTileK = 64;          // reduction rows per stage (one 128-byte swizzle span)
+__host__ __device__ constexpr int gemm_stages(int R) { return R == 1 ? 4 : 3; }  // ring depth (smem)
+constexpr int kABytes = kTileM * kTileK * 2;   // 32 KB
+constexpr int kBBytes = kTileK * kTileN * 2;   // 16 KB
+constexpr int kBookEntries = 256;              // shared tier (replicated, 128 B per entry)
+constexpr int kBookBytes = kBookEntries * 128; // per level
+
+struct GemmArgs {
+  const uint8_t* codes;  // GEMV_IL (8 rows of u16 codes / 16 rows of u8 codes per 16-byte word)
+  int64_t level_bytes;
+  const uint16_t* books; // (R, K, 8) fp16 or bf16
+  void* y;
+  int y_dtype;
+  int rows, M, N, G, K, n_sh;
+};
+
+// ---- tcgen05 / TMA PTX wrappers ----------------------------------------------
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SM100 shared-memory matrix descriptor (cute::UMMA::SmemDescriptor): start>>4 [0,14),
+  // LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48), SWIZZLE_128B (2) [61,64)
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fff);
+  d |= (uint64_t)((lbo >> 4) & 0x3fff) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3fff) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store_row32(void* y, int y_dtype, int64_t off, const uint32_t (&v)[32]) {
+  (void)y_dtype;
+  if constexpr (sizeof(OutT) == 4) {
+    float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      p[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
+                         __uint_as_float(v[4 * i + 3]));
+  } else {
+    uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<OutT*>(y) + off);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float lo = __uint_as_float(v[8 * i + 2 * j]), hi = __uint_as_float(v[8 * i + 2 * j + 1]);
+        if constexpr (std::is_same<OutT, __half>::value) {
+          const __half2 h = __floats2half2_rn(lo, hi);
+          w[j] = *reinterpret_cast<const uint32_t*>(&h);
+        } else {
+          const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+          w[j] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+      }
+      p[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+template <int CBYTES, int R, bool BF16, typename OutT>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                                                                  GemmArgs a) {
+  constexpr int RPL = 16 / CBYTES;          // K-rows per 16-byte code word
+  constexpr int WORDS = (kTileK / RPL) * (kTileN / 8);  // code words per level per stage
+  constexpr int STG = gemm_stages(R);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* book = smem;                                      // R x 256 entries x 128 B (replicated)
+  uint8_t* sa = smem + R * kBookBytes;                       // STG x 32 KB (A)
+  uint8_t* sb = sa + STG * kABytes;                  // STG x 16 KB (B)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + STG * kBBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STG + 1);
+  const uint32_t full_a0 = smem_u32(bars), full_b0 = smem_u32(bars + STG);
+  const uint32_t empty0 = smem_u32(bars + 2 * STG), tmem_full = smem_u32(bars + 3 * STG);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_tiles_n = a.N / kTileN;
+  const int tile_n = blockIdx.x % n_tiles_n, tile_m = blockIdx.x / n_tiles_n;
+  const int row0 = tile_m * kTileM, n0 = tile_n * kTileN;
+  const int k_iters = a.M / kTileK;
+
+  // ---- setup: barriers, TMEM, replicated shared codebook
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STG; ++s) {
+      mbar_init(full_a0 + 8 * s, 1);
+      mbar_init(full_b0 + 8 * s, 4);  // one arrive per dequant warp
+      mbar_init(empty0 + 8 * s, 1);   // tcgen05.commit
+    }
+    mbar_init(tmem_full, 1);
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int idx = tid; idx < R * a.n_sh; idx += kGemmThreads) {
+    const int r = idx / a.n_sh, e = idx - r * a.n_sh;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.books + ((int64_t)r * a.K + e) * 8));
+    uint8_t* row = book + ((size_t)r * kBookEntries + e) * 128;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(row + ((q + e) & 7) * 16) = v;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer (X tiles) =====
+    if (lane == 0) {
+      for (int it = 0; it < k_iters; ++it) {
+        const int s = it % STG;
+        mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
+        mbar_arrive_expect_tx(full_a0 + 8 * s, kABytes);
+        tma_load_2d(smem_u32(sa + s * kABytes), &tmap_x, it * kTileK, row0, full_a0 + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    // kind::f16, D fp32, A K-major, B MN-major, N = 128, M = 128
+    const uint32_t fmt = BF16 ? 1u : 0u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
+                           ((uint32_t)(kTileN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    if (lane == 0) {
+      for (int it = 0; it < k_iters; ++it) {
+        const int s = it % STG;
+        const uint32_t ph = (it / STG) & 1;
+        mbar_wait(full_a0 + 8 * s, ph);
+        mbar_wait(full_b0 + 8 * s, ph);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sa + s * kABytes), b_base = smem_u32(sb + s * kBBytes);
+#pragma unroll
+        for (int k = 0; k < kTileK / 16; ++k) {
+          // B: MN-major SW128, atoms of 8 K-rows x 64 columns (1 KB); LBO = column-atom
+          // stride (1 KB), SBO = 8-row-group stride (2 KB); K=16 spans two row groups.
+          const uint64_t bdesc = umma_desc(b_base + k * 4096, 1024, 2048);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            // A: K-major SW128 rows of 128 B; SBO = 8-row-group stride (1 KB); K step = 32 B
+            const uint64_t adesc = umma_desc(a_base + h * 16384 + k * 32, 16, 1024);
+            umma_f16(tmem_base + h * kTileN, adesc, bdesc, idesc, (it | k) != 0);
+          }
+        }
+        umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs completed
+      }
+      umma_commit(tmem_full);
+    }
+  } else {
+    // ===== dequantisation producers (warps 2..5) =====
+    const int dw = warp - 2;
+    const int dtid = dw * 32 + lane;  // 0..127
+    for (int it = 0; it < k_iters; ++it) {
+      const int s = it % STG;
+      // issue the code-word loads before waiting for the stage to drain
+      uint4 cw[R][(WORDS + 127) / 128];
+#pragma unroll
+      for (int i = 0; i < (WORDS + 127) / 128; ++i) {
+        const int item = dtid + i * 128;
+        if (item < WORDS) {
+          const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
+          const int64_t word = ((int64_t)(it * kTileK / RPL + blk) * a.G + n0 / 8 + grp) * 16;
+#pragma unroll
+          for (int r = 0; r < R; ++r) cw[r][i] = ldg_stream(a.codes + r * a.level_bytes + word);
+        }
+      }
+      mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
+      uint8_t* btile = sb + s * kBBytes;
+#pragma unroll
+      for (int i = 0; i < (WORDS + 127) / 128; ++i) {
+        const int item = dtid + i * 128;
+        if (item < WORDS) {
+          const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
+          const int c = grp & 7, nb = grp >> 3;  // 16-byte chunk and 64-column atom
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) {
+            float f[8];
+            uint4 e;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              uint32_t code;
+              if constexpr (CBYTES == 2) {
+                const uint32_t w = (&cw[r][i].x)[k / 2];
+                code = (k & 1) ? (w >> 16) : (w & 0xffff);
+              } else {
+                const uint32_t w = (&cw[r][i].x)[k / 4];
+                code = (w >> (8 * (k % 4))) & 0xff;
+              }
+              const uint4 q = code < (uint32_t)a.n_sh
+                                  ? *reinterpret_cast<const uint4*>(book + ((size_t)r * kBookEntries + code) * 128 +
+                                                                     (lane & 7) * 16)
+                                  : __ldg(reinterpret_cast<const uint4*>(a.books + ((int64_t)r * a.K + code) * 8));
+              if constexpr (R == 1) {
+                e = q;
+              } else {
+                const uint32_t* qw = &q.x;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  float lo, hi;
+                  if constexpr (BF16) {
+                    lo = __uint_as_float(qw[j] << 16);
+                    hi = __uint_as_float(qw[j] & 0xffff0000u);
+                  } else {
+                    const __half2 hv = *reinterpret_cast<const __half2*>(&qw[j]);
+                    lo = __low2float(hv);
+                    hi = __high2float(hv);
+                  }
+                  if (r == 0) {
+                    f[2 * j] = 0.0f + lo;
+                    f[2 * j + 1] = 0.0f + hi;
+                  } else {
+                    f[2 * j] += lo;
+                    f[2 * j + 1] += hi;
+                  }
+                }
+              }
+            }
+            if constexpr (R > 1) {
+              uint32_t o[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                if constexpr (BF16) {
+                  const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+                  o[j] = *reinterpret_cast<const uint32_t*>(&h);
+                } else {
+                  const __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+                  o[j] = *reinterpret_cast<const uint32_t*>(&h);
+                }
+              }
+              e = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            const int r = blk * RPL + k;  // K-row within the stage
+            uint8_t* dst = btile + ((r >> 3) * (kTileN / 64) + nb) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4*>(dst) = e;
+          }
+        }
+      }
+      fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full_b0 + 8 * s);
+    }
+
+    // ===== epilogue: TMEM -> registers -> global =====
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = row0 + h * 128 + quarter * 32 + lane;
+#pragma unroll
+      for (int cc = 0; cc < kTileN / 32; ++cc) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + h * kTileN + cc * 32;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < a.rows) store_row32<OutT>(a.y, a.y_dtype, (int64_t)row * a.N + n0 + cc * 32, v);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static size_t gemm_smem(int R) {
+  return (size_t)R * kBookBytes + gemm_stages(R) * (kABytes + kBBytes) + (3 * gemm_stages(R) + 1) * 8 + 16;
+}
+
+static bool gemm_fast_ok(const Geom& g, const VqbTensor* w, int x_dtype, const VqbLaunch* L) {
+  if (L && (L->flags & VQB_FLAG_FORCE_GENERIC)) return false;
+  if (w->layout != VQB_LAYOUT_GEMV_IL || g.v != 8 || g.sharing != VQB_SHARE_WHOLE) return false;
+  if (!(g.R == 1 || g.R == 2)) return false;
+  if (!(g.bits == 8 || (g.bits == 16 && g.R == 1))) return false;
+  if (!((w->codebook_dtype == VQB_F16 && x_dtype == VQB_F16) || (w->codebook_dtype == VQB_BF16 && x_dtype == VQB_BF16)))
+    return false;
+  if (g.rows % kTileK != 0 || g.cols % kTileN != 0) return false;
+  return true;
+}
+
+template <int CBYTES, int R, bool BF16, typename OutT>
+static int launch_gemm_t(const CUtensorMap& map, const GemmArgs& a, int grid, cudaStream_t st) {
+  auto kern = gemm_tc_kernel<CBYTES, R, BF16, OutT>;
+  const size_t smem = gemm_smem(R);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  if (attr_err != cudaSuccess) return cuda_error(attr_err, "cudaFuncSetAttribute(gemm_tc_kernel)");
+  kern<<<grid, kGemmThreads, smem, st>>>(map, a);
+  VQB_LAUNCH_CHECK("gemm_tc_kernel");
+  set_kernel("gemm_tc");
   return VQB_OK;
 }
+
+template <int CBYTES, int R, bool BF16>
+static int launch_gemm_out(const CUtensorMap& map, const GemmArgs& a, int grid, cudaStream_t st) {
+  if (a.y_dtype == VQB_F32) return launch_gemm_t<CBYTES, R, BF16, float>(map, a, grid, st);
+  if (a.y_dtype == VQB_F16) return launch_gemm_t<CBYTES, R, BF16, __half>(map, a, grid, st);
+  return launch_gemm_t<CBYTES, R, BF16, __nv_bfloat16>(map, a, grid, st);
+}
+
+int gemm_usage(VqbUsage* u) {
+  cudaFuncAttributes at;
+  auto k = gemm_tc_kernel<2, 1, false, float>;
+  VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
+  u->shared_bytes = (int)(at.sharedSizeBytes + gemm_smem(1));
+  u->regs_per_thread = at.numRegs;
+  u->threads_per_block = kGemmThreads;
+  u->max_blocks_per_sm = 1;
+  return VQB_OK;
+}
+
 }  // namespace vqb
+
+using namespace vqb;
 
 extern "C" int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows, void* d_y,
                         int32_t y_dtype, const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
+  Geom g;
+  int s = make_geom(w, &g);
+  if (s) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (g.ndim == 2 && rows >= 1 && y_dtype >= VQB_F32 && y_dtype <= VQB_BF16 && gemm_fast_ok(g, w, x_dtype, launch)) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)g.rows, (cuuint64_t)rows};          // {K = M, rows}
+    const cuuint64_t strides[1] = {(cuuint64_t)g.rows * 2};                      // bytes between rows
+    const cuuint32_t box[2] = {(cuuint32_t)kTileK, (cuuint32_t)kTileM};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&map, x_dtype == VQB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                      const_cast<void*>(d_x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    GemmArgs a;
+    a.codes = reinterpret_cast<const uint8_t*>(w->d_codes);
+    a.level_bytes = g.S * g.code_bytes;
+    a.books = reinterpret_cast<const uint16_t*>(w->d_codebooks);
+    a.y = d_y;
+    a.y_dtype = y_dtype;
+    a.rows = rows;
+    a.M = (int)g.rows;
+    a.N = (int)g.cols;
+    a.G = (int)g.gpr;
+    a.K = g.K;
+    a.n_sh = std::min(g.K, kBookEntries);
+    const int grid = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
+    const bool bf = w->codebook_dtype == VQB_BF16;
+    if (g.bits == 16) return bf ? launch_gemm_out<2, 1, true>(map, a, grid, st) : launch_gemm_out<2, 1, false>(map, a, grid, st);
+    if (g.R == 1) return bf ? launch_gemm_out<1, 1, true>(map, a, grid, st) : launch_gemm_out<1, 1, false>(map, a, grid, st);
+    return bf ? launch_gemm_out<1, 2, true>(map, a, grid, st) : launch_gemm_out<1, 2, false>(map, a, grid, st);
+  }
   VqbLaunch l = launch ? *launch : VqbLaunch{};
   l.flags |= VQB_FLAG_FORCE_GENERIC;
-  return vqb::gemv_dispatch(w, d_x, x_dtype, rows, d_y, y_dtype, &l, d_ws, ws_bytes,
-                            reinterpret_cast<cudaStream_t>(stream), nullptr);
+  return gemv_dispatch(w, d_x, x_dtype, rows, d_y, y_dtype, &l, d_ws, ws_bytes, st, nullptr);
 }

@@ -256,3 +256,37 @@ def test_shape_errors(dev):
     d = DeviceVQTensor.from_quantized(c.quantized(), device=dev)
     with pytest.raises(ShapeError):
         ops.vq_gemv(d, torch.zeros(c.shape[0] + 1, device=dev, dtype=torch.float16))
+
+
+# ---- prefill GEMM on tcgen05 --------------------------------------------------------------------
+
+GEMM_CASES = [
+    # (label, shape (M, N), v, bits, R, working set, rows)
+    ("C2_quip2", (1024, 512), 8, 16, 1, 256, 256),
+    ("C2_quip2_ragged_rows", (512, 384), 8, 16, 1, 256, 100),
+    ("C2_quip2_full_table", (256, 256), 8, 16, 1, None, 64),   # codes beyond the shared tier
+    ("C3_aqlm2x8", (1024, 256), 8, 8, 2, None, 300),
+    ("aqlm1x8", (768, 640), 8, 8, 1, None, 512),
+]
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("label,shape,v,bits,r,work,rows", GEMM_CASES)
+def test_gemm_tcgen05(label, shape, v, bits, r, work, rows, dtype, dev):
+    from paper_2503_02236_b200.codec import VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    tdt = getattr(torch, dtype)
+    cfg = VQConfig(v, bits, r)
+    nreg = 1
+    codes, books = O.synthetic_codes_books(shape, v, bits, r, nreg, 21, working_entries=work)
+    # the device codebook dtype is the operand dtype; the oracle sees the same rounding
+    books = torch.from_numpy(books).to(tdt).float().numpy()
+    dense = O.dequantize(codes, books, shape, v, nreg, O.region_ids(shape, v, "whole"))
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev, codebook_dtype=dtype)
+    x = torch.from_numpy(O.synthetic_tensor((rows, shape[0]), 22)).to(tdt)
+    ref = O.matmul_ref(x.float().numpy(), dense)
+    for out_dtype in (torch.float32, tdt):
+        y = ops.vq_gemm(d, x.to(dev), out_dtype=out_dtype)
+        assert N.last_kernel() == "gemm_tc", N.last_kernel()
+        tol = 2e-3 if dtype == "float16" else 1.6e-2
+        assert O.rel_err(y.float().cpu().numpy(), ref) <= tol, (label, out_dtype)
