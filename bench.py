@@ -110,25 +110,33 @@ def dist_env():
 # ---------------------------------------------------------------------------------------------------
 # CPU legs (oracle port: the reference's algorithm restated, V/codec.py:391-408 + V/sim.py:133-144)
 
+_CPU_CASE = {}
+
+
 def cpu_sample(seconds_budget=12.0):
-    """Oracle dequantize + fp32 GEMV of one 4096x4096 q_proj at the workload config, repeated
-    up to ~seconds_budget; returns (GB/s, sample description, cores)."""
+    """The reference algorithm (dequantize, V/codec.py:391-408, then the fp32 matmul of
+    reference_compute, V/sim.py:136-144) restated in C with OpenMP on all host cores, on one
+    4096x4096 q_proj of the workload config, repeated for ~seconds_budget.
+    Returns (GB/s over the same algorithmic bytes, sample description, threads)."""
+    from oracle import c_oracle as C
     from oracle import vq_oracle as O
 
     m, n, v = 4096, 4096, 8
-    codes, books = O.synthetic_codes_books((m, n), v, 16, 1, 1, 0, working_entries=WORK)
-    regions = np.zeros(m * n // v, dtype=np.int64)
-    x = O.synthetic_tensor((m,), 2)
+    if not _CPU_CASE:
+        codes, books = O.synthetic_codes_books((m, n), v, 16, 1, 1, 0, working_entries=WORK)
+        _CPU_CASE.update(codes=codes, books=books, regions=np.zeros(m * n // v, dtype=np.int32),
+                         x=O.synthetic_tensor((m,), 2))
+    c = _CPU_CASE
     reps, t0 = 0, time.perf_counter()
     while True:
-        w = O.dequantize(codes, books, (m, n), v, 1, regions)
-        O.matmul_ref(x, w)
+        C.gemv(c["codes"], c["books"], (m, n), v, 1, c["regions"], c["x"])
         reps += 1
-        if time.perf_counter() - t0 > seconds_budget or reps >= 50:
+        if time.perf_counter() - t0 > seconds_budget or reps >= 2000:
             break
     dt = (time.perf_counter() - t0) / reps
     gbs = algorithmic_bytes(m, n) / dt / 1e9
-    return gbs, f"numpy oracle dequantize+matmul of one 4096x4096 q_proj, {reps} reps, {dt*1e3:.1f} ms each", 1
+    return gbs, (f"C/OpenMP oracle (dequantize + fp32 matmul) of one 4096x4096 quip2 q_proj, {reps} reps, "
+                 f"{dt*1e3:.2f} ms each"), C.threads()
 
 
 def run_reference(args):
@@ -149,7 +157,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "llama7b-decode-linears quip2 VQ<8,16,1> ws256 batch1 (sampled on q_proj)"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+                         "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -317,12 +326,26 @@ def run_impl(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # tensor parallelism: every rank holds N/world columns of every linear; the step
+    # ends with the column all-gather of all outputs (NCCL over NVLink)
+    gathered = torch.empty(world * stack.y.numel(), dtype=stack.y.dtype, device=dev) if world > 1 else None
+
+    def step():
+        stack.replay()
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered, stack.y)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     clocks = Clocks(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
     for _ in range(args.steps):
-        stack.replay()
+        step()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -366,7 +389,7 @@ def run_impl(args):
             cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": "llama7b-decode-linears quip2 VQ<8,16,1> ws256 batch1",
                        "layers": N_LAYERS, "launches_per_step": stack.n_launches,

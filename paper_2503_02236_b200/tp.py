@@ -1,0 +1,213 @@
+"""Tensor parallelism for the fused VQ layers (one process per GPU, NCCL over NVLink).
+
+The reference is single-process; the north star shards layers
+tensor-parallel: GEMV/GEMM by output channel (column-parallel, all-gather) or by
+input channel (row-parallel, all-reduce), decode attention by head. Sub-vectors
+run along the last axis (pkg/src/vqforge/codec.py:229-236), so a column shard
+must start on a sub-vector boundary — and on a codebook-region boundary for tile
+or channel-group sharing, because a shard is itself a reference-format
+QuantizedTensor whose regions restart at its own column 0 (codec.py:135-177).
+Whole-tensor codebooks are replicated to every rank.
+
+Local compute defaults to the CUDA kernels; ``compute`` can be replaced (the
+multi-process CPU tests run the sharding and collectives with the oracle).
+"""
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .codec import Codebook, QuantizedTensor, region_count
+from .errors import ConfigError, ShapeError
+
+
+def _split(extent: int, world: int, rank: int, align: int):
+    if extent % world:
+        raise ShapeError(f"extent {extent} not divisible by tensor-parallel size {world}")
+    part = extent // world
+    if part % align:
+        raise ConfigError(f"shard width {part} is not a multiple of {align} (sub-vector / codebook region)")
+    return rank * part, (rank + 1) * part
+
+
+def _col_align(q: QuantizedTensor) -> int:
+    sh = q.config.sharing
+    if sh.kind == "tile":
+        return sh.tile_cols
+    if sh.kind == "channel_group":
+        return sh.group_width
+    return q.config.vector_size
+
+
+def shard_columns(q: QuantizedTensor, rank: int, world: int) -> QuantizedTensor:
+    """Column-parallel shard of a 2-D weight (M, N): columns [n0, n1) with their books."""
+    if len(q.shape) != 2:
+        raise ShapeError("column sharding expects a 2-D (M, N) weight")
+    m, n = q.shape
+    v = q.config.vector_size
+    n0, n1 = _split(n, world, rank, _col_align(q))
+    per_row = n // v
+    codes = q.codes.reshape(q.config.residuals, m, per_row)[:, :, n0 // v:n1 // v]
+    codes = np.ascontiguousarray(codes).reshape(q.config.residuals, -1)
+    shape = (m, n1 - n0)
+    nreg = region_count(shape, q.config)
+    sh = q.config.sharing
+    if sh.kind == "whole":
+        books = list(q.codebooks)
+    else:
+        # regions of the shard, expressed in the parent's region numbering
+        if sh.kind == "tile":
+            n_tc_parent = -(-n // sh.tile_cols)
+            n_tr = -(-m // sh.tile_rows)
+            n_tc = (n1 - n0) // sh.tile_cols
+            parent = [tr * n_tc_parent + n0 // sh.tile_cols + tc for tr in range(n_tr) for tc in range(n_tc)]
+        else:
+            g0 = n0 // sh.group_width
+            parent = [g0 + gi for gi in range(nreg)]
+        books = []
+        for lvl in range(q.config.residuals):
+            for local, p in enumerate(parent):
+                src = q.codebook_for(lvl, p)
+                books.append(Codebook(src.entries, lvl, local))
+    return QuantizedTensor(codes, shape, q.config, books, nreg)
+
+
+def shard_rows(q: QuantizedTensor, rank: int, world: int) -> QuantizedTensor:
+    """Row-parallel shard (input channels [m0, m1)) of a 2-D weight."""
+    if len(q.shape) != 2:
+        raise ShapeError("row sharding expects a 2-D (M, N) weight")
+    m, n = q.shape
+    sh = q.config.sharing
+    align = sh.tile_rows if sh.kind == "tile" else 1
+    m0, m1 = _split(m, world, rank, align)
+    per_row = n // q.config.vector_size
+    codes = q.codes.reshape(q.config.residuals, m, per_row)[:, m0:m1, :]
+    codes = np.ascontiguousarray(codes).reshape(q.config.residuals, -1)
+    shape = (m1 - m0, n)
+    nreg = region_count(shape, q.config)
+    if sh.kind == "tile":
+        n_tc = -(-n // sh.tile_cols)
+        tr0 = m0 // sh.tile_rows
+        books = [Codebook(q.codebook_for(lvl, (tr0 + r // n_tc) * n_tc + r % n_tc).entries, lvl, r)
+                 for lvl in range(q.config.residuals) for r in range(nreg)]
+    else:
+        books = list(q.codebooks)
+    return QuantizedTensor(codes, shape, q.config, books, nreg)
+
+
+def shard_heads(q: QuantizedTensor, rank: int, world: int) -> QuantizedTensor:
+    """Head shard of a (B, H, T, C) KV tensor; channel-group books move with their heads."""
+    if len(q.shape) != 4:
+        raise ShapeError("head sharding expects a (B, H, T, C) tensor")
+    b, h, t, c = q.shape
+    h0, h1 = _split(h, world, rank, 1)
+    v = q.config.vector_size
+    codes = q.codes.reshape(q.config.residuals, b, h, t, c // v)[:, :, h0:h1]
+    codes = np.ascontiguousarray(codes).reshape(q.config.residuals, -1)
+    shape = (b, h1 - h0, t, c)
+    nreg = region_count(shape, q.config)
+    sh = q.config.sharing
+    if sh.kind == "channel_group":
+        per_head = c // sh.group_width
+        books = [Codebook(q.codebook_for(lvl, (h0 * per_head) + r).entries, lvl, r)
+                 for lvl in range(q.config.residuals) for r in range(nreg)]
+    elif sh.kind == "whole":
+        books = list(q.codebooks)
+    else:
+        raise ConfigError("tile-shared KV tensors are shared across heads; shard them by columns instead")
+    return QuantizedTensor(codes, shape, q.config, books, nreg)
+
+
+def _default_linear(w, x):
+    from .device import DeviceVQTensor
+    from .ops import vq_gemm, vq_gemv
+
+    d = w if isinstance(w, DeviceVQTensor) else DeviceVQTensor.from_quantized(w, device=x.device)
+    return vq_gemv(d, x) if (x.dim() == 1 or x.shape[0] <= 8) else vq_gemm(d, x)
+
+
+def _default_attention(k, v, q):
+    from .device import DeviceVQTensor
+    from .ops import vq_attention
+
+    kd = k if isinstance(k, DeviceVQTensor) else DeviceVQTensor.from_quantized(k, device=q.device)
+    vd = v if isinstance(v, DeviceVQTensor) else DeviceVQTensor.from_quantized(v, device=q.device)
+    return vq_attention(kd, vd, q)
+
+
+@dataclass
+class TPLinear:
+    """A VQ linear layer sharded over a process group.
+
+    ``mode="column"``: every rank holds N/world output columns; ``forward`` all-gathers
+    the full output. ``mode="row"``: every rank holds M/world input rows and takes the
+    matching slice of x; ``forward`` all-reduces the partial sums.
+    """
+
+    weight: object
+    mode: str = "column"
+    group: Optional[object] = None
+    compute: Callable = _default_linear
+
+    @classmethod
+    def from_full(cls, q: QuantizedTensor, mode="column", group=None, compute=None, device=None):
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        shard = shard_columns(q, rank, world) if mode == "column" else shard_rows(q, rank, world)
+        w = shard
+        if compute is None:
+            from .device import DeviceVQTensor
+            w = DeviceVQTensor.from_quantized(shard, device=device)
+        return cls(w, mode, group, compute or _default_linear)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        world = dist.get_world_size(self.group)
+        if self.mode == "column":
+            y = self.compute(self.weight, x).contiguous()
+            out = torch.empty((world * y.shape[0],) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
+            dist.all_gather_into_tensor(out, y, group=self.group)
+            out = out.view((world,) + tuple(y.shape))
+            # (world, ..., N/world) -> (..., N)
+            return torch.movedim(out, 0, -2).reshape(tuple(y.shape[:-1]) + (world * y.shape[-1],))
+        rank = dist.get_rank(self.group)
+        m_local = self.weight.shape[0]
+        xs = x[..., rank * m_local:(rank + 1) * m_local].contiguous()
+        y = self.compute(self.weight, xs).contiguous()
+        dist.all_reduce(y, group=self.group)
+        return y
+
+    __call__ = forward
+
+
+@dataclass
+class TPAttention:
+    """Decode attention sharded by head; the output is all-gathered over heads."""
+
+    k: object
+    v: object
+    group: Optional[object] = None
+    compute: Callable = _default_attention
+
+    @classmethod
+    def from_full(cls, kq: QuantizedTensor, vq: QuantizedTensor, group=None, compute=None, device=None):
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        ks, vs = shard_heads(kq, rank, world), shard_heads(vq, rank, world)
+        if compute is None:
+            from .device import DeviceVQTensor
+            ks = DeviceVQTensor.from_quantized(ks, device=device)
+            vs = DeviceVQTensor.from_quantized(vs, device=device)
+        return cls(ks, vs, group, compute or _default_attention)
+
+    def forward(self, q: torch.Tensor) -> torch.Tensor:
+        world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        h_local = self.k.shape[1]
+        qs = q[:, rank * h_local:(rank + 1) * h_local].contiguous()
+        o = self.compute(self.k, self.v, qs).contiguous()
+        out = torch.empty((world * o.shape[0],) + tuple(o.shape[1:]), dtype=o.dtype, device=o.device)
+        dist.all_gather_into_tensor(out, o, group=self.group)
+        out = out.view((world,) + tuple(o.shape))
+        return torch.movedim(out, 0, 1).reshape(o.shape[0], world * h_local, o.shape[2])
+
+    __call__ = forward
