@@ -145,9 +145,10 @@ const char* vqb_last_kernel(void);
 int vqb_dequant(const VqbTensor* t, void* d_out, int32_t out_dtype, void* stream);
 
 /* Workspace bytes a fused call needs. The first VQB_WS_COUNTER_BYTES of every
- * workspace hold split-arrival counters: zero them once when the workspace is
- * allocated; kernels reset them after use and never write anything else there. */
-#define VQB_WS_COUNTER_BYTES 65536
+ * workspace are the self-resetting head: split-arrival counters (attention) and
+ * tagged split partials (GEMV). Zero it once when the workspace is allocated;
+ * kernels restore it to zero after use and never leave anything else there. */
+#define VQB_WS_COUNTER_BYTES 4194304
 /* Workspace bytes a fused call needs (split partials + arrival counters).
  * kind = VQB_KERNEL_*; rows = batch rows (GEMV/GEMM) or B*H (attention). */
 int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t rows,

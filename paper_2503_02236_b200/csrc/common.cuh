@@ -91,9 +91,14 @@ __device__ __forceinline__ int region_of(const Geom& g, int64_t s) {
 // Offset (in codes) of code (level r, sub-vector s) inside an interleaved layout.
 __device__ __forceinline__ int64_t il_offset(const Geom& g, int r, int64_t s) {
   if (g.layout == VQB_LAYOUT_GEMV_IL) {
+    // column-blocked: per level [N/256 column blocks][M/rpl row groups][256/v groups][rpl rows]
+    // (the last block may be narrower), so one block's chunk of rows is contiguous
     const int rpl = 16 / g.code_bytes;
+    const int64_t gcb = 256 / g.v;
     const int64_t m = s / g.gpr, grp = s - (s / g.gpr) * g.gpr;
-    return (int64_t)r * g.S + ((m / rpl) * g.gpr + grp) * rpl + (m % rpl);
+    const int64_t cb = grp / gcb, gi = grp - cb * gcb;
+    const int64_t wb = min(gcb, g.gpr - cb * gcb);
+    return (int64_t)r * g.S + cb * gcb * g.rows + ((m / rpl) * wb + gi) * rpl + (m % rpl);
   }
   // KV_IL: per (b,h), per 32-token batch: [Q = 2*GPL][32 lanes][16 bytes]; lane l owns
   // groups l + 32j and stores token (i ^ l) of the batch at slot i, byte i*GPL + j
@@ -158,6 +163,20 @@ __device__ __forceinline__ float fma_h(uint16_t a, uint16_t b, float c) {
 __device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// HFMA2 with the activation half (lo or hi of a packed pair) broadcast to both
+// lanes: ptxas folds the splat into the .H0_H0 / .H1_H1 operand selector.
+template <int HI>
+__device__ __forceinline__ uint32_t hfma2_bcast(uint32_t a, uint32_t xw, uint32_t c) {
+  uint32_t d;
+  if constexpr (HI)
+    asm("{.reg .f16 xl, xh; .reg .b32 xx; mov.b32 {xl, xh}, %2; mov.b32 xx, {xh, xh}; fma.rn.f16x2 %0, %1, xx, %3;}"
+        : "=r"(d) : "r"(a), "r"(xw), "r"(c));
+  else
+    asm("{.reg .f16 xl, xh; .reg .b32 xx; mov.b32 {xl, xh}, %2; mov.b32 xx, {xl, xl}; fma.rn.f16x2 %0, %1, xx, %3;}"
+        : "=r"(d) : "r"(a), "r"(xw), "r"(c));
   return d;
 }
 

@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         const int item = dtid + i * 128;
         if (item < WORDS) {
           const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
-          const int64_t word = ((int64_t)(it * kTileK / RPL + blk) * a.G + n0 / 8 + grp) * 16;
+          // column-blocked GEMV_IL: 32 groups (256 columns) per block, blocks of M/RPL row groups
+          const int gg = n0 / 8 + grp, cb = gg / 32, gi = gg % 32, wb = min(32, a.G - cb * 32);
+          const int64_t word = ((int64_t)cb * 32 * (a.M / RPL) + (int64_t)(it * kTileK / RPL + blk) * wb + gi) * 16;
 #pragma unroll
           for (int r = 0; r < R; ++r) cw[r][i] = ldg_stream(a.codes + r * a.level_bytes + word);
         }

@@ -6,11 +6,11 @@
 // (verify.py:200-215).
 //
 // Fast kernel (B200 design):
-//  * TMA-staged index stream — a producer warp streams each work unit's codes
-//    (GEMV_IL layout: 512-byte contiguous row-group segments) into a 4-stage
-//    shared-memory ring with cp.async.bulk + mbarrier transaction counts, so a
-//    CTA keeps up to 64 KB of code loads in flight independent of registers;
-//    consumer warps read their 16-byte code words from shared memory.
+//  * TMA-staged index stream — the GEMV_IL layout is column-blocked (256 output
+//    columns per block, row groups of 8/16 rows inside), so one block's 256-row
+//    chunk is a single contiguous run: a producer warp streams each chunk with ONE
+//    cp.async.bulk per level (+ one per activation row) into a 3-stage ring with
+//    mbarrier transaction counts; consumer warps read 16-byte code words from it.
 //  * codebook cache — the first n_shared entries of every codebook a CTA needs
 //    live in shared memory REPLICATED 128/EB times (EB = entry bytes): entry e
 //    owns one 128-byte bank row and lane l reads replica (l mod 128/EB), so a
@@ -18,17 +18,16 @@
 //    LDS.128 quarter-warp / 16 lanes of an LDS.64 half-warp always hit distinct
 //    bank groups). Entries >= n_shared come from the global/L2 tier; when the
 //    tensor's max code is known to be < n_shared the global tier is compiled out.
-//  * codebook-centric dataflow — work units are (column block of 32*WG
-//    sub-vector columns, 256-row chunk); a tile-shared book (GPTVQ) covers whole
-//    chunks, the next region's book is prefetched while the current chunk
-//    computes; whole-tensor books are loaded once per persistent CTA.
-//  * persistent CTAs own contiguous unit ranges and accumulate consecutive
-//    chunks of a column block in registers; spans that do not cover a whole
-//    column block leave a partial that the last arriving CTA sums in chunk order
-//    (deterministic, like the reference's ordered split reduction, sim.py:735).
+//  * codebook-centric, persistent stream-K dataflow — one CTA per SM owns a
+//    contiguous range of (column block, chunk) units (balanced to one unit); a
+//    whole-tensor book is loaded once per CTA, a tile-shared book (GPTVQ) is
+//    prefetched for the next unit while the current one computes. A column block
+//    split across CTAs is finished by the CTA holding its first chunk, which adds
+//    the later CTAs' published fp32 partials in chunk order (deterministic, like
+//    the reference's ordered split reduction, sim.py:735).
 //  * programmatic dependent launch — the code stream and the codebook fill start
-//    before griddepcontrol.wait, overlapping the previous kernel's tail; x, y and
-//    the workspace are only touched after it.
+//    before griddepcontrol.wait, overlapping the previous kernel's tail; x and y
+//    are only touched after it.
 //  * register-level fusion — a lane owns one sub-vector column and multiplies
 //    the looked-up fp16 entry straight into fp32 accumulators with the sm_100
 //    mixed-precision FMA (fma.rn.f32.f16): no staging, no shuffles.
@@ -36,6 +35,7 @@
 // Generic kernel: any VQConfig / sharing / layout / dtype, fp32 math on the
 // bit-exact dequantised W, used for parity mode (fp32 codebooks) and for
 // configurations outside the fast table.
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -47,26 +47,66 @@ constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kGemvThreads = kConsumers + 32;  // + one producer warp
 constexpr int kChunkRows = 256;
-constexpr int kStages = 4;
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
-// bytes of one work unit's codes (= one ring stage): R levels x 256 rows x 32*WG columns
+// ring depth: 3 stages (2 for tile-shared books, whose double-buffered codebook
+// takes the room) keeps a CTA under half of the SM's shared memory, so the next
+// kernel's CTA (programmatic dependent launch) can be resident beside it
+__host__ __device__ constexpr int gemv_stages(bool tile) { return tile ? 3 : 6; }
+// bytes of one chunk's codes: R levels x 256 rows x 32*WG columns
 __host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG) { return R * cbytes * WG * kChunkRows * 32; }
+// a ring stage also carries the chunk's activations: B rows x 256 fp16
+__host__ __device__ constexpr int stage_total(int R, int cbytes, int WG, int B) {
+  return stage_bytes(R, cbytes, WG) + B * kChunkRows * 2;
+}
 
 struct GemvFastArgs {
-  const uint8_t* codes;   // GEMV_IL, level r at codes + r * level_bytes
+  const uint8_t* codes;   // GEMV_IL (column-blocked), level r at codes + r * level_bytes
   int64_t level_bytes;
   const __half* books;    // (R*n_regions, K, V)
   const __half* x;        // (B, M)
   void* y;
   int y_dtype;
-  float* part;            // (n_cblk * n_chunks, B, COLS) span partials
-  int* span_len;          // (n_cblk * n_chunks) chunks covered by the partial at that slot
-  int* counters;          // (n_cblk) chunks reduced so far
   int M, N, G, K, n_regions;
   int tile_rows, tile_cols, n_tc;
   int n_chunks, n_cblk, n_sh;
+  unsigned long long* part;  // (grid, B, COLS) tagged partials {fp32 value, tag 1}, one slot per CTA,
+                             // in the self-resetting workspace head (zeroed by the consumer)
+  unsigned long long* trace;  // optional per-CTA phase timestamps (debug flag 32), 8 per CTA
+  int debug_nocompute;    // experiment: consumers only wait for and release the stages
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
+  if (tr) tr[blockIdx.x * 8 + slot] = gtimer();
+}
+// A partial travels as one 64-bit word {fp32 value, tag}: an aligned 8-byte store
+// is single-copy atomic, so a reader that sees the tag also sees the value — no
+// fence or flag round trip between producer and consumer.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long tag_partial(float v) {
+  return (1ull << 32) | (unsigned long long)__float_as_uint(v);
+}
+
+// Persistent stream-K decode GEMV. Work units are (column block, 256-row chunk),
+// ordered column-block major; CTA i owns the contiguous unit range
+// [i*U/grid, (i+1)*U/grid) and walks it as "spans" (maximal runs inside one column
+// block), accumulating a span in registers. A span that covers its whole column
+// block writes y. A column block split across CTAs is finished by the CTA holding
+// its first chunk — for that CTA it is the last span of its range — which adds the
+// later CTAs' fp32 partials (computed at the start of their ranges, so normally
+// already published) in chunk order: deterministic, like the reference's ordered
+// split reduction (sim.py:735), with no atomics and no extra launch.
 template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, bool H2>
 __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a) {
   constexpr int EB = V * 2;              // fp16 entry bytes
@@ -76,23 +116,32 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   constexpr int RW = kChunkRows / WM;    // rows per warp per chunk
   constexpr int LOADS = RW / RPL;        // code words per lane per level per chunk
   constexpr int COLS = 32 * WG * V;      // output columns per column block
-  constexpr int NSEG = kChunkRows / RPL; // row-group segments per level per unit
-  constexpr int SEGB = 32 * WG * 16;     // bytes per segment
-  constexpr int LEVB = NSEG * SEGB;      // bytes per level per unit
+  constexpr int GC = 32 * WG;            // sub-vector columns per column block
+  constexpr int NQ = V / 4;              // float4 per lane in the cross-warp reduction
+  constexpr int NSEG = kChunkRows / RPL; // row groups per chunk
+  constexpr int LEVB = NSEG * GC * 16;   // bytes per level per chunk (contiguous in GEMV_IL)
   constexpr int NBUF = TILE ? 2 : 1;     // codebook buffers
+  // WIDE book layout (every code < 256 is in shared memory): entry e owns a 256-byte
+  // row, half h = level (R == 2) or buffer (tile double buffering) holds its
+  // replicas, so a lookup address is ONE PRMT of the code byte and the lane's
+  // replica offset (the book base and the half fold into the LDS immediate/UR).
+  constexpr bool WIDE = !GTIER && R * NBUF <= 2;
   static_assert(LOADS >= 1 && RW % 8 == 0, "bad tiling");
   constexpr int STAGEB = R * LEVB;
   static_assert(STAGEB == stage_bytes(R, CBYTES, WG), "stage size");
-  static_assert(NSEG <= 32, "one segment per producer lane");
+  constexpr int XROWB = kChunkRows * 2;  // one batch row's activations per chunk
+  constexpr int STG = stage_total(R, CBYTES, WG, B);
+  static_assert(B <= 32, "one activation row per producer lane");
+  constexpr int kStages = gemv_stages(TILE);
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint8_t* stages = smem;                                        // kStages x STAGEB
-  uint8_t* books_s = smem + kStages * STAGEB;                    // NBUF x R x n_sh x 128
+  uint8_t* stages = smem;                                        // kStages x (codes | x)
+  uint8_t* books_s = smem + kStages * STG;                       // WIDE: 256 x 256 B; else NBUF x R x n_sh x 128
   const size_t book_bytes = (size_t)R * a.n_sh * 128;
-  float* red = reinterpret_cast<float*>(books_s + NBUF * book_bytes);  // WM * COLS
+  const size_t book_region = WIDE ? 65536 : NBUF * book_bytes;
+  float* red = reinterpret_cast<float*>(books_s + book_region);  // WM x COLS cross-warp partials
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + WM * COLS);       // full[kStages], empty[kStages]
-  int* s_last = reinterpret_cast<int*>(bars + 2 * kStages);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
 
   const int U = a.n_cblk * a.n_chunks;
@@ -100,6 +149,12 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
 
   if (tid == 0) {
+    trace_at(a.trace, 0);
+    if (a.trace) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+      a.trace[blockIdx.x * 8 + 7] = sm;
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, kConsumerWarps);
@@ -110,22 +165,44 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   pdl_launch_dependents();
 
   if (warp == kConsumerWarps) {
-    // ===== producer: stream each unit's code segments into the stage ring =====
-    for (int idx = 0; idx < u1 - u0; ++idx) {
-      const int u = u0 + idx;
-      const int cblk = u / a.n_chunks, chunk = u - cblk * a.n_chunks;
-      const int s = idx % kStages;
-      if (idx >= kStages) mbar_wait(empty0 + 8 * s, ((idx / kStages) + 1) & 1);
-      if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * s, STAGEB);
-      __syncwarp();
-      if (lane < NSEG) {
-        const int64_t rg = (int64_t)chunk * NSEG + lane;  // row-group index along M
+    // ===== producer: stream each unit's codes (one bulk copy per level: a column
+    // block's chunk is contiguous in the column-blocked GEMV_IL layout) and its
+    // activations into the ring. Codes do not depend on the previous kernel, so the
+    // first kStages units are requested before griddepcontrol.wait; activations
+    // (possibly written by the previous kernel) only after it.
+    const int n = u1 - u0;
+    auto issue_codes = [&](int idx) {
+      const int s = idx % kStages, u = u0 + idx;
+      const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
+      if (lane == 0) {
+        const int64_t off = ((int64_t)cb * GC * (a.M / RPL) + (int64_t)chunk * NSEG * GC) * 16;
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          tma_load_1d(smem_u32(stages + s * STAGEB + r * LEVB + lane * SEGB),
-                      a.codes + r * a.level_bytes + (rg * a.G + (int64_t)cblk * 32 * WG) * 16, SEGB,
-                      full0 + 8 * s);
+          tma_load_1d(smem_u32(stages + s * STG + r * LEVB), a.codes + r * a.level_bytes + off, LEVB, full0 + 8 * s);
       }
+    };
+    auto issue_x = [&](int idx) {
+      const int s = idx % kStages, u = u0 + idx;
+      const int chunk = u % a.n_chunks;
+      if (lane < B)
+        tma_load_1d(smem_u32(stages + s * STG + STAGEB + lane * XROWB),
+                    a.x + (int64_t)lane * a.M + (int64_t)chunk * kChunkRows, XROWB, full0 + 8 * s);
+    };
+    const int pre = min(n, kStages);
+    for (int idx = 0; idx < pre; ++idx) {
+      if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * idx, STG);
+      __syncwarp();
+      issue_codes(idx);
+    }
+    pdl_wait();
+    for (int idx = 0; idx < pre; ++idx) issue_x(idx);
+    for (int idx = kStages; idx < n; ++idx) {
+      const int s = idx % kStages;
+      mbar_wait(empty0 + 8 * s, ((idx / kStages) + 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * s, STG);
+      __syncwarp();
+      issue_codes(idx);
+      issue_x(idx);
     }
     return;
   }
@@ -133,6 +210,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   // ===== consumers =====
   const int wm = warp / WG, wg = warp % WG;
   const uint32_t rep_off = (uint32_t)(lane % REP) * EB;
+  const int g_local = wg * 32 + lane;
 
   constexpr int MAX_PER_THREAD = (1024 + kConsumers - 1) / kConsumers;  // n_sh * R <= 1024 entries
   auto book_issue = [&](int region, uint4 (&buf)[MAX_PER_THREAD]) {
@@ -157,7 +235,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
       const int idx = tid + k * kConsumers;
       if (idx < R * a.n_sh) {
         const int r = idx / a.n_sh, e = idx - r * a.n_sh;
-        uint8_t* row = books_s + bufi * book_bytes + ((size_t)r * a.n_sh + e) * 128;
+        uint8_t* row = WIDE ? books_s + (size_t)e * 256 + (R == 2 ? r : bufi) * 128
+                            : books_s + bufi * book_bytes + ((size_t)r * a.n_sh + e) * 128;
 #pragma unroll
         for (int q = 0; q < REP; ++q) {
           uint8_t* d = row + ((q + e) % REP) * EB;  // rotate so 8/16 threads hit distinct banks
@@ -168,118 +247,145 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
     }
   };
   auto csync = [&]() { named_bar_sync(1, kConsumers); };
+  // region (codebook) of a unit: tile sharing (codec.py:135-177) changes books per
+  // 256-row tile and per column tile; whole-tensor sharing has one book
+  auto region_of = [&](int u) {
+    if constexpr (!TILE) return 0;
+    const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
+    return (chunk * kChunkRows / a.tile_rows) * a.n_tc + (cb * COLS) / a.tile_cols;
+  };
 
-  if constexpr (!TILE) {
+  {
     uint4 bb[MAX_PER_THREAD];
-    book_issue(0, bb);
+    book_issue(region_of(u0), bb);
     book_commit(0, bb);
   }
-  pdl_wait();  // x / y / workspace may belong to the previous kernel
+  pdl_wait();  // x / y / the partial workspace may belong to the previous kernel
   csync();
+  if (tid == 0) trace_at(a.trace, 1);
 
-  int idx = 0;
+  float acc[B][V];
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
+
   int cur_buf = 0;
-  for (int u = u0; u < u1;) {
-    const int cblk = u / a.n_chunks;
-    const int c0 = u - cblk * a.n_chunks;
-    const int c1 = min(a.n_chunks, c0 + (u1 - u));
-    const int g_local = wg * 32 + lane;
-    const int col_tile = TILE ? (cblk * COLS) / a.tile_cols : 0;
-    auto region_of_chunk = [&](int chunk) {
-      return TILE ? (chunk * kChunkRows / a.tile_rows) * a.n_tc + col_tile : 0;
-    };
+  int span_first = u0;  // first unit of the current span
+  for (int u = u0, idx = 0; u < u1; ++u, ++idx) {
+    const int s = idx % kStages;
+    uint4 nb[MAX_PER_THREAD];
+    bool sw = false;
     if constexpr (TILE) {
-      uint4 bb[MAX_PER_THREAD];
-      book_issue(region_of_chunk(c0), bb);
-      csync();  // the previous span is done with both buffers
-      book_commit(0, bb);
-      cur_buf = 0;
-      csync();
+      sw = (u + 1 < u1) && region_of(u + 1) != region_of(u);
+      if (sw) book_issue(region_of(u + 1), nb);
     }
-
-    float acc[B][V];
+    mbar_wait(full0 + 8 * s, (idx / kStages) & 1);
+    if (tid == 0 && idx == 0) trace_at(a.trace, 2);
+    const uint8_t* st = stages + s * STG;
+    const uint8_t* xs = st + STAGEB + (wm * RW) * 2;  // this warp's rows of the chunk's activations
+    const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
+    const int region = region_of(u);
+    if (!a.debug_nocompute) {
+      // code words of this chunk (LOADS x R 16-byte words per lane)
+      uint4 cw[LOADS][R];
 #pragma unroll
-    for (int b = 0; b < B; ++b)
-#pragma unroll
-      for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
-
-    for (int chunk = c0; chunk < c1; ++chunk, ++idx) {
-      const int s = idx % kStages;
-      uint4 nb[MAX_PER_THREAD];
-      bool sw = false;
-      if constexpr (TILE) {
-        sw = (chunk + 1 < c1) && region_of_chunk(chunk + 1) != region_of_chunk(chunk);
-        if (sw) book_issue(region_of_chunk(chunk + 1), nb);
-      }
-      mbar_wait(full0 + 8 * s, (idx / kStages) & 1);
-      const uint8_t* st = stages + s * STAGEB;
-      const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
-      const int region = region_of_chunk(chunk);
-      const int m0 = chunk * kChunkRows + wm * RW;
-#pragma unroll
-      for (int i = 0; i < LOADS; ++i) {
-        uint4 cw[R];
+      for (int i = 0; i < LOADS; ++i)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          cw[r] = *reinterpret_cast<const uint4*>(st + r * LEVB + (wm * LOADS + i) * SEGB + g_local * 16);
-        uint4 xv[B][RPL / 8];
+          cw[i][r] = *reinterpret_cast<const uint4*>(st + r * LEVB + ((wm * LOADS + i) * GC + g_local) * 16);
+      // Software pipeline over batches of NBR rows: the codebook lookups of batch
+      // j+1 are issued before batch j's FMAs, so each warp keeps up to 2 x 32
+      // registers of shared-memory gathers in flight (the kernel runs one CTA of
+      // 16 consumer warps per SM; without this the LDS latency is exposed).
+      auto lookup = [&](int k, int r) -> const uint8_t* {
+        const int i = k / RPL, kr = k % RPL;
+        if constexpr (WIDE) {
+          // code byte -> bits 8..15, replica offset in bits 0..7: one PRMT
+          const uint32_t w = (&cw[i][r].x)[CBYTES == 2 ? kr / 2 : kr / 4];
+          const uint32_t byte = CBYTES == 2 ? (kr & 1) * 2 : (kr % 4);
+          const uint32_t off = __byte_perm(w, rep_off, 0x5504 | (byte << 4));
+          return books_s + off + (R == 2 ? r : cur_buf) * 128;
+        }
+        uint32_t code;
+        if constexpr (CBYTES == 2) {
+          const uint32_t w = (&cw[i][r].x)[kr / 2];
+          code = (kr & 1) ? (w >> 16) : (w & 0xffff);
+        } else {
+          const uint32_t w = (&cw[i][r].x)[kr / 4];
+          code = (w >> (8 * (kr % 4))) & 0xff;
+        }
+        bool in_smem = true;
+        if constexpr (GTIER) in_smem = code < (uint32_t)a.n_sh;
+        return in_smem ? bsm + (size_t)r * a.n_sh * 128 + ((size_t)code << 7)
+                       : reinterpret_cast<const uint8_t*>(a.books) +
+                             (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
+      };
+      auto load_entry = [&](const uint8_t* src, uint32_t (&e)[V / 2]) {
+        // plain C++ loads: the compiler folds the shared base into [R+UR+imm]
+        if constexpr (EB == 16) {
+          const uint4 q = *reinterpret_cast<const uint4*>(src);
+          e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
+        } else {
+          const uint2 q = *reinterpret_cast<const uint2*>(src);
+          e[0] = q.x; e[1] = q.y;
+        }
+      };
+      constexpr int NBR = (R * EB / 4 * RPL <= 32) ? RPL : 32 / (R * EB / 4);  // rows per batch
+      constexpr int NROWS = LOADS * RPL;
+      constexpr int NBATCH = NROWS / NBR;
+      static_assert(NROWS % NBR == 0 && NBR % 8 == 0 || NBR == 4, "batch shape");
+      uint32_t ent[2][NBR * R][V / 2];
+      auto load_batch = [&](int bi, uint32_t (&dst)[NBR * R][V / 2]) {
+#pragma unroll
+        for (int kk = 0; kk < NBR; ++kk)
+#pragma unroll
+          for (int r = 0; r < R; ++r) load_entry(lookup(bi * NBR + kk, r), dst[kk * R + r]);
+      };
+      uint32_t hw[B][V / 2];  // fp16x2 window accumulators (H2 path), 8 rows per window
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int j = 0; j < V / 2; ++j) hw[b][j] = 0u;
+      load_batch(0, ent[0]);
+#pragma unroll
+      for (int bi = 0; bi < NBATCH; ++bi) {
+        if (bi + 1 < NBATCH) load_batch(bi + 1, ent[(bi + 1) & 1]);
+        uint4 xv[B][(NBR + 7) / 8];  // the batch's activations (shared-memory broadcast)
+        const int xbase = (bi * NBR) & ~7;  // 16-byte aligned row of the batch's first word
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
-          for (int q = 0; q < RPL / 8; ++q)
-            xv[b][q] = __ldg(reinterpret_cast<const uint4*>(a.x + (int64_t)b * a.M + m0 + i * RPL) + q);
-        uint32_t hw[B][V / 2];  // fp16x2 window accumulators (H2 path)
+          for (int q = 0; q < (NBR + 7) / 8; ++q)
+            xv[b][q] = *reinterpret_cast<const uint4*>(xs + b * XROWB + (xbase + q * 8) * 2);
 #pragma unroll
-        for (int b = 0; b < B; ++b)
-#pragma unroll
-          for (int j = 0; j < V / 2; ++j) hw[b][j] = 0u;
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-          uint16_t xh[B];
+        for (int kk = 0; kk < NBR; ++kk) {
+          const int k = bi * NBR + kk;  // row within this warp's slab of the chunk
+          uint32_t xw[B];  // the packed activation pair holding row k (selected by k & 1)
 #pragma unroll
           for (int b = 0; b < B; ++b) {
-            const uint32_t w = (&xv[b][k / 8].x)[(k % 8) / 2];
-            xh[b] = (uint16_t)((k & 1) ? (w >> 16) : (w & 0xffff));
+            const int kx = k - xbase;
+            xw[b] = (&xv[b][kx / 8].x)[(kx % 8) / 2];
           }
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            uint32_t code;
-            if constexpr (CBYTES == 2) {
-              const uint32_t w = (&cw[r].x)[k / 2];
-              code = (k & 1) ? (w >> 16) : (w & 0xffff);
-            } else {
-              const uint32_t w = (&cw[r].x)[k / 4];
-              code = (w >> (8 * (k % 4))) & 0xff;
-            }
-            bool in_smem = true;
-            if constexpr (GTIER) in_smem = code < (uint32_t)a.n_sh;
-            uint32_t e[V / 2];
-            const uint8_t* src = in_smem ? bsm + (size_t)r * a.n_sh * 128 + ((size_t)code << 7)
-                                         : reinterpret_cast<const uint8_t*>(a.books) +
-                                               (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
-            if constexpr (EB == 16) {
-              const uint4 q = in_smem ? *reinterpret_cast<const uint4*>(src) : __ldg(reinterpret_cast<const uint4*>(src));
-              e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
-            } else {
-              const uint2 q = in_smem ? *reinterpret_cast<const uint2*>(src) : __ldg(reinterpret_cast<const uint2*>(src));
-              e[0] = q.x; e[1] = q.y;
-            }
+            const uint32_t (&e)[V / 2] = ent[bi & 1][kk * R + r];
             if constexpr (H2) {
               // packed fp16x2 FMA into an 8-row fp16 window (full-rate HFMA2; the
               // mixed-precision FHFMA issues at a quarter of that rate on sm_100)
 #pragma unroll
-              for (int b = 0; b < B; ++b) {
-                const uint32_t x2 = (uint32_t)xh[b] * 0x10001u;
+              for (int b = 0; b < B; ++b)
 #pragma unroll
-                for (int j = 0; j < V / 2; ++j) hw[b][j] = hfma2(e[j], x2, hw[b][j]);
-              }
+                for (int j = 0; j < V / 2; ++j)
+                  hw[b][j] = (k & 1) ? hfma2_bcast<1>(e[j], xw[b], hw[b][j]) : hfma2_bcast<0>(e[j], xw[b], hw[b][j]);
             } else {
 #pragma unroll
               for (int b = 0; b < B; ++b)
 #pragma unroll
                 for (int j = 0; j < V / 2; ++j) {
-                  acc[b][2 * j] = fma_h((uint16_t)(e[j] & 0xffff), xh[b], acc[b][2 * j]);
-                  acc[b][2 * j + 1] = fma_h((uint16_t)(e[j] >> 16), xh[b], acc[b][2 * j + 1]);
+                  const uint16_t xh = (uint16_t)((k & 1) ? (xw[b] >> 16) : (xw[b] & 0xffff));
+                  acc[b][2 * j] = fma_h((uint16_t)(e[j] & 0xffff), xh, acc[b][2 * j]);
+                  acc[b][2 * j + 1] = fma_h((uint16_t)(e[j] >> 16), xh, acc[b][2 * j + 1]);
                 }
             }
           }
@@ -297,59 +403,94 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * s);
-      if constexpr (TILE) {
-        if (sw) {
-          book_commit(cur_buf ^ 1, nb);
-          csync();
-          cur_buf ^= 1;
-        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    if constexpr (TILE) {
+      if (sw) {
+        book_commit(cur_buf ^ 1, nb);  // the other buffer was released at the previous swap
+        csync();
+        cur_buf ^= 1;
       }
     }
 
-    // ---- reduce the WM row-slabs of this span in a fixed order, one batch row at a time
-    const int n0 = cblk * COLS;
-    const bool whole = (c0 == 0 && c1 == a.n_chunks);
-    const int slot = cblk * a.n_chunks + c0;
+    // ---- end of a span: reduce the WM row-slabs in a fixed order, then write y,
+    // publish a partial, or finish a split column block
+    if (u + 1 == u1 || (u + 1) % a.n_chunks == 0) {
+      if (tid == 0 && u + 1 == u1) trace_at(a.trace, 3);
+      const int cb = u / a.n_chunks;
+      const int cf = span_first - cb * a.n_chunks;  // first chunk of the span
+      const int cl = u - cb * a.n_chunks;           // last chunk
+      const bool whole = (cf == 0 && cl == a.n_chunks - 1);
+      const bool finisher = (cf == 0 && !whole);
+      float keep[B];
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
+      for (int b = 0; b < B; ++b) {
+        // partials stored [w][q][g][4]: each lane's float4 stores are conflict-free
 #pragma unroll
-      for (int j = 0; j < V; ++j) red[(size_t)wm * COLS + g_local * V + j] = acc[b][j];
-      csync();
-      for (int col = tid; col < COLS; col += kConsumers) {
-        float sum = 0.f;
-#pragma unroll
-        for (int w = 0; w < WM; ++w) sum += red[(size_t)w * COLS + col];
-        if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, sum);
-        else a.part[((int64_t)slot * B + b) * COLS + col] = sum;
-      }
-      csync();
-    }
-    if (!whole) {
-      if (tid == 0) a.span_len[slot] = c1 - c0;
-      __threadfence();
-      csync();
-      if (tid == 0) *s_last = (atomicAdd(a.counters + cblk, c1 - c0) + (c1 - c0) == a.n_chunks);
-      csync();
-      if (*s_last) {
-        __threadfence();
-        for (int o = tid; o < B * COLS; o += kConsumers) {
-          const int b = o / COLS, col = o - (o / COLS) * COLS;
+        for (int q = 0; q < NQ; ++q)
+          *reinterpret_cast<float4*>(red + (size_t)wm * COLS + (q * GC + g_local) * 4) =
+              make_float4(acc[b][4 * q], acc[b][4 * q + 1], acc[b][4 * q + 2], acc[b][4 * q + 3]);
+        csync();
+        keep[b] = 0.f;
+        if (tid < COLS) {
+          const int o = tid;
           float sum = 0.f;
-          for (int c = 0; c < a.n_chunks;) {
-            const int sl = cblk * a.n_chunks + c;
-            sum += __ldcg(a.part + (int64_t)sl * B * COLS + o);
-            c += __ldcg(a.span_len + sl);
-          }
-          store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + n0 + col, sum);
+#pragma unroll
+          for (int w = 0; w < WM; ++w) sum += red[(size_t)w * COLS + o];
+          const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
+          const int col = g * V + q * 4 + c;
+          if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * COLS + col, sum);
+          else if (finisher) keep[b] = sum;
+          else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + b) * COLS + col, tag_partial(sum));
         }
-        if (tid == 0) a.counters[cblk] = 0;  // self-reset for the next launch
+        csync();
       }
+      if (finisher) {
+        // the later spans of this column block are the first spans of the CTAs
+        // k in (blockIdx.x, k_end); their tagged partials are polled in parallel,
+        // summed in chunk order, and the slots zeroed for the next launch
+        int k_end = blockIdx.x + 1;
+        while (k_end < (int)gridDim.x && (int)((int64_t)k_end * U / gridDim.x) < (cb + 1) * a.n_chunks) ++k_end;
+        const int n_later = k_end - blockIdx.x - 1;
+        if (tid < COLS) {
+          const int o = tid;
+          const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
+          const int col = g * V + q * 4 + c;
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            float sum = keep[b];
+            constexpr int PF = 8;  // partial loads in flight
+            for (int j0 = 0; j0 < n_later; j0 += PF) {
+              unsigned long long pv[PF];
+              unsigned long long* pp[PF];
+#pragma unroll
+              for (int j = 0; j < PF; ++j) {
+                pp[j] = a.part + ((int64_t)(blockIdx.x + 1 + j0 + j) * B + b) * COLS + col;
+                pv[j] = (j0 + j < n_later) ? ld_relaxed_u64(pp[j]) : (1ull << 32);
+              }
+#pragma unroll
+              for (int j = 0; j < PF; ++j) {
+                while ((pv[j] >> 32) == 0) pv[j] = ld_relaxed_u64(pp[j]);
+                if (j0 + j < n_later) {
+                  sum += __uint_as_float((uint32_t)pv[j]);
+                  st_relaxed_u64(pp[j], 0ull);
+                }
+              }
+            }
+            store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * COLS + col, sum);
+          }
+        }
+        if (tid == 0) trace_at(a.trace, 5);
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
+      span_first = u + 1;
     }
-    csync();  // red / s_last reuse by the next span
-    u += c1 - c0;
   }
+  if (tid == 0) trace_at(a.trace, 6);
 }
 
 // generic path
@@ -446,25 +587,31 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   n_sh = std::min(n_sh, g.K);
   n_sh = std::min(n_sh, 1024 / g.R);
   if (L && (L->flags & VQB_FLAG_NO_SHARED)) n_sh = 0;
+  // every code of the stream is resident when the shared span covers the codebook
+  // or the largest code; the WIDE (256-row) layout then drops the global tier
+  const int span = g.K <= n_sh ? g.K : ((t->max_code >= 0 && t->max_code < n_sh) ? t->max_code + 1 : -1);
+  p.gtier = !(span > 0 && span <= 256);
+  if (!p.gtier) n_sh = std::min(n_sh, 256);
   p.n_sh = n_sh;
-  p.gtier = !(t->max_code >= 0 && t->max_code < n_sh);
   p.h2 = !(L && (L->flags & VQB_FLAG_EXACT_ACCUM));
   p.n_cblk = (int)(g.cols / cols_per_cta);
   p.n_chunks = (int)(g.rows / kChunkRows);
+  const int nst = gemv_stages(p.tile);
   const int WM = kConsumerWarps / p.WG;
-  p.smem = (size_t)kStages * stage_bytes(p.R, p.cbytes, p.WG) + (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128 +
-           (size_t)WM * cols_per_cta * sizeof(float) + 2 * kStages * 8 + 16;
+  const bool wide = !p.gtier && p.R * (p.tile ? 2 : 1) <= 2;  // mirrors the kernel's WIDE layout
+  p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows) +
+           (wide ? (size_t)65536 : (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128) + (size_t)WM * cols_per_cta * 4 +
+           2 * nst * 8 + 16;
   p.ok = true;
   return p;
 }
 
-static int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
+// workspace: the tagged partials (one B x COLS slot of 8-byte words per CTA) live
+// in the self-resetting head
 static int64_t fast_ws_bytes(const FastPlan& p, const Geom& g, int rows) {
   if (!p.ok) return 0;
-  const int64_t slots = (int64_t)p.n_cblk * p.n_chunks;
-  const int64_t cols = 32 * p.WG * p.V;
-  return VQB_WS_COUNTER_BYTES + align256(slots * 4) + slots * rows * cols * 4;
+  return VQB_WS_COUNTER_BYTES + 1024 * 64;  // tagged partials live in the head; + debug trace
 }
 
 static int generic_chunk_rows(const Geom& g) { return g.rows > 4096 ? 512 : 256; }
@@ -498,7 +645,9 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
     }
   }
   if (occ < 1) return set_error(VQB_ECAPACITY, "GEMV plan (n_shared=%d) does not fit one CTA per SM", p.n_sh);
-  int grid = std::min(p.n_cblk * p.n_chunks, occ * sm_count());
+  // one persistent CTA per SM: every CTA is resident (a finishing CTA polls the
+  // partials of later CTAs) and the SM's second slot is left to the next kernel
+  int grid = std::min(p.n_cblk * p.n_chunks, sm_count());
   if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -553,14 +702,14 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     return set_error(VQB_ECONFIG, "unknown activation/output dtype");
   FastPlan p = plan_fast(g, w, rows, x_dtype, L);
   GemvKernel kernel = p.ok ? fast_kernel_for(p, rows) : nullptr;
+  // the activations are TMA-staged: 16-byte aligned rows
+  if (kernel && ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (g.rows % 8) != 0)) kernel = nullptr;
   if (used_fast) *used_fast = kernel != nullptr;
   if (kernel) {
     const int64_t need = fast_ws_bytes(p, g, rows);
     if ((int64_t)ws_bytes < need || !ws)
       return set_error(VQB_ECAPACITY, "GEMV workspace too small: %zu < %lld", ws_bytes, (long long)need);
-    const int64_t slots = (int64_t)p.n_cblk * p.n_chunks;
-    if ((int64_t)p.n_cblk * 4 > VQB_WS_COUNTER_BYTES)
-      return set_error(VQB_ECAPACITY, "too many GEMV column blocks (%d) for the counter region", p.n_cblk);
+    const int64_t units = (int64_t)p.n_cblk * p.n_chunks;
     uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
     GemvFastArgs a;
     a.codes = reinterpret_cast<const uint8_t*>(w->d_codes);
@@ -569,9 +718,6 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.x = reinterpret_cast<const __half*>(x);
     a.y = y;
     a.y_dtype = y_dtype;
-    a.counters = reinterpret_cast<int*>(wsb);
-    a.span_len = reinterpret_cast<int*>(wsb + VQB_WS_COUNTER_BYTES);
-    a.part = reinterpret_cast<float*>(wsb + VQB_WS_COUNTER_BYTES + align256(slots * 4));
     a.M = (int)g.rows;
     a.N = (int)g.cols;
     a.G = (int)g.gpr;
@@ -583,6 +729,13 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.n_chunks = p.n_chunks;
     a.n_cblk = p.n_cblk;
     a.n_sh = p.n_sh;
+    const int grid = std::min<int64_t>(units, sm_count());
+    // head layout: [0, 64 KB) split-arrival counters (attention), then the GEMV slots
+    if ((int64_t)grid * rows * (32 * p.WG * p.V) * 8 > VQB_WS_COUNTER_BYTES - 65536)
+      return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
+    a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
+    a.debug_nocompute = (L && (L->flags & 64)) ? 1 : 0;
+    a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
     return launch_gemv_kernel(kernel, p, a, st, L);
   }
   // generic: per-chunk partials then an ordered reduction
@@ -630,7 +783,7 @@ int gemv_usage(VqbUsage* u) {
   cudaFuncAttributes at;
   auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, true, true>;
   VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
-  const size_t smem = kStages * stage_bytes(1, 2, 1) + 256 * 128 + kConsumerWarps * 256 * 4 + 2 * kStages * 8 + 16;
+  const size_t smem = gemv_stages(false) * stage_total(1, 2, 1, 1) + 256 * 128 + 2 * gemv_stages(false) * 8 + 16;
   u->shared_bytes = (int)(at.sharedSizeBytes + smem);
   u->regs_per_thread = at.numRegs;
   u->threads_per_block = kGemvThreads;

@@ -56,6 +56,8 @@ def main():
     ap.add_argument("--copies", type=int, default=0, help="distinct weights cycled (0: enough for > 256 MB)")
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--n_shared", type=int, default=0)
+    ap.add_argument("--split", type=int, default=0, help="M split (cluster size) override")
+    ap.add_argument("--grid", type=int, default=0, help="grid limit (persistent CTAs)")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -81,21 +83,48 @@ def main():
             ws.append(DeviceVQTensor.from_device_codes(codes, (m, n), cfg, books).relayout("gemv"))
         x = torch.randn((args.rows, m), generator=g, device=dev).half()
         ys = [torch.empty((args.rows, n), device=dev, dtype=torch.float16) for _ in ws]
-        L = launch_struct(n_shared=args.n_shared or None)
+        L = launch_struct(n_shared=args.n_shared or None, grid_limit=args.grid)
         L.flags = args.flags
+        if args.split:
+            L.split_axis, L.split_factor = ord("M"), args.split
         lib = N.lib()
         structs = [w.struct() for w in ws]
         from paper_2503_02236_b200.ops import workspace
         need = max(N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMV, st, args.rows, L)) for st in structs)
 
+        bufs = []
+
         def run():
             buf = workspace(need, dev)
+            bufs.append(buf)
             stream = torch.cuda.current_stream(dev).cuda_stream
             for st, y in zip(structs, ys):
                 N.check(lib.vqb_gemv(st, x.data_ptr(), N.F16, args.rows, y.data_ptr(), N.F16, L,
                                      buf.data_ptr(), buf.numel(), stream))
 
         us = graph_time(run, 20) / len(ws)
+        if args.flags & 32:
+            torch.cuda.synchronize()
+            buf = bufs[-1]
+            off = 4194304
+            buf[off:off + 64 * 148].zero_() if False else None
+            tr = buf[off:off + 64 * 148].view(torch.int64).view(-1, 8).cpu()
+            valid = tr[:, 0] > 0
+            tr = tr[valid]
+            t0 = int(tr[:, 0].min())
+            rel = (tr[:, :7] - t0).double() / 1e3
+            sms = tr[:, 7]
+            import collections
+            occ = collections.Counter(collections.Counter(sms.tolist()).values())
+            q = lambda c: [round(float(rel[:, c].quantile(p)), 2) for p in (0.0, 0.5, 1.0)]
+            print(json.dumps({"shape": [m, n], "ctas": int(valid.sum()), "ctas_per_sm_hist": dict(occ),
+                              "start": q(0), "book_ready": q(1), "first_data": q(2), "compute_done": q(3),
+                              "end": q(6)}), flush=True)
+            pub = tr[:, 4] > 0
+            fin = tr[:, 5] > 0
+            print(json.dumps({"publishers": int(pub.sum()), "publish_minus_done": [round(float(x), 2) for x in ((tr[pub, 4] - tr[pub, 3]).double() / 1e3).quantile(torch.tensor([0.0, 0.5, 1.0], dtype=torch.float64))] if pub.any() else None,
+                              "finishers": int(fin.sum()), "flags_seen_minus_done": [round(float(x), 2) for x in ((tr[fin, 5] - tr[fin, 3]).double() / 1e3).quantile(torch.tensor([0.0, 0.5, 1.0], dtype=torch.float64))] if fin.any() else None,
+                              "end_minus_flags": [round(float(x), 2) for x in ((tr[fin, 6] - tr[fin, 5]).double() / 1e3).quantile(torch.tensor([0.0, 0.5, 1.0], dtype=torch.float64))] if fin.any() else None}), flush=True)
         kern = N.last_kernel()
         alg = ws[0].algorithmic_bytes(work) + args.rows * (m + n) * 2
         dense = [torch.randn((m, n), device=dev, dtype=torch.float16) for _ in range(max(2, min(16, (512 << 20) // (m * n * 2) + 1)))]
@@ -106,7 +135,7 @@ def main():
                 torch.matmul(x, d, out=o)
 
         dus = graph_time(run_dense, 20) / len(dense)
-        print(json.dumps({"cfg": args.cfg, "shape": [m, n], "rows": args.rows, "kernel": kern, "copies": len(ws),
+        print(json.dumps({"cfg": args.cfg, "shape": [m, n], "rows": args.rows, "kernel": kern, "split": args.split, "flags": args.flags, "copies": len(ws),
                           "us_per_call": round(us, 2), "alg_MB": round(alg / 1e6, 2),
                           "GB_s": round(alg / us / 1e3, 1), "frac_hbm": round(alg / us / 1e3 / peak, 3),
                           "fp16_cublas_us": round(dus, 2),
