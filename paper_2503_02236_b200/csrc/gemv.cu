@@ -43,20 +43,24 @@
 
 namespace vqb {
 
-constexpr int kConsumerWarps = 16;
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kGemvThreads = kConsumers + 32;  // + one producer warp
-constexpr int kChunkRows = 256;
+// Every warp computes; thread 0 also feeds the TMA ring. 32 warps (one 1024-thread
+// CTA per SM) hide the shared-memory gather latency at batch 1-2; at larger batch each
+// looked-up entry feeds B FMAs, so fewer warps with more registers do (16 at B=4,
+// 8 at B=8, which keeps the B x V fp32 accumulators in registers).
+__host__ __device__ constexpr int gemv_warps(int B) { return B >= 8 ? 8 : 16; }
+constexpr int kSlabRows = 16;   // rows a warp handles per chunk (one 16-byte code word of u8, two of u16)
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
-// ring depth: 3 stages (2 for tile-shared books, whose double-buffered codebook
-// takes the room) keeps a CTA under half of the SM's shared memory, so the next
-// kernel's CTA (programmatic dependent launch) can be resident beside it
-__host__ __device__ constexpr int gemv_stages(bool tile) { return tile ? 3 : 6; }
-// bytes of one chunk's codes: R levels x 256 rows x 32*WG columns
-__host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG) { return R * cbytes * WG * kChunkRows * 32; }
-// a ring stage also carries the chunk's activations: B rows x 256 fp16
+// chunk rows: the warps along M each take one 16-row slab (WG = warps across N)
+__host__ __device__ constexpr int gemv_chunk_rows(int WG, int B) { return kSlabRows * (gemv_warps(B) / WG); }
+// ring depth (tile-shared books double-buffer their codebook in the same 64 KB region)
+__host__ __device__ constexpr int gemv_stages(bool tile) { return tile ? 4 : 3; }
+// bytes of one chunk's codes: R levels x chunk rows x 32*WG columns
+__host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG, int B) {
+  return R * cbytes * WG * gemv_chunk_rows(WG, B) * 32;
+}
+// a ring stage also carries the chunk's activations: B rows x chunk rows fp16
 __host__ __device__ constexpr int stage_total(int R, int cbytes, int WG, int B) {
-  return stage_bytes(R, cbytes, WG) + B * kChunkRows * 2;
+  return stage_bytes(R, cbytes, WG, B) + B * gemv_chunk_rows(WG, B) * 2;
 }
 
 struct GemvFastArgs {
@@ -72,7 +76,6 @@ struct GemvFastArgs {
   unsigned long long* part;  // (grid, B, COLS) tagged partials {fp32 value, tag 1}, one slot per CTA,
                              // in the self-resetting workspace head (zeroed by the consumer)
   unsigned long long* trace;  // optional per-CTA phase timestamps (debug flag 32), 8 per CTA
-  int debug_nocompute;    // experiment: consumers only wait for and release the stages
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -98,7 +101,7 @@ __device__ __forceinline__ unsigned long long tag_partial(float v) {
   return (1ull << 32) | (unsigned long long)__float_as_uint(v);
 }
 
-// Persistent stream-K decode GEMV. Work units are (column block, 256-row chunk),
+// Persistent stream-K decode GEMV. Work units are (column block, chunk of CR rows),
 // ordered column-block major; CTA i owns the contiguous unit range
 // [i*U/grid, (i+1)*U/grid) and walks it as "spans" (maximal runs inside one column
 // block), accumulating a span in registers. A span that covers its whole column
@@ -108,30 +111,31 @@ __device__ __forceinline__ unsigned long long tag_partial(float v) {
 // already published) in chunk order: deterministic, like the reference's ordered
 // split reduction (sim.py:735), with no atomics and no extra launch.
 template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, bool H2>
-__global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a) {
+__global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
+  constexpr int kGemvWarps = gemv_warps(B);
+  constexpr int kGemvThreads = kGemvWarps * 32;
   constexpr int EB = V * 2;              // fp16 entry bytes
   constexpr int REP = 128 / EB;          // replicas per bank row
   constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code word
-  constexpr int WM = kConsumerWarps / WG;  // warps along M
-  constexpr int RW = kChunkRows / WM;    // rows per warp per chunk
-  constexpr int LOADS = RW / RPL;        // code words per lane per level per chunk
-  constexpr int COLS = 32 * WG * V;      // output columns per column block
+  constexpr int WM = kGemvWarps / WG;    // warps along M
+  constexpr int CR = gemv_chunk_rows(WG, B);
+  constexpr int LOADS = kSlabRows / RPL; // code words per lane per level per chunk
+  constexpr int COLS = 32 * WG * V;      // output columns per column block (256)
   constexpr int GC = 32 * WG;            // sub-vector columns per column block
   constexpr int NQ = V / 4;              // float4 per lane in the cross-warp reduction
-  constexpr int NSEG = kChunkRows / RPL; // row groups per chunk
-  constexpr int LEVB = NSEG * GC * 16;   // bytes per level per chunk (contiguous in GEMV_IL)
+  constexpr int RGB = GC * 16;           // bytes of one row group of a column block, per level
+  constexpr int LEVB = (CR / RPL) * RGB; // bytes per level per full chunk (contiguous in GEMV_IL)
   constexpr int NBUF = TILE ? 2 : 1;     // codebook buffers
   // WIDE book layout (every code < 256 is in shared memory): entry e owns a 256-byte
   // row, half h = level (R == 2) or buffer (tile double buffering) holds its
   // replicas, so a lookup address is ONE PRMT of the code byte and the lane's
-  // replica offset (the book base and the half fold into the LDS immediate/UR).
+  // replica offset (the book base and the half fold into the LDS addressing).
   constexpr bool WIDE = !GTIER && R * NBUF <= 2;
-  static_assert(LOADS >= 1 && RW % 8 == 0, "bad tiling");
+  static_assert(LOADS >= 1, "bad tiling");
   constexpr int STAGEB = R * LEVB;
-  static_assert(STAGEB == stage_bytes(R, CBYTES, WG), "stage size");
-  constexpr int XROWB = kChunkRows * 2;  // one batch row's activations per chunk
+  static_assert(STAGEB == stage_bytes(R, CBYTES, WG, B), "stage size");
+  constexpr int XROWB = CR * 2;          // one batch row's activations per chunk
   constexpr int STG = stage_total(R, CBYTES, WG, B);
-  static_assert(B <= 32, "one activation row per producer lane");
   constexpr int kStages = gemv_stages(TILE);
 
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -147,6 +151,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   const int U = a.n_cblk * a.n_chunks;
   const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+  const int n = u1 - u0;
+  const int last_rows = a.M - (a.n_chunks - 1) * CR;  // rows of the (possibly partial) last chunk
 
   if (tid == 0) {
     trace_at(a.trace, 0);
@@ -157,66 +163,58 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
     }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, kConsumerWarps);
+      mbar_init(empty0 + 8 * s, kGemvWarps);
     }
     mbar_fence_init();
   }
   __syncthreads();
   pdl_launch_dependents();
 
-  if (warp == kConsumerWarps) {
-    // ===== producer: stream each unit's codes (one bulk copy per level: a column
-    // block's chunk is contiguous in the column-blocked GEMV_IL layout) and its
-    // activations into the ring. Codes do not depend on the previous kernel, so the
-    // first kStages units are requested before griddepcontrol.wait; activations
-    // (possibly written by the previous kernel) only after it.
-    const int n = u1 - u0;
-    auto issue_codes = [&](int idx) {
-      const int s = idx % kStages, u = u0 + idx;
-      const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
-      if (lane == 0) {
-        const int64_t off = ((int64_t)cb * GC * (a.M / RPL) + (int64_t)chunk * NSEG * GC) * 16;
+  // ---- TMA feed (thread 0): a column block's chunk is contiguous in the
+  // column-blocked GEMV_IL layout, so each unit is one bulk copy per level plus one
+  // per activation row. Codes do not depend on the previous kernel and are
+  // requested before griddepcontrol.wait; activations only after it.
+  auto unit_rows = [&](int u) { return (u % a.n_chunks == a.n_chunks - 1) ? last_rows : CR; };
+  auto expect = [&](int idx) {
+    const int rows = unit_rows(u0 + idx);
+    mbar_arrive_expect_tx(full0 + 8 * (idx % kStages), (uint32_t)(R * (rows / RPL) * RGB + B * rows * 2));
+  };
+  auto issue_codes = [&](int idx) {
+    const int s = idx % kStages, u = u0 + idx;
+    const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
+    const int rows = unit_rows(u);
+    const int64_t off = (int64_t)cb * GC * (a.M / RPL) * 16 + (int64_t)chunk * (CR / RPL) * RGB;
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          tma_load_1d(smem_u32(stages + s * STG + r * LEVB), a.codes + r * a.level_bytes + off, LEVB, full0 + 8 * s);
-      }
-    };
-    auto issue_x = [&](int idx) {
-      const int s = idx % kStages, u = u0 + idx;
-      const int chunk = u % a.n_chunks;
-      if (lane < B)
-        tma_load_1d(smem_u32(stages + s * STG + STAGEB + lane * XROWB),
-                    a.x + (int64_t)lane * a.M + (int64_t)chunk * kChunkRows, XROWB, full0 + 8 * s);
-    };
-    const int pre = min(n, kStages);
+    for (int r = 0; r < R; ++r)
+      tma_load_1d(smem_u32(stages + s * STG + r * LEVB), a.codes + r * a.level_bytes + off,
+                  (uint32_t)((rows / RPL) * RGB), full0 + 8 * s);
+  };
+  auto issue_x = [&](int idx) {
+    const int s = idx % kStages, u = u0 + idx;
+    const int chunk = u % a.n_chunks;
+    const int rows = unit_rows(u);
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      tma_load_1d(smem_u32(stages + s * STG + STAGEB + b * XROWB), a.x + (int64_t)b * a.M + (int64_t)chunk * CR,
+                  (uint32_t)(rows * 2), full0 + 8 * s);
+  };
+  const int pre = min(n, kStages);
+  if (tid == 0)
     for (int idx = 0; idx < pre; ++idx) {
-      if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * idx, STG);
-      __syncwarp();
+      expect(idx);
       issue_codes(idx);
     }
-    pdl_wait();
-    for (int idx = 0; idx < pre; ++idx) issue_x(idx);
-    for (int idx = kStages; idx < n; ++idx) {
-      const int s = idx % kStages;
-      mbar_wait(empty0 + 8 * s, ((idx / kStages) + 1) & 1);
-      if (lane == 0) mbar_arrive_expect_tx(full0 + 8 * s, STG);
-      __syncwarp();
-      issue_codes(idx);
-      issue_x(idx);
-    }
-    return;
-  }
 
-  // ===== consumers =====
+  // ===== codebook cache fill =====
   const int wm = warp / WG, wg = warp % WG;
   const uint32_t rep_off = (uint32_t)(lane % REP) * EB;
   const int g_local = wg * 32 + lane;
 
-  constexpr int MAX_PER_THREAD = (1024 + kConsumers - 1) / kConsumers;  // n_sh * R <= 1024 entries
+  constexpr int MAX_PER_THREAD = (1024 + kGemvThreads - 1) / kGemvThreads;  // n_sh * R <= 1024 entries
   auto book_issue = [&](int region, uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
     for (int k = 0; k < MAX_PER_THREAD; ++k) {
-      const int idx = tid + k * kConsumers;
+      const int idx = tid + k * kGemvThreads;
       if (idx < R * a.n_sh) {
         const int r = idx / a.n_sh, e = idx - r * a.n_sh;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(a.books) +
@@ -232,7 +230,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
   auto book_commit = [&](int bufi, const uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
     for (int k = 0; k < MAX_PER_THREAD; ++k) {
-      const int idx = tid + k * kConsumers;
+      const int idx = tid + k * kGemvThreads;
       if (idx < R * a.n_sh) {
         const int r = idx / a.n_sh, e = idx - r * a.n_sh;
         uint8_t* row = WIDE ? books_s + (size_t)e * 256 + (R == 2 ? r : bufi) * 128
@@ -246,13 +244,12 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
       }
     }
   };
-  auto csync = [&]() { named_bar_sync(1, kConsumers); };
   // region (codebook) of a unit: tile sharing (codec.py:135-177) changes books per
-  // 256-row tile and per column tile; whole-tensor sharing has one book
+  // row tile and per column tile; whole-tensor sharing has one book
   auto region_of = [&](int u) {
     if constexpr (!TILE) return 0;
     const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
-    return (chunk * kChunkRows / a.tile_rows) * a.n_tc + (cb * COLS) / a.tile_cols;
+    return (chunk * CR / a.tile_rows) * a.n_tc + (cb * COLS) / a.tile_cols;
   };
 
   {
@@ -261,7 +258,9 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
     book_commit(0, bb);
   }
   pdl_wait();  // x / y / the partial workspace may belong to the previous kernel
-  csync();
+  if (tid == 0)
+    for (int idx = 0; idx < pre; ++idx) issue_x(idx);
+  __syncthreads();
   if (tid == 0) trace_at(a.trace, 1);
 
   float acc[B][V];
@@ -272,8 +271,22 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
 
   int cur_buf = 0;
   int span_first = u0;  // first unit of the current span
+  int cb = u0 / a.n_chunks;
+  int span_end = min(u1, (cb + 1) * a.n_chunks);
   for (int u = u0, idx = 0; u < u1; ++u, ++idx) {
     const int s = idx % kStages;
+    // refill the stage unit idx-1 used with unit idx-1+kStages (thread 0 only: it
+    // waits until every warp has released that stage)
+    if (idx >= 1 && idx - 1 + kStages < n) {
+      if (tid == 0) {
+        const int j = idx - 1 + kStages;
+        mbar_wait(empty0 + 8 * (j % kStages), ((idx - 1) / kStages) & 1);
+        expect(j);
+        issue_codes(j);
+        issue_x(j);
+      }
+      __syncwarp();
+    }
     uint4 nb[MAX_PER_THREAD];
     bool sw = false;
     if constexpr (TILE) {
@@ -283,21 +296,18 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
     mbar_wait(full0 + 8 * s, (idx / kStages) & 1);
     if (tid == 0 && idx == 0) trace_at(a.trace, 2);
     const uint8_t* st = stages + s * STG;
-    const uint8_t* xs = st + STAGEB + (wm * RW) * 2;  // this warp's rows of the chunk's activations
+    const uint8_t* xs = st + STAGEB + (wm * kSlabRows) * 2;  // this warp's rows of the chunk's activations
     const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
     const int region = region_of(u);
-    if (!a.debug_nocompute) {
-      // code words of this chunk (LOADS x R 16-byte words per lane)
+    const bool active = wm * kSlabRows < unit_rows(u);  // the last chunk may be partial
+    if (active) {
+      // code words of this warp's slab (LOADS x R 16-byte words per lane)
       uint4 cw[LOADS][R];
 #pragma unroll
       for (int i = 0; i < LOADS; ++i)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          cw[i][r] = *reinterpret_cast<const uint4*>(st + r * LEVB + ((wm * LOADS + i) * GC + g_local) * 16);
-      // Software pipeline over batches of NBR rows: the codebook lookups of batch
-      // j+1 are issued before batch j's FMAs, so each warp keeps up to 2 x 32
-      // registers of shared-memory gathers in flight (the kernel runs one CTA of
-      // 16 consumer warps per SM; without this the LDS latency is exposed).
+          cw[i][r] = *reinterpret_cast<const uint4*>(st + r * LEVB + (wm * LOADS + i) * RGB + g_local * 16);
       auto lookup = [&](int k, int r) -> const uint8_t* {
         const int i = k / RPL, kr = k % RPL;
         if constexpr (WIDE) {
@@ -321,87 +331,113 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
                        : reinterpret_cast<const uint8_t*>(a.books) +
                              (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
       };
-      auto load_entry = [&](const uint8_t* src, uint32_t (&e)[V / 2]) {
-        // plain C++ loads: the compiler folds the shared base into [R+UR+imm]
-        if constexpr (EB == 16) {
-          const uint4 q = *reinterpret_cast<const uint4*>(src);
-          e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
-        } else {
-          const uint2 q = *reinterpret_cast<const uint2*>(src);
-          e[0] = q.x; e[1] = q.y;
+      if constexpr (B >= 4 && H2) {
+        // large batch: an 8-row window's entries stay in registers while each batch
+        // row runs its own fp16x2 window, so only one window accumulator is live
+#pragma unroll
+        for (int w8 = 0; w8 < kSlabRows / 8; ++w8) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            uint32_t ent[8][V / 2];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint8_t* src = lookup(w8 * 8 + kk, r);
+              if constexpr (EB == 16) {
+                const uint4 q = *reinterpret_cast<const uint4*>(src);
+                ent[kk][0] = q.x; ent[kk][1] = q.y; ent[kk][2] = q.z; ent[kk][3] = q.w;
+              } else {
+                const uint2 q = *reinterpret_cast<const uint2*>(src);
+                ent[kk][0] = q.x; ent[kk][1] = q.y;
+              }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              const uint4 xv = *reinterpret_cast<const uint4*>(xs + b * XROWB + w8 * 16);
+              uint32_t hw[V / 2];
+#pragma unroll
+              for (int j = 0; j < V / 2; ++j) hw[j] = 0u;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t xw = (&xv.x)[kk / 2];
+#pragma unroll
+                for (int j = 0; j < V / 2; ++j)
+                  hw[j] = (kk & 1) ? hfma2_bcast<1>(ent[kk][j], xw, hw[j]) : hfma2_bcast<0>(ent[kk][j], xw, hw[j]);
+              }
+#pragma unroll
+              for (int j = 0; j < V / 2; ++j) {
+                acc[b][2 * j] = fma_h((uint16_t)(hw[j] & 0xffff), kHalfOne, acc[b][2 * j]);
+                acc[b][2 * j + 1] = fma_h((uint16_t)(hw[j] >> 16), kHalfOne, acc[b][2 * j + 1]);
+              }
+            }
+          }
         }
-      };
-      constexpr int NBR = (R * EB / 4 * RPL <= 32) ? RPL : 32 / (R * EB / 4);  // rows per batch
-      constexpr int NROWS = LOADS * RPL;
-      constexpr int NBATCH = NROWS / NBR;
-      static_assert(NROWS % NBR == 0 && NBR % 8 == 0 || NBR == 4, "batch shape");
-      uint32_t ent[2][NBR * R][V / 2];
-      auto load_batch = [&](int bi, uint32_t (&dst)[NBR * R][V / 2]) {
+      } else {
+      // lookups are issued LB rows at a time ahead of their FMAs (register budget:
+      // 64 per thread at 1024 threads)
+      constexpr int LB = (R == 2 || B >= 4) ? 4 : 8;
 #pragma unroll
-        for (int kk = 0; kk < NBR; ++kk)
-#pragma unroll
-          for (int r = 0; r < R; ++r) load_entry(lookup(bi * NBR + kk, r), dst[kk * R + r]);
-      };
-      uint32_t hw[B][V / 2];  // fp16x2 window accumulators (H2 path), 8 rows per window
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-#pragma unroll
-        for (int j = 0; j < V / 2; ++j) hw[b][j] = 0u;
-      load_batch(0, ent[0]);
-#pragma unroll
-      for (int bi = 0; bi < NBATCH; ++bi) {
-        if (bi + 1 < NBATCH) load_batch(bi + 1, ent[(bi + 1) & 1]);
-        uint4 xv[B][(NBR + 7) / 8];  // the batch's activations (shared-memory broadcast)
-        const int xbase = (bi * NBR) & ~7;  // 16-byte aligned row of the batch's first word
+      for (int w8 = 0; w8 < kSlabRows / 8; ++w8) {  // 8-row fp16 windows
+        uint32_t hw[B][V / 2];
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
-          for (int q = 0; q < (NBR + 7) / 8; ++q)
-            xv[b][q] = *reinterpret_cast<const uint4*>(xs + b * XROWB + (xbase + q * 8) * 2);
+          for (int j = 0; j < V / 2; ++j) hw[b][j] = 0u;
+        uint4 xv[B];  // the window's 8 activations per batch row (shared-memory broadcast)
 #pragma unroll
-        for (int kk = 0; kk < NBR; ++kk) {
-          const int k = bi * NBR + kk;  // row within this warp's slab of the chunk
-          uint32_t xw[B];  // the packed activation pair holding row k (selected by k & 1)
+        for (int b = 0; b < B; ++b) xv[b] = *reinterpret_cast<const uint4*>(xs + b * XROWB + w8 * 16);
 #pragma unroll
-          for (int b = 0; b < B; ++b) {
-            const int kx = k - xbase;
-            xw[b] = (&xv[b][kx / 8].x)[(kx % 8) / 2];
-          }
+        for (int l0 = 0; l0 < 8; l0 += LB) {
+        uint32_t ent[LB][R][V / 2];
+#pragma unroll
+        for (int kk = 0; kk < LB; ++kk)
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const uint32_t (&e)[V / 2] = ent[bi & 1][kk * R + r];
-            if constexpr (H2) {
-              // packed fp16x2 FMA into an 8-row fp16 window (full-rate HFMA2; the
-              // mixed-precision FHFMA issues at a quarter of that rate on sm_100)
-#pragma unroll
-              for (int b = 0; b < B; ++b)
-#pragma unroll
-                for (int j = 0; j < V / 2; ++j)
-                  hw[b][j] = (k & 1) ? hfma2_bcast<1>(e[j], xw[b], hw[b][j]) : hfma2_bcast<0>(e[j], xw[b], hw[b][j]);
+            const uint8_t* src = lookup(w8 * 8 + l0 + kk, r);
+            if constexpr (EB == 16) {
+              const uint4 q = *reinterpret_cast<const uint4*>(src);
+              ent[kk][r][0] = q.x; ent[kk][r][1] = q.y; ent[kk][r][2] = q.z; ent[kk][r][3] = q.w;
             } else {
-#pragma unroll
-              for (int b = 0; b < B; ++b)
-#pragma unroll
-                for (int j = 0; j < V / 2; ++j) {
-                  const uint16_t xh = (uint16_t)((k & 1) ? (xw[b] >> 16) : (xw[b] & 0xffff));
-                  acc[b][2 * j] = fma_h((uint16_t)(e[j] & 0xffff), xh, acc[b][2 * j]);
-                  acc[b][2 * j + 1] = fma_h((uint16_t)(e[j] >> 16), xh, acc[b][2 * j + 1]);
-                }
+              const uint2 q = *reinterpret_cast<const uint2*>(src);
+              ent[kk][r][0] = q.x; ent[kk][r][1] = q.y;
             }
           }
-          if constexpr (H2) {
-            if ((k & 7) == 7) {  // flush the window into the fp32 accumulators (exact widening)
 #pragma unroll
-              for (int b = 0; b < B; ++b)
+        for (int kk = 0; kk < LB; ++kk) {
+          const int k = w8 * 8 + l0 + kk;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              const uint32_t xw = (&xv[b].x)[(k % 8) / 2];  // packed pair holding row k
+              if constexpr (H2) {
+                // packed fp16x2 FMA into the 8-row window, activation broadcast by the
+                // operand selector (full-rate HFMA2; mixed-precision FHFMA is quarter rate)
+#pragma unroll
+                for (int j = 0; j < V / 2; ++j)
+                  hw[b][j] = (k & 1) ? hfma2_bcast<1>(ent[kk][r][j], xw, hw[b][j])
+                                     : hfma2_bcast<0>(ent[kk][r][j], xw, hw[b][j]);
+              } else {
+                const uint16_t xh = (uint16_t)((k & 1) ? (xw >> 16) : (xw & 0xffff));
 #pragma unroll
                 for (int j = 0; j < V / 2; ++j) {
-                  acc[b][2 * j] = fma_h((uint16_t)(hw[b][j] & 0xffff), kHalfOne, acc[b][2 * j]);
-                  acc[b][2 * j + 1] = fma_h((uint16_t)(hw[b][j] >> 16), kHalfOne, acc[b][2 * j + 1]);
-                  hw[b][j] = 0u;
+                  acc[b][2 * j] = fma_h((uint16_t)(ent[kk][r][j] & 0xffff), xh, acc[b][2 * j]);
+                  acc[b][2 * j + 1] = fma_h((uint16_t)(ent[kk][r][j] >> 16), xh, acc[b][2 * j + 1]);
                 }
+              }
             }
           }
         }
+        }
+        if constexpr (H2) {  // flush the window into the fp32 accumulators (exact widening)
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+#pragma unroll
+            for (int j = 0; j < V / 2; ++j) {
+              acc[b][2 * j] = fma_h((uint16_t)(hw[b][j] & 0xffff), kHalfOne, acc[b][2 * j]);
+              acc[b][2 * j + 1] = fma_h((uint16_t)(hw[b][j] >> 16), kHalfOne, acc[b][2 * j + 1]);
+            }
+        }
+      }
       }
     }
     __syncwarp();
@@ -409,16 +445,15 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
     if constexpr (TILE) {
       if (sw) {
         book_commit(cur_buf ^ 1, nb);  // the other buffer was released at the previous swap
-        csync();
+        __syncthreads();
         cur_buf ^= 1;
       }
     }
 
     // ---- end of a span: reduce the WM row-slabs in a fixed order, then write y,
     // publish a partial, or finish a split column block
-    if (u + 1 == u1 || (u + 1) % a.n_chunks == 0) {
+    if (u + 1 == span_end) {
       if (tid == 0 && u + 1 == u1) trace_at(a.trace, 3);
-      const int cb = u / a.n_chunks;
       const int cf = span_first - cb * a.n_chunks;  // first chunk of the span
       const int cl = u - cb * a.n_chunks;           // last chunk
       const bool whole = (cf == 0 && cl == a.n_chunks - 1);
@@ -431,7 +466,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
         for (int q = 0; q < NQ; ++q)
           *reinterpret_cast<float4*>(red + (size_t)wm * COLS + (q * GC + g_local) * 4) =
               make_float4(acc[b][4 * q], acc[b][4 * q + 1], acc[b][4 * q + 2], acc[b][4 * q + 3]);
-        csync();
+        __syncthreads();
         keep[b] = 0.f;
         if (tid < COLS) {
           const int o = tid;
@@ -444,7 +479,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
           else if (finisher) keep[b] = sum;
           else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + b) * COLS + col, tag_partial(sum));
         }
-        csync();
+        __syncthreads();
       }
       if (finisher) {
         // the later spans of this column block are the first spans of the CTAs
@@ -488,6 +523,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_fast_kernel(GemvFastArgs a)
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
       span_first = u + 1;
+      cb += 1;
+      span_end = min(u1, (cb + 1) * a.n_chunks);
     }
   }
   if (tid == 0) trace_at(a.trace, 6);
@@ -559,7 +596,7 @@ struct FastPlan {
   bool ok = false;
   int V = 0, cbytes = 0, R = 0, WG = 1;
   bool tile = false, gtier = true, h2 = true;
-  int n_sh = 0, n_cblk = 0, n_chunks = 0;
+  int n_sh = 0, n_cblk = 0, n_chunks = 0, threads = 0;
   size_t smem = 0;
 };
 
@@ -576,9 +613,10 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   p.R = g.R;
   p.WG = (g.v == 4) ? 2 : 1;
   const int cols_per_cta = 32 * p.WG * g.v;
-  if (g.rows % kChunkRows != 0 || g.cols % cols_per_cta != 0) return p;
+  const int CR = gemv_chunk_rows(p.WG, rows);
+  if (g.rows % kSlabRows != 0 || g.cols % cols_per_cta != 0) return p;
   if (g.sharing == VQB_SHARE_TILE) {
-    if (g.tile_rows % kChunkRows != 0 || g.tile_cols % cols_per_cta != 0) return p;
+    if (g.tile_rows % CR != 0 || g.tile_cols % cols_per_cta != 0) return p;
     p.tile = true;
   } else if (g.sharing != VQB_SHARE_WHOLE) {
     return p;
@@ -595,9 +633,10 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   p.n_sh = n_sh;
   p.h2 = !(L && (L->flags & VQB_FLAG_EXACT_ACCUM));
   p.n_cblk = (int)(g.cols / cols_per_cta);
-  p.n_chunks = (int)(g.rows / kChunkRows);
+  p.n_chunks = (int)((g.rows + CR - 1) / CR);
+  p.threads = gemv_warps(rows) * 32;
   const int nst = gemv_stages(p.tile);
-  const int WM = kConsumerWarps / p.WG;
+  const int WM = gemv_warps(rows) / p.WG;
   const bool wide = !p.gtier && p.R * (p.tile ? 2 : 1) <= 2;  // mirrors the kernel's WIDE layout
   p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows) +
            (wide ? (size_t)65536 : (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128) + (size_t)WM * cols_per_cta * 4 +
@@ -638,7 +677,7 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
     if (it == occ_cache.end()) {
       // always opt in: static shared memory pushes even a 48 KB dynamic request over the default
       VQB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-      VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kGemvThreads, p.smem));
+      VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, p.threads, p.smem));
       occ_cache[key] = occ;
     } else {
       occ = it->second;
@@ -651,7 +690,7 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
   if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemvThreads);
+  cfg.blockDim = dim3(p.threads);
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -734,7 +773,6 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     if ((int64_t)grid * rows * (32 * p.WG * p.V) * 8 > VQB_WS_COUNTER_BYTES - 65536)
       return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
     a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
-    a.debug_nocompute = (L && (L->flags & 64)) ? 1 : 0;
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
     return launch_gemv_kernel(kernel, p, a, st, L);
   }
@@ -781,14 +819,17 @@ int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
 
 int gemv_usage(VqbUsage* u) {
   cudaFuncAttributes at;
-  auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, true, true>;
+  auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, false, true>;
   VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
-  const size_t smem = gemv_stages(false) * stage_total(1, 2, 1, 1) + 256 * 128 + 2 * gemv_stages(false) * 8 + 16;
+  const int threads = gemv_warps(1) * 32;
+  const size_t smem = gemv_stages(false) * stage_total(1, 2, 1, 1) + 65536 + (size_t)gemv_warps(1) * 256 * 4 +
+                      2 * gemv_stages(false) * 8 + 16;
+  VQB_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
   u->shared_bytes = (int)(at.sharedSizeBytes + smem);
   u->regs_per_thread = at.numRegs;
-  u->threads_per_block = kGemvThreads;
+  u->threads_per_block = threads;
   int occ = 0;
-  VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kGemvThreads, smem));
+  VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem));
   u->max_blocks_per_sm = occ;
   return VQB_OK;
 }
