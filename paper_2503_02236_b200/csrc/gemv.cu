@@ -48,19 +48,28 @@ namespace vqb {
 // looked-up entry feeds B FMAs, so fewer warps with more registers do (16 at B=4,
 // 8 at B=8, which keeps the B x V fp32 accumulators in registers).
 __host__ __device__ constexpr int gemv_warps(int B) { return B >= 8 ? 8 : 16; }
-constexpr int kSlabRows = 16;   // rows a warp handles per chunk (one 16-byte code word of u8, two of u16)
+// rows a warp handles per chunk: 16 (one 16-byte code word of u8 codes, two of u16) —
+// 8-row slabs double the per-chunk overhead and measured slower
+__host__ __device__ constexpr int gemv_slab_rows(int cbytes) { return 16; }
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
 // chunk rows: the warps along M each take one 16-row slab (WG = warps across N)
-__host__ __device__ constexpr int gemv_chunk_rows(int WG, int B) { return kSlabRows * (gemv_warps(B) / WG); }
-// ring depth (tile-shared books double-buffer their codebook in the same 64 KB region)
-__host__ __device__ constexpr int gemv_stages(bool tile) { return tile ? 4 : 3; }
+__host__ __device__ constexpr int gemv_chunk_rows(int WG, int B, int cbytes) {
+  return gemv_slab_rows(cbytes) * (gemv_warps(B) / WG);
+}
 // bytes of one chunk's codes: R levels x chunk rows x 32*WG columns
 __host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG, int B) {
-  return R * cbytes * WG * gemv_chunk_rows(WG, B) * 32;
+  return R * cbytes * WG * gemv_chunk_rows(WG, B, cbytes) * 32;
 }
 // a ring stage also carries the chunk's activations: B rows x chunk rows fp16
 __host__ __device__ constexpr int stage_total(int R, int cbytes, int WG, int B) {
-  return stage_bytes(R, cbytes, WG, B) + B * gemv_chunk_rows(WG, B) * 2;
+  return stage_bytes(R, cbytes, WG, B) + B * gemv_chunk_rows(WG, B, cbytes) * 2;
+}
+// ring depth: ~96 KB of code loads in flight per SM (HBM latency x per-SM share of
+// the bandwidth), 3..12 stages
+__host__ __device__ constexpr int gemv_stages(int R, int cbytes, int WG, int B) {
+  return (98304 / stage_total(R, cbytes, WG, B)) < 3    ? 3
+         : (98304 / stage_total(R, cbytes, WG, B)) > 12 ? 12
+                                                        : 98304 / stage_total(R, cbytes, WG, B);
 }
 
 struct GemvFastArgs {
@@ -118,8 +127,9 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
   constexpr int REP = 128 / EB;          // replicas per bank row
   constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code word
   constexpr int WM = kGemvWarps / WG;    // warps along M
-  constexpr int CR = gemv_chunk_rows(WG, B);
-  constexpr int LOADS = kSlabRows / RPL; // code words per lane per level per chunk
+  constexpr int CR = gemv_chunk_rows(WG, B, CBYTES);
+  constexpr int kSlabRows = gemv_slab_rows(CBYTES);
+  constexpr int LOADS = kSlabRows / RPL;  // code words per lane per level per chunk
   constexpr int COLS = 32 * WG * V;      // output columns per column block (256)
   constexpr int GC = 32 * WG;            // sub-vector columns per column block
   constexpr int NQ = V / 4;              // float4 per lane in the cross-warp reduction
@@ -132,11 +142,12 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
   // replica offset (the book base and the half fold into the LDS addressing).
   constexpr bool WIDE = !GTIER && R * NBUF <= 2;
   static_assert(LOADS >= 1, "bad tiling");
+  static_assert(gemv_stages(R, CBYTES, WG, B) >= 3, "the ring refill lags two units");
   constexpr int STAGEB = R * LEVB;
   static_assert(STAGEB == stage_bytes(R, CBYTES, WG, B), "stage size");
   constexpr int XROWB = CR * 2;          // one batch row's activations per chunk
   constexpr int STG = stage_total(R, CBYTES, WG, B);
-  constexpr int kStages = gemv_stages(TILE);
+  constexpr int kStages = gemv_stages(R, CBYTES, WG, B);
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -275,12 +286,13 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
   int span_end = min(u1, (cb + 1) * a.n_chunks);
   for (int u = u0, idx = 0; u < u1; ++u, ++idx) {
     const int s = idx % kStages;
-    // refill the stage unit idx-1 used with unit idx-1+kStages (thread 0 only: it
-    // waits until every warp has released that stage)
-    if (idx >= 1 && idx - 1 + kStages < n) {
+    // refill the stage unit idx-2 used with unit idx-2+kStages (thread 0 only). Lagging
+    // two units means every warp has long released that stage, so warp 0 rarely
+    // waits (lagging one unit made it wait for the slowest warp every unit).
+    if (idx >= 2 && idx - 2 + kStages < n) {
       if (tid == 0) {
-        const int j = idx - 1 + kStages;
-        mbar_wait(empty0 + 8 * (j % kStages), ((idx - 1) / kStages) & 1);
+        const int j = idx - 2 + kStages;
+        mbar_wait(empty0 + 8 * (j % kStages), ((idx - 2) / kStages) & 1);
         expect(j);
         issue_codes(j);
         issue_x(j);
@@ -613,8 +625,8 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   p.R = g.R;
   p.WG = (g.v == 4) ? 2 : 1;
   const int cols_per_cta = 32 * p.WG * g.v;
-  const int CR = gemv_chunk_rows(p.WG, rows);
-  if (g.rows % kSlabRows != 0 || g.cols % cols_per_cta != 0) return p;
+  const int CR = gemv_chunk_rows(p.WG, rows, p.cbytes);
+  if (g.rows % gemv_slab_rows(p.cbytes) != 0 || g.cols % cols_per_cta != 0) return p;
   if (g.sharing == VQB_SHARE_TILE) {
     if (g.tile_rows % CR != 0 || g.tile_cols % cols_per_cta != 0) return p;
     p.tile = true;
@@ -635,7 +647,7 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   p.n_cblk = (int)(g.cols / cols_per_cta);
   p.n_chunks = (int)((g.rows + CR - 1) / CR);
   p.threads = gemv_warps(rows) * 32;
-  const int nst = gemv_stages(p.tile);
+  const int nst = gemv_stages(p.R, p.cbytes, p.WG, rows);
   const int WM = gemv_warps(rows) / p.WG;
   const bool wide = !p.gtier && p.R * (p.tile ? 2 : 1) <= 2;  // mirrors the kernel's WIDE layout
   p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows) +
@@ -822,8 +834,8 @@ int gemv_usage(VqbUsage* u) {
   auto k = gemv_fast_kernel<8, 2, 1, 1, 1, false, false, true>;
   VQB_CUDA_CHECK(cudaFuncGetAttributes(&at, k));
   const int threads = gemv_warps(1) * 32;
-  const size_t smem = gemv_stages(false) * stage_total(1, 2, 1, 1) + 65536 + (size_t)gemv_warps(1) * 256 * 4 +
-                      2 * gemv_stages(false) * 8 + 16;
+  const int nst = gemv_stages(1, 2, 1, 1);
+  const size_t smem = nst * stage_total(1, 2, 1, 1) + 65536 + (size_t)gemv_warps(1) * 256 * 4 + 2 * nst * 8 + 16;
   VQB_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
   u->shared_bytes = (int)(at.sharedSizeBytes + smem);
   u->regs_per_thread = at.numRegs;
