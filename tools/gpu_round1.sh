@@ -1,11 +1,13 @@
+# Round measurement: gpu tests, smoke, bench (both arms), ncu launch list + full captures.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu_info.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1
-tail -40 gpurun_out/pytest_gpu.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -5 gpurun_out/smoke.txt
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; tail -3 gpurun_out/bench1.err; cat gpurun_out/bench1.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-extra --no-cpu > gpurun_out/ncu_launch.log 2>&1; tail -3 gpurun_out/ncu_launch.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_fast -s 200 -c 1 -o gpurun_out/prof_gemv python bench.py --steps 1 --warmup 1 --no-extra --no-cpu > gpurun_out/ncu_gemv.log 2>&1; tail -3 gpurun_out/ncu_gemv.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_cq -s 2 -c 1 -o gpurun_out/prof_attn python bench.py --steps 1 --warmup 1 --no-cpu > gpurun_out/ncu_attn.log 2>&1; tail -3 gpurun_out/ncu_attn.log
+tail -5 gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -3 gpurun_out/smoke.txt
+timeout 600 python bench.py > gpurun_out/bench1.json 2> gpurun_out/bench1.err; tail -3 gpurun_out/bench1.err; cat gpurun_out/bench1.json
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; cat gpurun_out/bench_ref.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemv_fast|attn_cq" -c 300 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launch.log 2>&1; tail -2 gpurun_out/ncu_launch.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_fast -s 8 -c 1 -o gpurun_out/prof_gemv python tools/gemv_sweep.py --cfg quip2 --shapes 4096x12288 --copies 4 > gpurun_out/ncu_gemv.log 2>&1; tail -1 gpurun_out/ncu_gemv.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_cq -s 2 -c 1 -o gpurun_out/prof_attn python tools/attn_bench.py > gpurun_out/ncu_attn.log 2>&1; tail -1 gpurun_out/ncu_attn.log
 ls -la gpurun_out
