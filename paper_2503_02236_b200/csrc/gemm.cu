@@ -214,14 +214,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     // ===== dequantisation producers (warps 2..5) =====
     const int dw = warp - 2;
     const int dtid = dw * 32 + lane;  // 0..127
-    for (int it = 0; it < k_iters; ++it) {
-      const int s = it % STG;
-      // issue the code-word loads before waiting for the stage to drain
-      uint4 cw[R][(WORDS + 127) / 128];
+    // code words are prefetched PF stages ahead into a register ring, so the global
+    // load latency overlaps the dequantisation of the previous stages
+    constexpr int NW = (WORDS + 127) / 128;
+    constexpr int PF = 3;
+    uint4 ring[PF][R][NW];
+    auto fetch = [&](int it, uint4 (&cw)[R][NW]) {
 #pragma unroll
-      for (int i = 0; i < (WORDS + 127) / 128; ++i) {
+      for (int i = 0; i < NW; ++i) {
         const int item = dtid + i * 128;
-        if (item < WORDS) {
+        if (item < WORDS && it < k_iters) {
           const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
           // column-blocked GEMV_IL: 32 groups (256 columns) per block, blocks of M/RPL row groups
           const int gg = n0 / 8 + grp, cb = gg / 32, gi = gg % 32, wb = min(32, a.G - cb * 32);
@@ -230,6 +232,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           for (int r = 0; r < R; ++r) cw[r][i] = ldg_stream(a.codes + r * a.level_bytes + word);
         }
       }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p) fetch(p, ring[p]);
+    for (int it0 = 0; it0 < k_iters; it0 += PF)
+#pragma unroll
+    for (int pp = 0; pp < PF; ++pp) {
+      const int it = it0 + pp;
+      if (it >= k_iters) break;
+      const int s = it % STG;
+      uint4 cw[R][NW];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int i = 0; i < NW; ++i) cw[r][i] = ring[pp][r][i];
+      fetch(it + PF, ring[pp]);
       mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
       uint8_t* btile = sb + s * kBBytes;
 #pragma unroll
