@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -216,14 +217,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     const int dtid = dw * 32 + lane;  // 0..127
     // code words are prefetched PF stages ahead into a register ring, so the global
     // load latency overlaps the dequantisation of the previous stages
-    constexpr int NW = (WORDS + 127) / 128;
+    // 128 producer threads: with u16 codes (128 words per level per stage) a thread
+    // owns one word (8 rows); with u8 codes (64 words) two threads share a word and
+    // take 8 of its 16 rows each, so every thread dequantises 8 rows x R levels
+    static_assert(WORDS == 128 || WORDS == 64, "producer split");
+    constexpr int NW = 1;
+    constexpr int KROWS = 8;                   // rows per thread per word
+    const int my_item = dtid % WORDS;
+    const int k_off = (dtid / WORDS) * KROWS;  // 0, or 8 for the upper half of a u8 word
     constexpr int PF = 3;
     uint4 ring[PF][R][NW];
     auto fetch = [&](int it, uint4 (&cw)[R][NW]) {
 #pragma unroll
       for (int i = 0; i < NW; ++i) {
-        const int item = dtid + i * 128;
-        if (item < WORDS && it < k_iters) {
+        const int item = my_item;
+        if (it < k_iters) {
           const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
           // column-blocked GEMV_IL: 32 groups (256 columns) per block, blocks of M/RPL row groups
           const int gg = n0 / 8 + grp, cb = gg / 32, gi = gg % 32, wb = min(32, a.G - cb * 32);
@@ -250,13 +258,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
       uint8_t* btile = sb + s * kBBytes;
 #pragma unroll
-      for (int i = 0; i < (WORDS + 127) / 128; ++i) {
-        const int item = dtid + i * 128;
-        if (item < WORDS) {
+      for (int i = 0; i < NW; ++i) {
+        const int item = my_item;
+        {
           const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
           const int c = grp & 7, nb = grp >> 3;  // 16-byte chunk and 64-column atom
+          // the row offset must be a compile-time constant for cw[] to stay in registers
+          auto rows = [&](auto ko) {
+            constexpr int KO = decltype(ko)::value;
 #pragma unroll
-          for (int k = 0; k < RPL; ++k) {
+          for (int kk = 0; kk < KROWS; ++kk) {
+            const int k = KO + kk;  // compile-time: the code word stays in registers
             float f[8];
             uint4 e;
 #pragma unroll
@@ -316,6 +328,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
             uint8_t* dst = btile + ((r >> 3) * (kTileN / 64) + nb) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
             *reinterpret_cast<uint4*>(dst) = e;
           }
+          };
+          if constexpr (WORDS == 128) rows(std::integral_constant<int, 0>{});
+          else if (k_off == 0) rows(std::integral_constant<int, 0>{});
+          else rows(std::integral_constant<int, 8>{});
         }
       }
       fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
