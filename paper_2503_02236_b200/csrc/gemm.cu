@@ -10,7 +10,7 @@
 //  * warp 0 — TMA producer: X tiles (256 rows x 64 K, fp16/bf16) are loaded with
 //    cp.async.bulk.tensor (SWIZZLE_128B) into a 4-stage ring; this is exactly the
 //    UMMA K-major SW128 canonical layout, so no reshuffle is needed.
-//  * warps 2-5 — dequantisation producers (the paper's "shared" fusion level:
+//  * warps 2-9 — dequantisation producers (the paper's "shared" fusion level:
 //    tcgen05 reads operands only from shared memory / TMEM): each lane takes one
 //    16-byte code word (8 K-rows of one 8-column sub-vector group, GEMV_IL layout),
 //    looks each code up in the replicated, bank-conflict-free shared codebook
@@ -20,7 +20,7 @@
 //  * warp 1 — a single thread issues tcgen05.mma.cta_group::1.kind::f16
 //    (M=128, N=128, K=16) for both accumulators and commits each stage back to
 //    the producers through an mbarrier; the final commit releases the epilogue.
-//  * epilogue (warps 2-5 again, one TMEM lane quarter each): tcgen05.ld 32x32b,
+//  * epilogue (the producer warps again, two per TMEM lane quarter): tcgen05.ld 32x32b,
 //    convert, store.
 #include <cuda.h>
 
@@ -34,7 +34,8 @@ namespace vqb {
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast);
 
-constexpr int kGemmThreads = 192;   // 6 warps
+constexpr int kProdWarps = 8;       // dequantisation producer warps (2..9)
+constexpr int kGemmThreads = 64 + kProdWarps * 32;  // + TMA warp + MMA warp
 constexpr int kTileM = 256;         // rows (two 128-row accumulators)
 constexpr int kTileN = 128;         // output columns (16 sub-vector groups of 8)
 constexpr int kTileK = 64;          // reduction rows per stage (one 128-byte swizzle span)
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STG; ++s) {
       mbar_init(full_a0 + 8 * s, 1);
-      mbar_init(full_b0 + 8 * s, 4);  // one arrive per dequant warp
+      mbar_init(full_b0 + 8 * s, kProdWarps);  // one arrive per dequant warp
       mbar_init(empty0 + 8 * s, 1);   // tcgen05.commit
     }
     mbar_init(tmem_full, 1);
@@ -212,19 +213,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       umma_commit(tmem_full);
     }
   } else {
-    // ===== dequantisation producers (warps 2..5) =====
+    // ===== dequantisation producers (warps 2..2+kProdWarps) =====
     const int dw = warp - 2;
-    const int dtid = dw * 32 + lane;  // 0..127
+    const int dtid = dw * 32 + lane;  // 0..kProdWarps*32-1
     // code words are prefetched PF stages ahead into a register ring, so the global
     // load latency overlaps the dequantisation of the previous stages
-    // 128 producer threads: with u16 codes (128 words per level per stage) a thread
-    // owns one word (8 rows); with u8 codes (64 words) two threads share a word and
-    // take 8 of its 16 rows each, so every thread dequantises 8 rows x R levels
-    static_assert(WORDS == 128 || WORDS == 64, "producer split");
+    // 256 producer threads share the stage's 64 K-rows x 16 groups evenly: a thread
+    // owns one code word (8 rows of u16 codes / 16 rows of u8) and KROWS of its rows,
+    // so every thread dequantises 4 rows x R levels
+    constexpr int NPT = kProdWarps * 32;
+    static_assert(WORDS * RPL % NPT == 0 && NPT % WORDS == 0, "producer split");
     constexpr int NW = 1;
-    constexpr int KROWS = 8;                   // rows per thread per word
+    constexpr int KROWS = WORDS * RPL / NPT;  // rows per thread per word
     const int my_item = dtid % WORDS;
-    const int k_off = (dtid / WORDS) * KROWS;  // 0, or 8 for the upper half of a u8 word
+    const int k_off = (dtid / WORDS) * KROWS;
     constexpr int PF = 3;
     uint4 ring[PF][R][NW];
     auto fetch = [&](int it, uint4 (&cw)[R][NW]) {
@@ -329,9 +331,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
             *reinterpret_cast<uint4*>(dst) = e;
           }
           };
-          if constexpr (WORDS == 128) rows(std::integral_constant<int, 0>{});
-          else if (k_off == 0) rows(std::integral_constant<int, 0>{});
-          else rows(std::integral_constant<int, 8>{});
+          static_assert(RPL / KROWS <= 4, "row-offset dispatch");
+          if (k_off == 0) rows(std::integral_constant<int, 0>{});
+          else if (k_off == KROWS) rows(std::integral_constant<int, (KROWS < RPL ? KROWS : 0)>{});
+          else if (k_off == 2 * KROWS) rows(std::integral_constant<int, (2 * KROWS < RPL ? 2 * KROWS : 0)>{});
+          else rows(std::integral_constant<int, (3 * KROWS < RPL ? 3 * KROWS : 0)>{});
         }
       }
       fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
@@ -343,11 +347,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    constexpr int CPW = (kTileN / 32) / (kProdWarps / 4);  // 32-column chunks per warp
+    const int cc0 = ((warp - 2) / 4) * CPW;                  // warps sharing a quarter split the columns
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int row = row0 + h * 128 + quarter * 32 + lane;
 #pragma unroll
-      for (int cc = 0; cc < kTileN / 32; ++cc) {
+      for (int c2 = 0; c2 < CPW; ++c2) {
+        const int cc = cc0 + c2;
         uint32_t v[32];
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + h * kTileN + cc * 32;
         asm volatile(
