@@ -34,7 +34,7 @@ namespace vqb {
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast);
 
-constexpr int kProdWarps = 8;       // dequantisation producer warps (2..9)
+constexpr int kProdWarps = 16;      // dequantisation producer warps (2..17)
 constexpr int kGemmThreads = 64 + kProdWarps * 32;  // + TMA warp + MMA warp
 constexpr int kTileM = 256;         // rows (two 128-row accumulators)
 constexpr int kTileN = 128;         // output columns (16 sub-vector groups of 8)
@@ -91,6 +91,16 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// Calls f(integral_constant<I * STEP>) for the runtime index idx in [0, N), so the
+// callee can index register arrays with a compile-time row offset.
+template <int I, int N, int STEP, typename F>
+__device__ __forceinline__ void dispatch_rows(int idx, F&& f) {
+  if constexpr (I < N) {
+    if (idx == I) f(std::integral_constant<int, I * STEP>{});
+    else dispatch_rows<I + 1, N, STEP>(idx, f);
+  }
 }
 
 template <typename OutT>
@@ -271,7 +281,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 #pragma unroll
           for (int kk = 0; kk < KROWS; ++kk) {
             const int k = KO + kk;  // compile-time: the code word stays in registers
-            float f[8];
             uint4 e;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -287,55 +296,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
                                   ? *reinterpret_cast<const uint4*>(book + ((size_t)r * kBookEntries + code) * 128 +
                                                                      (lane & 7) * 16)
                                   : __ldg(reinterpret_cast<const uint4*>(a.books + ((int64_t)r * a.K + code) * 8));
-              if constexpr (R == 1) {
+              if (r == 0) {
                 e = q;
               } else {
+                // residual level: packed fp16x2 / bf16x2 add, a single rounding of the
+                // exact two-term sum (the fp32 dequant rounds it to fp32 first; both
+                // agree unless that rounding creates an fp16 tie — within the GEMM
+                // tolerance, never observed on the parity sets)
+                uint32_t* ew = &e.x;
                 const uint32_t* qw = &q.x;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  float lo, hi;
                   if constexpr (BF16) {
-                    lo = __uint_as_float(qw[j] << 16);
-                    hi = __uint_as_float(qw[j] & 0xffff0000u);
+                    const __nv_bfloat162 h = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&ew[j]),
+                                                     *reinterpret_cast<const __nv_bfloat162*>(&qw[j]));
+                    ew[j] = *reinterpret_cast<const uint32_t*>(&h);
                   } else {
-                    const __half2 hv = *reinterpret_cast<const __half2*>(&qw[j]);
-                    lo = __low2float(hv);
-                    hi = __high2float(hv);
-                  }
-                  if (r == 0) {
-                    f[2 * j] = 0.0f + lo;
-                    f[2 * j + 1] = 0.0f + hi;
-                  } else {
-                    f[2 * j] += lo;
-                    f[2 * j + 1] += hi;
+                    const __half2 h = __hadd2(*reinterpret_cast<const __half2*>(&ew[j]),
+                                              *reinterpret_cast<const __half2*>(&qw[j]));
+                    ew[j] = *reinterpret_cast<const uint32_t*>(&h);
                   }
                 }
               }
-            }
-            if constexpr (R > 1) {
-              uint32_t o[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                if constexpr (BF16) {
-                  const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-                  o[j] = *reinterpret_cast<const uint32_t*>(&h);
-                } else {
-                  const __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
-                  o[j] = *reinterpret_cast<const uint32_t*>(&h);
-                }
-              }
-              e = make_uint4(o[0], o[1], o[2], o[3]);
             }
             const int r = blk * RPL + k;  // K-row within the stage
             uint8_t* dst = btile + ((r >> 3) * (kTileN / 64) + nb) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
             *reinterpret_cast<uint4*>(dst) = e;
           }
           };
-          static_assert(RPL / KROWS <= 4, "row-offset dispatch");
-          if (k_off == 0) rows(std::integral_constant<int, 0>{});
-          else if (k_off == KROWS) rows(std::integral_constant<int, (KROWS < RPL ? KROWS : 0)>{});
-          else if (k_off == 2 * KROWS) rows(std::integral_constant<int, (2 * KROWS < RPL ? 2 * KROWS : 0)>{});
-          else rows(std::integral_constant<int, (3 * KROWS < RPL ? 3 * KROWS : 0)>{});
+          dispatch_rows<0, RPL / KROWS, KROWS>(k_off / KROWS, rows);
         }
       }
       fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
