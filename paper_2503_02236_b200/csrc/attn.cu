@@ -140,6 +140,16 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int 
       vc[q] = ldg_stream(vbase + off + q * 512);
     }
   };
+  // L2 prefetch of a later batch (one bulk prefetch of each 2*GPL x 512-byte run):
+  // the register double buffer alone keeps too few bytes in flight to cover the HBM
+  // latency, so the batches PF_AHEAD strides ahead are pulled into L2 meanwhile
+  auto prefetch = [&](int t0) {
+    if (lane == 0 && t0 < tok1) {
+      const int64_t off = (int64_t)(t0 / 32) * 32 * G;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kbase + off), "r"(Q * 512) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vbase + off), "r"(Q * 512) : "memory");
+    }
+  };
   auto batch = [&](const uint4 (&kc)[Q], const uint4 (&vc)[Q]) {
     // K phase: lane partial logits for the 32 slots (slot i = token i ^ lane)
     auto partial = [&](int i) {
@@ -209,12 +219,16 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int 
   if (t0 >= tok1) return;
   constexpr int STRIDE = kAttnWarps * 32;
   uint4 kb[Q], vb[Q];
+  constexpr int PF_AHEAD = 3;
+  for (int p = 2; p <= PF_AHEAD; ++p) prefetch(t0 + p * STRIDE);
   for (; t0 < tok1; t0 += 2 * STRIDE) {
     const bool has_b = t0 + STRIDE < tok1;
     if (has_b) load(kb, vb, t0 + STRIDE);
+    prefetch(t0 + (PF_AHEAD + 1) * STRIDE);
     batch(ka, va);
     if (has_b) {
       if (t0 + 2 * STRIDE < tok1) load(ka, va, t0 + 2 * STRIDE);
+      prefetch(t0 + (PF_AHEAD + 2) * STRIDE);
       batch(kb, vb);
     }
   }
