@@ -18,6 +18,11 @@
  *   vqb_query_usage  <- sim.KERNEL_USAGE (sim.py:53-57): real per-kernel resource usage
  *                       feeding compute_slack (cacheplan.py:27-62)
  *   vqb_last_error   <- the message of the raised vqforge.errors exception (errors.py:4-25)
+ *   vqb_cq_quantize  <- vqforge.codec.quantize / _nearest (codec.py:239-253, 367-389) for KV rows:
+ *                       online nearest-centroid quantization of new tokens into a KV cache
+ *   vqb_attn_decode_len, vqb_rmsnorm, vqb_qkv_rope, vqb_silu_mul, vqb_add_len
+ *                    <- the end-to-end decode step around the fused ops (
+ *                       no vqforge counterpart: the reference stops at single fused kernels)
  *
  * Conventions
  *  - Plain pointers and sizes only. Every pointer named d_* is DEVICE memory owned
@@ -175,6 +180,37 @@ int vqb_attn_decode(const VqbTensor* k, const VqbTensor* v, const void* d_q,
                     int32_t q_dtype, int32_t B, int32_t H, int32_t T, int32_t C,
                     void* d_out, int32_t out_dtype, const VqbLaunch* launch,
                     void* d_ws, size_t ws_bytes, void* stream);
+
+/* Decode attention over the first T tokens of a KV cache whose capacity is dims[2]
+ * (a partial last 32-token batch is masked). If d_len is non-NULL the valid length
+ * is read on the device at launch (d_len[0], clamped to the capacity), so a decode
+ * step can replay as a CUDA graph while the cache grows; T is then ignored except
+ * for validation (1 <= T <= capacity). */
+int vqb_attn_decode_len(const VqbTensor* k, const VqbTensor* v, const void* d_q, int32_t q_dtype, int32_t B,
+                        int32_t H, int32_t T, int32_t C, const int32_t* d_len, void* d_out, int32_t out_dtype,
+                        const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Online KV quantization (codec.py:367-389): nearest centroid (float64 distance,
+ * lowest index on ties) of n_tok new rows per (b, h) into the (B, H, T_cap, C) code
+ * stream of t (KV_IL or PLAIN layout, fp16 codebooks, any R). Row (b, h, j) of the
+ * input is at d_x + b*xs_b + h*xs_h + j*xs_t elements (channels contiguous, fp16 or
+ * fp32). The rows land at tokens [tok0, tok0 + n_tok), or, if d_len is non-NULL, at
+ * [d_len[0] - n_tok, d_len[0]) read on the device. */
+int vqb_cq_quantize(const VqbTensor* t, const void* d_x, int32_t x_dtype, int64_t xs_b, int64_t xs_h,
+                    int64_t xs_t, int32_t n_tok, int32_t tok0, const int32_t* d_len, void* stream);
+
+/* Llama decode glue (fp16): h = x + residual (residual updated; x may be NULL),
+ * out = weight * rmsnorm(h) with fp32 statistics. */
+int vqb_rmsnorm(const void* d_x, void* d_residual, const void* d_weight, void* d_out, int32_t rows,
+                int32_t dim, float eps, void* stream);
+/* RoPE (rotate-half) at position d_len[0]-1 on the q and k thirds of the fused qkv
+ * output (B, 3*H*C): roped q -> d_q_out (B, H, C), k roped in place. */
+int vqb_qkv_rope(void* d_qkv, void* d_q_out, int32_t B, int32_t H, int32_t C, const int32_t* d_len, float theta,
+                 void* stream);
+/* out (rows, F) = silu(gate) * up for a fused [gate | up] (rows, 2F) input. */
+int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, int32_t ffn, void* stream);
+/* d_len[0] += delta on the stream (advances a graph-replayed decode loop). */
+int vqb_add_len(int32_t* d_len, int32_t delta, void* stream);
 
 /* Convert a PACKED stream (src, layout must be VQB_LAYOUT_PACKED) into
  * `dst_layout`, writing into d_dst (dst_bytes available). Bytes needed are

@@ -53,7 +53,9 @@ struct AttnArgs {
   int out_dtype;
   float* part;   // (B*H, NT, C + 3)
   int* counters; // B*H
-  int B, H, T, NT;
+  int B, H, T, NT;       // valid tokens and 512-token chunks (when len_ptr is null)
+  int T_cap, NT_cap;      // cache capacity (layout stride) and its chunk count
+  const int* len_ptr;     // optional device-resident valid length (decode loops in CUDA graphs)
   float scale_log2;
 };
 
@@ -103,7 +105,7 @@ __device__ __forceinline__ void attn_load_batch(const AttnArgs& a, int bh, int t
                                                 uint4 (&vc)[2 * GPL]) {
   constexpr int G = 32 * GPL;
   const int lane = threadIdx.x & 31;
-  const int64_t base = (int64_t)bh * a.T * G + (int64_t)(t0 / 32) * 32 * G + lane * 16;
+  const int64_t base = (int64_t)bh * a.T_cap * G + (int64_t)(t0 / 32) * 32 * G + lane * 16;
 #pragma unroll
   for (int q = 0; q < 2 * GPL; ++q) {
     kc[q] = ldg_stream(a.kc + base + q * 512);
@@ -112,7 +114,7 @@ __device__ __forceinline__ void attn_load_batch(const AttnArgs& a, int bh, int t
 }
 
 template <int V, int GPL, bool PRMT>
-__device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int tok0, int tok1, uint32_t lut_base,
+__device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int bh, int tok0, int tok1, uint32_t lut_base,
                                                  uint32_t vbook_base, float& m_w, float& l_lane,
                                                  float (&acc)[GPL][V], uint4 (&ka)[2 * GPL],
                                                  uint4 (&va)[2 * GPL]) {
@@ -120,7 +122,7 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int 
   constexpr int G = SM::G, EPB = SM::EPB;
   constexpr int Q = 2 * GPL;  // 16-byte loads per lane per 32-token batch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t TG = (int64_t)a.T * G;
+  const int64_t TG = (int64_t)a.T_cap * G;
   const uint8_t* kbase = a.kc + (int64_t)bh * TG;
   const uint8_t* vbase = a.vc + (int64_t)bh * TG;
   // per-lane columns (and, for the single-prmt form, the region's high address bytes)
@@ -150,7 +152,7 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int 
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vbase + off), "r"(Q * 512) : "memory");
     }
   };
-  auto batch = [&](const uint4 (&kc)[Q], const uint4 (&vc)[Q]) {
+  auto batch = [&](const uint4 (&kc)[Q], const uint4 (&vc)[Q], int tb) {
     // K phase: lane partial logits for the 32 slots (slot i = token i ^ lane)
     auto partial = [&](int i) {
       float acc_s = 0.f;
@@ -176,7 +178,8 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int 
     for (int off = 8; off >= 1; off >>= 1)
 #pragma unroll
       for (int i = 0; i < off; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i + off], off);
-    const float z = s[0];
+    // tokens past the valid length (a partial last batch) get p = 0
+    const float z = (tb + lane < T) ? s[0] : -INFINITY;
     float mb = z;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
@@ -225,11 +228,11 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int bh, int 
     const bool has_b = t0 + STRIDE < tok1;
     if (has_b) load(kb, vb, t0 + STRIDE);
     prefetch(t0 + (PF_AHEAD + 1) * STRIDE);
-    batch(ka, va);
+    batch(ka, va, t0);
     if (has_b) {
       if (t0 + 2 * STRIDE < tok1) load(ka, va, t0 + 2 * STRIDE);
       prefetch(t0 + (PF_AHEAD + 2) * STRIDE);
-      batch(kb, vb);
+      batch(kb, vb, t0 + STRIDE);
     }
   }
 }
@@ -252,7 +255,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   const uint32_t lut_base = smem_u32(lut_s);
   const uint32_t vbook_base = smem_u32(vbook_s);
   constexpr bool aligned = true;  // by construction: single-prmt addressing
-  const int BNT = a.B * a.NT;
+  // valid length: the host's, or read on the device (a graph-replayed decode step)
+  const int T = a.len_ptr ? max(1, min(__ldg(a.len_ptr), a.T_cap)) : a.T;
+  const int NT = (T + kAttnChunk - 1) / kAttnChunk;
+  const int BNT = a.B * NT;
   const int U = a.H * BNT;
   const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
@@ -260,13 +266,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   int cur_h = -1;
   for (int u = u0; u < u1;) {
     const int h = u / BNT;
-    const int b = (u / a.NT) % a.B;
-    const int tc0 = u % a.NT;
-    const int span_end = min(u1, (u / a.NT + 1) * a.NT);
+    const int b = (u / NT) % a.B;
+    const int tc0 = u % NT;
+    const int span_end = min(u1, (u / NT + 1) * NT);
     const int tc1 = tc0 + (span_end - u);
     const int bh = b * a.H + h;
     const int tok0 = tc0 * kAttnChunk;
-    const int tok1 = min(tc1 * kAttnChunk, a.T);
+    const int tok1 = min(tc1 * kAttnChunk, T);
 
     // ---- span prologue. The query and K-book reads for the LUT are issued before
     // waiting for the previous span to release shared memory.
@@ -341,8 +347,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
     uint4 ka[2 * GPL], va[2 * GPL];
     if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va);
-    if (aligned) attn_stream_span<V, GPL, true>(a, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
-    else attn_stream_span<V, GPL, false>(a, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
+    if (aligned) attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
+    else attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
 
     // ---- merge the warps of this span
     float l_w = l_lane;
@@ -358,8 +364,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
 #pragma unroll
       for (int i = 0; i < V; ++i) my[2 + (lane + 32 * j) * V + i] = acc[j][i];
     __syncthreads();
-    const bool whole = (tc0 == 0 && tc1 == a.NT);
-    float* rec = a.part + ((int64_t)bh * a.NT + tc0) * (C + 3);
+    const bool whole = (tc0 == 0 && tc1 == NT);
+    float* rec = a.part + ((int64_t)bh * a.NT_cap + tc0) * (C + 3);
     if (tid <= C) {
       float M = -INFINITY;
 #pragma unroll
@@ -389,20 +395,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     } else {
       __threadfence();
       __syncthreads();
-      if (tid == 0) *s_last = (atomicAdd(a.counters + bh, tc1 - tc0) + (tc1 - tc0) == a.NT);
+      if (tid == 0) *s_last = (atomicAdd(a.counters + bh, tc1 - tc0) + (tc1 - tc0) == NT);
       __syncthreads();
       if (*s_last) {
         __threadfence();
         if (tid < C) {
-          const float* base = a.part + (int64_t)bh * a.NT * (C + 3);
+          const float* base = a.part + (int64_t)bh * a.NT_cap * (C + 3);
           float MM = -INFINITY;
-          for (int tc = 0; tc < a.NT;) {
+          for (int tc = 0; tc < NT;) {
             const float* r = base + (int64_t)tc * (C + 3);
             MM = fmaxf(MM, __ldcg(r));
             tc += (int)__ldcg(r + 2);
           }
           float L = 0.f, A = 0.f;
-          for (int tc = 0; tc < a.NT;) {
+          for (int tc = 0; tc < NT;) {
             const float* r = base + (int64_t)tc * (C + 3);
             const float mi = __ldcg(r);
             const float sc = (mi == -INFINITY) ? 0.f : fast_exp2(mi - MM);
@@ -423,13 +429,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
 // generic path: dense fp32 K/V in the workspace
 
 __global__ void __launch_bounds__(256) attn_dense_kernel(const float* __restrict__ k, const float* __restrict__ v,
-                                                         const void* __restrict__ q, int q_dtype, int T, int C,
+                                                         const void* __restrict__ q, int q_dtype, int T, int T_cap,
+                                                         int C,
                                                          float* __restrict__ logits, void* __restrict__ out,
                                                          int out_dtype) {
   const int bh = blockIdx.x;
-  const float* kb = k + (int64_t)bh * T * C;
-  const float* vb = v + (int64_t)bh * T * C;
-  float* lg = logits + (int64_t)bh * T;
+  const float* kb = k + (int64_t)bh * T_cap * C;
+  const float* vb = v + (int64_t)bh * T_cap * C;
+  float* lg = logits + (int64_t)bh * T_cap;
   __shared__ float red[256];
   const float inv = 1.0f / sqrtf((float)C);
   float mx = -INFINITY;
@@ -509,7 +516,7 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
     VQB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[dev & 63] = true;
   }
-  const int U = a.B * a.H * a.NT;
+  const int U = a.B * a.H * (a.len_ptr ? a.NT_cap : a.NT);  // a device length is bounded by the capacity
   int grid = std::min(U, sm_count());
   if (grid_limit > 0) grid = std::min(grid, grid_limit);
   kern<<<grid, kAttnThreads, smem, st>>>(a);
@@ -519,15 +526,18 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
 }
 
 int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_dtype, int B, int H, int T, int C,
-                  void* out, int out_dtype, const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st,
-                  bool* used_fast) {
+                  const int* d_len, void* out, int out_dtype, const VqbLaunch* L, void* ws, size_t ws_bytes,
+                  cudaStream_t st, bool* used_fast) {
   Geom gk, gv;
   int s = make_geom(k, &gk);
   if (s) return s;
   s = make_geom(v, &gv);
   if (s) return s;
-  if (gk.ndim != 4 || gv.ndim != 4 || gk.dims[0] != B || gk.dims[1] != H || gk.dims[2] != T || gk.dims[3] != C)
+  // T is the number of valid tokens: a prefix of the cache's capacity dims[2]
+  if (gk.ndim != 4 || gv.ndim != 4 || gk.dims[0] != B || gk.dims[1] != H || T < 1 || gk.dims[2] < T ||
+      gk.dims[3] != C)
     return set_error(VQB_ESHAPE, "quantized KV shape does not match op axes (%d, %d, %d, %d)", B, H, T, C);
+  const int T_cap = (int)gk.dims[2];
   for (int i = 0; i < 4; ++i)
     if (gv.dims[i] != gk.dims[i]) return set_error(VQB_ESHAPE, "K and V shapes differ");
   if (q_dtype < VQB_F32 || q_dtype > VQB_BF16 || out_dtype < VQB_F32 || out_dtype > VQB_BF16)
@@ -536,8 +546,10 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
   const int64_t need = attn_ws_bytes(k, BH);
   if ((int64_t)ws_bytes < need || !ws)
     return set_error(VQB_ECAPACITY, "attention workspace too small: %zu < %lld", ws_bytes, (long long)need);
-  const bool fast = attn_fast_ok(gk, gv, k, v, T, L) && BH * 4 <= VQB_WS_COUNTER_BYTES;
+  const bool fast = attn_fast_ok(gk, gv, k, v, T_cap, L) && BH * 4 <= VQB_WS_COUNTER_BYTES;
   if (used_fast) *used_fast = fast;
+  if (!fast && d_len)
+    return set_error(VQB_ECONFIG, "a device-resident KV length needs the fast attention configuration");
   if (fast) {
     AttnArgs a;
     a.kc = reinterpret_cast<const uint8_t*>(k->d_codes);
@@ -554,6 +566,9 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.H = H;
     a.T = T;
     a.NT = (int)ceil_div(T, kAttnChunk);
+    a.T_cap = T_cap;
+    a.NT_cap = (int)ceil_div(T_cap, kAttnChunk);
+    a.len_ptr = d_len;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)C);
     const int gl = L ? L->grid_limit : 0;
     const int gpl = (int)(gk.gpr / 32);
@@ -563,13 +578,14 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     return set_error(VQB_ECONFIG, "no fast attention instance for this configuration");
   }
   float* kd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);
-  float* vd = kd + BH * T * C;
-  float* lg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES + a256(2 * BH * T * C * 4));
+  float* vd = kd + BH * T_cap * C;
+  float* lg =
+      reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES + a256(2 * BH * T_cap * C * 4));
   s = launch_dequant(gk, k, kd, VQB_F32, st);
   if (s) return s;
   s = launch_dequant(gv, v, vd, VQB_F32, st);
   if (s) return s;
-  attn_dense_kernel<<<(unsigned)BH, 256, 0, st>>>(kd, vd, q, q_dtype, T, C, lg, out, out_dtype);
+  attn_dense_kernel<<<(unsigned)BH, 256, 0, st>>>(kd, vd, q, q_dtype, T, T_cap, C, lg, out, out_dtype);
   VQB_LAUNCH_CHECK("attn_dense_kernel");
   set_kernel("attn_generic");
   return VQB_OK;
@@ -595,6 +611,14 @@ int attn_usage(VqbUsage* u) {
 extern "C" int vqb_attn_decode(const VqbTensor* k, const VqbTensor* v, const void* d_q, int32_t q_dtype, int32_t B,
                                int32_t H, int32_t T, int32_t C, void* d_out, int32_t out_dtype,
                                const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
-  return vqb::attn_dispatch(k, v, d_q, q_dtype, B, H, T, C, d_out, out_dtype, launch, d_ws, ws_bytes,
+  return vqb::attn_dispatch(k, v, d_q, q_dtype, B, H, T, C, nullptr, d_out, out_dtype, launch, d_ws, ws_bytes,
+                            reinterpret_cast<cudaStream_t>(stream), nullptr);
+}
+
+extern "C" int vqb_attn_decode_len(const VqbTensor* k, const VqbTensor* v, const void* d_q, int32_t q_dtype,
+                                   int32_t B, int32_t H, int32_t T, int32_t C, const int32_t* d_len, void* d_out,
+                                   int32_t out_dtype, const VqbLaunch* launch, void* d_ws, size_t ws_bytes,
+                                   void* stream) {
+  return vqb::attn_dispatch(k, v, d_q, q_dtype, B, H, T, C, d_len, d_out, out_dtype, launch, d_ws, ws_bytes,
                             reinterpret_cast<cudaStream_t>(stream), nullptr);
 }

@@ -1,0 +1,258 @@
+// decode.cu — the kernels around the fused VQ ops in a Llama decode step (C5):
+// RMSNorm with a fused residual add, RoPE on the fresh q/k, online CQ
+// quantization of the new K/V rows into the KV cache, SiLU-gated FFN glue and the
+// device-resident position counter that lets a whole step replay as a CUDA graph.
+//
+// Online KV quantization is the reference's `quantize` (pkg/src/vqforge/codec.py:
+// 367-389) — nearest centroid per sub-vector and level, residual carried to the next
+// level — with `_nearest`'s float64 distance |c|^2 - 2 p.c (+|p|^2) and its
+// lowest-index tie rule (codec.py:239-253), evaluated on the GPU (the paper's KV
+// online quantization).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vqb {
+
+// ---------------------------------------------------------------------------
+// RMSNorm (Llama): h = x + residual (residual updated in place), out = w * norm(h);
+// statistics in fp32 like the HF reference implementation.
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const __half* __restrict__ x, __half* __restrict__ res,
+                                                          const __half* __restrict__ w, __half* __restrict__ out,
+                                                          int dim, float eps) {
+  const int row = blockIdx.x;
+  const __half* xr = x ? x + (int64_t)row * dim : nullptr;
+  __half* rr = res + (int64_t)row * dim;
+  __half* orow = out + (int64_t)row * dim;
+  __shared__ float red[THREADS / 32];
+  float ss = 0.f;
+  for (int i = threadIdx.x * 2; i < dim; i += THREADS * 2) {
+    float2 h = __half22float2(*reinterpret_cast<const __half2*>(rr + i));
+    if (xr) {
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(xr + i));
+      // the residual stream is fp16: round the sum like the fp16 reference add
+      const __half2 hs = __floats2half2_rn(h.x + a.x, h.y + a.y);
+      *reinterpret_cast<__half2*>(rr + i) = hs;
+      h = __half22float2(hs);
+    }
+    ss += h.x * h.x + h.y * h.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)dim + eps);
+  for (int i = threadIdx.x * 2; i < dim; i += THREADS * 2) {
+    const float2 h = __half22float2(*reinterpret_cast<const __half2*>(rr + i));
+    const float2 ww = __half22float2(*reinterpret_cast<const __half2*>(w + i));
+    // HF: weight * (h * inv).to(fp16)
+    const __half2 hn = __floats2half2_rn(h.x * inv, h.y * inv);
+    const float2 hf = __half22float2(hn);
+    *reinterpret_cast<__half2*>(orow + i) = __floats2half2_rn(ww.x * hf.x, ww.y * hf.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RoPE (rotate-half convention) on the q and k thirds of the fused qkv projection
+// output (B, 3*H*C): q is written roped into a contiguous (B, H, C) buffer for the
+// attention kernel, k is roped in place for the KV quantizer. pos = *d_len - 1.
+
+__global__ void __launch_bounds__(128) qkv_rope_kernel(__half* __restrict__ qkv, __half* __restrict__ q_out, int H,
+                                                       int C, const int* __restrict__ d_len, float log2_theta) {
+  const int b = blockIdx.y, hh = blockIdx.x;  // hh in [0, 2H): q heads then k heads
+  const int half = C / 2;
+  const int pos = __ldg(d_len) - 1;
+  __half* src = qkv + (int64_t)b * 3 * H * C + (int64_t)hh * C;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    // inv_freq = theta^(-2i/C), angle in fp32 like the HF rotary embedding
+    const float inv_freq = exp2f(-log2_theta * (2.0f * i) / (float)C);
+    const float ang = (float)pos * inv_freq;
+    float sn, cs;
+    sincosf(ang, &sn, &cs);
+    const float x0 = __half2float(src[i]), x1 = __half2float(src[i + half]);
+    const __half y0 = __float2half_rn(x0 * cs - x1 * sn);
+    const __half y1 = __float2half_rn(x1 * cs + x0 * sn);
+    if (hh < H) {
+      __half* dst = q_out + ((int64_t)b * H + hh) * C;
+      dst[i] = y0;
+      dst[i + half] = y1;
+    } else {
+      src[i] = y0;
+      src[i + half] = y1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SiLU-gated FFN glue: out[r, i] = silu(gate[r, i]) * up[r, i] with the fused
+// gate_up output laid out [gate (F) | up (F)] per row.
+
+__global__ void __launch_bounds__(256) silu_mul_kernel(const __half* __restrict__ gu, __half* __restrict__ out,
+                                                       int rows, int F) {
+  const int64_t n = (int64_t)rows * F;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F, c = i - r * F;
+    const float g = __half2float(gu[r * 2 * F + c]);
+    const float u = __half2float(gu[r * 2 * F + F + c]);
+    // HF: act(gate) in fp16, then * up in fp16
+    const __half s = __float2half_rn(g / (1.0f + __expf(-g)));
+    out[i] = __float2half_rn(__half2float(s) * u);
+  }
+}
+
+__global__ void add_len_kernel(int* d_len, int delta) { *d_len += delta; }
+
+// ---------------------------------------------------------------------------
+// Nearest-centroid quantization of KV rows into a (B, H, T_cap, C) code stream.
+// One warp per sub-vector: lane l scores entries l, l+32, ...; float64 distances,
+// argmin with the lowest index on ties (codec.py:239-253); R levels quantize the
+// running residual (codec.py:376-381).
+
+template <typename XT>
+__global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restrict__ codes,
+                                                          const __half* __restrict__ books, const XT* __restrict__ x,
+                                                          int64_t xs_b, int64_t xs_h, int64_t xs_t, int n_tok,
+                                                          int tok0, const int* __restrict__ d_len) {
+  const int warps = blockDim.x / 32;
+  const int64_t sv = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);  // sub-vector of the new rows
+  const int lane = threadIdx.x & 31;
+  const int B = (int)g.dims[0], H = (int)g.dims[1];
+  const int G = (int)g.gpr, V = g.v;
+  const int64_t total = (int64_t)B * H * n_tok * G;
+  if (sv >= total) return;
+  const int gi = (int)(sv % G);
+  int64_t rest = sv / G;
+  const int t = (int)(rest % n_tok);
+  rest /= n_tok;
+  const int h = (int)(rest % H);
+  const int b = (int)(rest / H);
+  const int p0 = d_len ? __ldg(d_len) - n_tok : tok0;  // decode: the rows end at the current length
+  const int tok = p0 + t;
+  const XT* xp = x + b * xs_b + h * xs_h + t * xs_t + gi * V;
+  double res[16];
+  for (int j = 0; j < V; ++j) res[j] = (double)to_f32<XT>(xp[j]);
+  // sub-vector index in the reference's row-major order over (B, H, T_cap, C)
+  const int64_t row = ((int64_t)b * H + h) * g.d_T + tok;
+  const int64_t s = row * G + gi;
+  const int region = region_of(g, s);
+  for (int r = 0; r < g.R; ++r) {
+    const __half* book = books + (int64_t)(r * g.n_regions + region) * g.K * V;
+    // d = (-2 * p.c + |c|^2) + |p|^2 in the reference's float64 operation order,
+    // no FMA contraction (codec.py:241-251)
+    double pn = 0.0;
+    for (int j = 0; j < V; ++j) pn = __dadd_rn(pn, __dmul_rn(res[j], res[j]));
+    double best = DBL_MAX;
+    int best_e = 0x7fffffff;
+    for (int e = lane; e < g.K; e += 32) {
+      double dot = 0.0, cn = 0.0;
+      for (int j = 0; j < V; ++j) {
+        const double c = (double)__half2float(book[(int64_t)e * V + j]);
+        dot = __dadd_rn(dot, __dmul_rn(res[j], c));
+        cn = __dadd_rn(cn, __dmul_rn(c, c));
+      }
+      const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
+      if (d < best) {
+        best = d;
+        best_e = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+      if (ob < best || (ob == best && oe < best_e)) {
+        best = ob;
+        best_e = oe;
+      }
+    }
+    if (lane == 0) {
+      const int64_t off = (g.layout == VQB_LAYOUT_PLAIN) ? (int64_t)r * g.S + s : il_offset(g, r, s);
+      if (g.code_bytes == 1) reinterpret_cast<uint8_t*>(codes)[off] = (uint8_t)best_e;
+      else reinterpret_cast<uint16_t*>(codes)[off] = (uint16_t)best_e;
+    }
+    for (int j = 0; j < V; ++j) res[j] -= (double)__half2float(book[(int64_t)best_e * V + j]);
+  }
+}
+
+}  // namespace vqb
+
+using namespace vqb;
+
+extern "C" int vqb_rmsnorm(const void* d_x, void* d_residual, const void* d_weight, void* d_out, int32_t rows,
+                           int32_t dim, float eps, void* stream) {
+  if (rows < 1 || dim < 2 || (dim & 1)) return set_error(VQB_ESHAPE, "rmsnorm needs rows >= 1 and an even dim");
+  rmsnorm_kernel<256><<<rows, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __half*>(d_x), reinterpret_cast<__half*>(d_residual),
+      reinterpret_cast<const __half*>(d_weight), reinterpret_cast<__half*>(d_out), dim, eps);
+  VQB_LAUNCH_CHECK("rmsnorm_kernel");
+  set_kernel("rmsnorm");
+  return VQB_OK;
+}
+
+extern "C" int vqb_qkv_rope(void* d_qkv, void* d_q_out, int32_t B, int32_t H, int32_t C, const int32_t* d_len,
+                            float theta, void* stream) {
+  if (B < 1 || H < 1 || C < 2 || (C & 1) || !d_len) return set_error(VQB_ESHAPE, "bad rope arguments");
+  qkv_rope_kernel<<<dim3(2 * H, B), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<__half*>(d_qkv), reinterpret_cast<__half*>(d_q_out), H, C, d_len, log2f(theta));
+  VQB_LAUNCH_CHECK("qkv_rope_kernel");
+  set_kernel("qkv_rope");
+  return VQB_OK;
+}
+
+extern "C" int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, int32_t ffn, void* stream) {
+  if (rows < 1 || ffn < 1) return set_error(VQB_ESHAPE, "bad silu_mul arguments");
+  const int64_t n = (int64_t)rows * ffn;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
+  silu_mul_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __half*>(d_gate_up), reinterpret_cast<__half*>(d_out), rows, ffn);
+  VQB_LAUNCH_CHECK("silu_mul_kernel");
+  set_kernel("silu_mul");
+  return VQB_OK;
+}
+
+extern "C" int vqb_add_len(int32_t* d_len, int32_t delta, void* stream) {
+  add_len_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_len, delta);
+  VQB_LAUNCH_CHECK("add_len_kernel");
+  return VQB_OK;
+}
+
+extern "C" int vqb_cq_quantize(const VqbTensor* t, const void* d_x, int32_t x_dtype, int64_t xs_b, int64_t xs_h,
+                               int64_t xs_t, int32_t n_tok, int32_t tok0, const int32_t* d_len, void* stream) {
+  Geom g;
+  int s = make_geom(t, &g);
+  if (s) return s;
+  if (g.ndim != 4) return set_error(VQB_ESHAPE, "KV quantization needs a (B, H, T, C) tensor");
+  if (t->codebook_dtype != VQB_F16) return set_error(VQB_ECONFIG, "KV quantization needs fp16 codebooks");
+  if (g.layout != VQB_LAYOUT_KV_IL && g.layout != VQB_LAYOUT_PLAIN)
+    return set_error(VQB_ECONFIG, "KV quantization writes the KV_IL or PLAIN layout");
+  if (g.v > 16 || n_tok < 1) return set_error(VQB_ESHAPE, "bad quantization extent");
+  if (!d_len && (tok0 < 0 || tok0 + n_tok > g.dims[2]))
+    return set_error(VQB_ESHAPE, "tokens [%d, %d) outside the cache capacity %lld", tok0, tok0 + n_tok,
+                     (long long)g.dims[2]);
+  const int64_t total = g.dims[0] * g.dims[1] * (int64_t)n_tok * g.gpr;
+  const int64_t blocks = (total + 7) / 8;
+  if (blocks > INT32_MAX) return set_error(VQB_ESHAPE, "too many sub-vectors");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* codes = const_cast<void*>(t->d_codes);
+  const __half* books = reinterpret_cast<const __half*>(t->d_codebooks);
+  if (x_dtype == VQB_F16)
+    cq_quantize_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>(g, codes, books, reinterpret_cast<const __half*>(d_x),
+                                                                 xs_b, xs_h, xs_t, n_tok, tok0, d_len);
+  else if (x_dtype == VQB_F32)
+    cq_quantize_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, codes, books, reinterpret_cast<const float*>(d_x),
+                                                                xs_b, xs_h, xs_t, n_tok, tok0, d_len);
+  else
+    return set_error(VQB_ECONFIG, "KV quantization takes fp16 or fp32 rows");
+  VQB_LAUNCH_CHECK("cq_quantize_kernel");
+  set_kernel("cq_quantize");
+  return VQB_OK;
+}

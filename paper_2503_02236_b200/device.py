@@ -105,6 +105,19 @@ class DeviceVQTensor:
         return plain if layout == "plain" else plain.relayout(layout)
 
     @classmethod
+    def empty_cache(cls, shape, config: VQConfig, codebooks: torch.Tensor, layout: str = "kv") -> "DeviceVQTensor":
+        """A zero-coded (B, H, T_capacity, C) KV cache over `codebooks`, filled token by
+        token by ops.vq_quantize_kv (the online quantizer)."""
+        shape = tuple(int(s) for s in shape)
+        n_regions = region_count(shape, config)
+        dev = codebooks.device
+        probe = cls(config, shape, n_regions, torch.empty(0, dtype=torch.uint8, device=dev), "plain",
+                    codebooks.contiguous())
+        need = N.check(N.lib().vqb_layout_bytes(probe.struct(), _LAYOUTS[layout]))
+        codes = torch.zeros(need, dtype=torch.uint8, device=dev)
+        return cls(config, shape, n_regions, codes, layout, codebooks.contiguous(), config.n_entries - 1)
+
+    @classmethod
     def from_packed(cls, stream: bytes, shape, config: VQConfig, codebooks, device=None,
                     codebook_dtype="float16", layout: str = "packed") -> "DeviceVQTensor":
         """Ingest the reference packed stream as-is (no host unpacking)."""

@@ -108,8 +108,12 @@ def vq_gemm(w: DeviceVQTensor, x: torch.Tensor, out_dtype=None, launch=None) -> 
 
 
 def vq_attention(k: DeviceVQTensor, v: DeviceVQTensor, q: torch.Tensor, out_dtype=None,
-                 launch=None) -> torch.Tensor:
-    """Decode attention softmax(q K^T / sqrt(C)) V over a VQ KV cache, q (B, H, C)."""
+                 launch=None, length: int = None, d_len: torch.Tensor = None) -> torch.Tensor:
+    """Decode attention softmax(q K^T / sqrt(C)) V over a VQ KV cache, q (B, H, C).
+
+    ``length`` attends to the first tokens of a cache whose capacity is K's T axis;
+    ``d_len`` (a device int32) supplies that length on the device instead, so a
+    decode step can replay as a CUDA graph while the cache grows."""
     if len(k.shape) != 4:
         raise ShapeError(f"quantized K must be (B, H, T, C), got {k.shape}")
     b, h, t, c = k.shape
@@ -123,9 +127,59 @@ def vq_attention(k: DeviceVQTensor, v: DeviceVQTensor, q: torch.Tensor, out_dtyp
     ks, vs = k.struct(), v.struct()
     need = N.check(lib.vqb_workspace_bytes(N.KERNEL_ATTN, ks, b * h, L))
     ws = workspace(need, k.device)
-    N.check(lib.vqb_attn_decode(ks, vs, q.data_ptr(), dtype_enum(q.dtype), b, h, t, c, out.data_ptr(),
-                                dtype_enum(od), L, ws.data_ptr(), ws.numel(), _stream(k.device)))
+    n = t if length is None else int(length)
+    N.check(lib.vqb_attn_decode_len(ks, vs, q.data_ptr(), dtype_enum(q.dtype), b, h, n, c,
+                                    d_len.data_ptr() if d_len is not None else None, out.data_ptr(),
+                                    dtype_enum(od), L, ws.data_ptr(), ws.numel(), _stream(k.device)))
     return out
+
+
+def rmsnorm(x, residual: torch.Tensor, weight: torch.Tensor, eps: float = 1e-5, out=None) -> torch.Tensor:
+    """Llama RMSNorm with the residual add fused: residual += x (in place, fp16;
+    x may be None), returns weight * rmsnorm(residual)."""
+    rows, dim = residual.shape
+    out = torch.empty_like(residual) if out is None else out
+    N.check(N.lib().vqb_rmsnorm(x.data_ptr() if x is not None else None, residual.data_ptr(), weight.data_ptr(),
+                                out.data_ptr(), rows, dim, float(eps), _stream(residual.device)))
+    return out
+
+
+def qkv_rope(qkv: torch.Tensor, heads: int, head_dim: int, d_len: torch.Tensor, theta: float = 10000.0,
+             q_out=None) -> torch.Tensor:
+    """RoPE at position d_len[0]-1 on the q/k thirds of a fused qkv row block; returns q."""
+    b = qkv.shape[0]
+    q_out = torch.empty((b, heads, head_dim), dtype=qkv.dtype, device=qkv.device) if q_out is None else q_out
+    N.check(N.lib().vqb_qkv_rope(qkv.data_ptr(), q_out.data_ptr(), b, heads, head_dim, d_len.data_ptr(),
+                                 float(theta), _stream(qkv.device)))
+    return q_out
+
+
+def silu_mul(gate_up: torch.Tensor, out=None) -> torch.Tensor:
+    rows, f2 = gate_up.shape
+    out = torch.empty((rows, f2 // 2), dtype=gate_up.dtype, device=gate_up.device) if out is None else out
+    N.check(N.lib().vqb_silu_mul(gate_up.data_ptr(), out.data_ptr(), rows, f2 // 2, _stream(gate_up.device)))
+    return out
+
+
+def add_len(d_len: torch.Tensor, delta: int = 1) -> None:
+    N.check(N.lib().vqb_add_len(d_len.data_ptr(), int(delta), _stream(d_len.device)))
+
+
+def vq_quantize_kv(cache: DeviceVQTensor, x: torch.Tensor, tok0: int = 0, d_len: torch.Tensor = None) -> None:
+    """Online KV quantization (reference quantize, codec.py:367-389) of new rows
+    x (B, H, n_tok, C) into the cache at tokens [tok0, tok0 + n_tok) — or ending at
+    d_len[0] (a device int32) when given, for graph-replayed decode steps. Any strides
+    with contiguous channels are accepted."""
+    if len(cache.shape) != 4:
+        raise ShapeError(f"KV cache must be (B, H, T, C), got {cache.shape}")
+    b, h, _, c = cache.shape
+    if x.dim() != 4 or x.shape[0] != b or x.shape[1] != h or x.shape[3] != c or x.stride(3) != 1:
+        raise ShapeError(f"rows {tuple(x.shape)} do not match cache {cache.shape}")
+    if x.dtype not in (torch.float16, torch.float32):
+        raise ConfigError("KV rows must be fp16 or fp32")
+    ptr = d_len.data_ptr() if d_len is not None else None
+    N.check(N.lib().vqb_cq_quantize(cache.struct(), x.data_ptr(), dtype_enum(x.dtype), x.stride(0), x.stride(1),
+                                    x.stride(2), x.shape[2], int(tok0), ptr, _stream(cache.device)))
 
 
 def vq_codes_regions(w: DeviceVQTensor):

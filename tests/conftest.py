@@ -11,7 +11,7 @@ for p in (ROOT, GOLDEN):
     if p not in sys.path:
         sys.path.insert(0, p)
 
-from cases import ATTENTION_CASES, DEQUANT_CASES, MATMUL_CASES  # noqa: E402
+from cases import ATTENTION_CASES, DEQUANT_CASES, MATMUL_CASES, QUANTIZE_CASES  # noqa: E402
 from oracle import vq_oracle as O  # noqa: E402
 
 

@@ -27,6 +27,8 @@ DEQUANT_CASES = [
     ("cg2d", (16, 64), 4, 4, 1, "channel_group", (0, 0), 8, 11, None),
     # v = 16, 3-bit codes, three residual levels on a 3-D tensor
     ("v16r3", (3, 8, 64), 16, 3, 3, "whole", (0, 0), 0, 12, None),
+    # a residual (R=2) KV cache with per-head channel groups
+    ("kv_r2", (1, 2, 32, 64), 4, 6, 2, "channel_group", (0, 0), 4, 13, None),
 ]
 
 # fused-op cases: (name, dequant-case name, op, extra)
@@ -48,3 +50,11 @@ ATTENTION_CASES = [
 ]
 
 PRESETS_FOR_PLANS = ("quip4", "aqlm3", "gptvq2", "cq4", "cq2")
+
+# online KV quantization (V/codec.py:367-389): (name, dequant-case name supplying the
+# config and fp16-rounded books, data seed). Data = synthetic_tensor(shape, seed).
+QUANTIZE_CASES = [
+    ("qz_cq4", "cq4", 21),
+    ("qz_cq2", "cq2", 22),
+    ("qz_r2", "kv_r2", 23),
+]

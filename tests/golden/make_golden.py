@@ -26,8 +26,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REF)
 sys.path.insert(0, HERE)
 
-from cases import ATTENTION_CASES, DEQUANT_CASES, MATMUL_CASES, PRESETS_FOR_PLANS  # noqa: E402
-from vqforge.codec import Sharing, VQConfig, dequantize  # noqa: E402
+from cases import ATTENTION_CASES, DEQUANT_CASES, MATMUL_CASES, PRESETS_FOR_PLANS, QUANTIZE_CASES  # noqa: E402
+from vqforge.codec import Sharing, VQConfig, dequantize, quantize  # noqa: E402
 from vqforge.dataflow import ComputeOp  # noqa: E402
 from vqforge.gpumodel import load_gpu_model  # noqa: E402
 from vqforge.presets import PRESETS  # noqa: E402
@@ -50,7 +50,7 @@ def make_cfg(v, bits, r, sharing, tile, gw):
 
 
 def main():
-    arrays, meta = {}, {"dequant": {}, "matmul": {}, "attention": {}, "plans": {}, "kat": {}}
+    arrays, meta = {}, {"dequant": {}, "matmul": {}, "attention": {}, "plans": {}, "kat": {}, "quantize": {}}
     qts = {}
     for (name, shape, v, bits, r, sharing, tile, gw, seed, work) in DEQUANT_CASES:
         cfg = make_cfg(v, bits, r, sharing, tile, gw)
@@ -107,6 +107,18 @@ def main():
         arrays[f"at_ref_{name}"] = ref
         arrays[f"at_sim_{name}"] = fused
         meta["attention"][name] = {"v_codes_sha": sha(vq.codes), "query_sha": sha(query)}
+
+    # online quantization: the reference's nearest-centroid quantize() with the
+    # fp16-rounded codebooks the device holds
+    for (name, base, dseed) in QUANTIZE_CASES:
+        q, cfg, seed, work = qts[base]
+        q16 = synthetic_quantized(q.shape, cfg, seed, working_entries=work)
+        for cb in q16.codebooks:
+            cb.entries = cb.entries.astype(np.float16).astype(np.float32)
+        data = synthetic_tensor(q.shape, dseed).astype(np.float16).astype(np.float32)
+        qq = quantize(data, q16.codebooks, cfg)
+        arrays[f"qz_codes_{name}"] = qq.codes.astype(np.int32)
+        meta["quantize"][name] = {"data_sha": sha(data), "codes_sha": sha(qq.codes.astype(np.int32))}
 
     # planner outputs at the reference's own configs and the BASELINE configs
     ops = {

@@ -4,7 +4,7 @@ import hashlib
 
 import numpy as np
 import pytest
-from conftest import ATTENTION_CASES, CASES, MATMUL_CASES, Case, O
+from conftest import ATTENTION_CASES, CASES, MATMUL_CASES, QUANTIZE_CASES, Case, O
 
 
 def sha(a):
@@ -73,3 +73,13 @@ def test_dequant_signed_zero_becomes_positive():
     codes = np.array([[0, 1]], np.int32)
     out = O.dequantize(codes, books, (1, 4), 2, 1, np.zeros(2, np.int64))
     assert not np.signbit(out).any()
+
+
+@pytest.mark.parametrize("name,base,dseed", QUANTIZE_CASES)
+def test_quantize_matches_reference(name, base, dseed, meta, arrays):
+    """Online KV quantization oracle vs the reference's quantize() (fp16-rounded books)."""
+    c = Case(base, books_f16=True)
+    data = O.round_f16(O.synthetic_tensor(c.shape, dseed))
+    assert sha(data) == meta["quantize"][name]["data_sha"]
+    codes = O.quantize(data, c.books, c.shape, c.v, c.n_regions, c.regions, c.R)
+    assert np.array_equal(codes, arrays[f"qz_codes_{name}"])
