@@ -1,0 +1,161 @@
+"""End-to-end Llama decode with VQ weights and a CQ-quantized KV cache.
+
+The reference stops at single fused kernels; this module chains them into the decode
+step the paper evaluates end to end: per layer
+
+    RMSNorm(+residual) -> fused VQ GEMV qkv -> RoPE -> online CQ quantization of the
+    new K/V rows (reference quantize, codec.py:367-389) -> decode attention over the
+    CQ cache -> VQ GEMV o -> RMSNorm(+residual) -> VQ GEMV gate|up -> SiLU*up ->
+    VQ GEMV down
+
+then the final RMSNorm, a dense fp16 LM head (cuBLAS, a plain library GEMM) and
+greedy sampling. The current length lives in a device int32 that the step advances
+itself, so one CUDA graph replays every decode step while the cache grows.
+Batches of 1-8 rows take the CUDA-core GEMV, larger batches the tcgen05 GEMM.
+"""
+
+from dataclasses import dataclass
+
+import torch
+
+from .codec import Sharing, VQConfig
+from .device import DeviceVQTensor
+from . import ops
+
+
+@dataclass(frozen=True)
+class LlamaShape:
+    hidden: int = 4096
+    heads: int = 32
+    head_dim: int = 128
+    ffn: int = 11008
+    layers: int = 32
+    vocab: int = 32000
+    rope_theta: float = 10000.0
+    eps: float = 1e-5
+
+
+WEIGHT_CFG = VQConfig(8, 16, 1)  # QuiP#-style E8 VQ (BASELINE C2)
+KV_CFG = VQConfig(2, 8, 1, Sharing.per_channel_group(2))  # CQ-4 (BASELINE C4)
+
+
+@dataclass
+class DecoderLayer:
+    qkv: DeviceVQTensor      # (hidden, 3*hidden): [q | k | v]
+    o: DeviceVQTensor        # (hidden, hidden)
+    gate_up: DeviceVQTensor  # (hidden, 2*ffn): [gate | up]
+    down: DeviceVQTensor     # (ffn, hidden)
+    attn_norm: torch.Tensor
+    ffn_norm: torch.Tensor
+    k_cache: DeviceVQTensor  # (B, heads, T_cap, head_dim) CQ codes
+    v_cache: DeviceVQTensor
+
+
+class VQLlamaDecoder:
+    def __init__(self, shape: LlamaShape, layers, embed: torch.Tensor, final_norm: torch.Tensor,
+                 lm_head: torch.Tensor, batch: int):
+        self.shape = shape
+        self.layers = list(layers)
+        self.embed = embed          # (vocab, hidden) fp16
+        self.final_norm = final_norm
+        self.lm_head = lm_head      # (hidden, vocab) fp16: logits = x @ lm_head
+        self.batch = batch
+        self.device = embed.device
+        self.d_len = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.tokens = torch.zeros(batch, dtype=torch.int64, device=self.device)
+        self.res = torch.zeros((batch, shape.hidden), dtype=torch.float16, device=self.device)
+        self.logits = None
+        self._graph = None
+
+    # -- construction -------------------------------------------------------------------------
+
+    @staticmethod
+    def synthetic(shape: LlamaShape, batch: int, capacity: int, device, seed: int = 0, working_entries: int = 256):
+        """Random weights of the named architecture (no checkpoints offline): codes
+        from the working set, N(0, 0.1) books; CQ books per head and channel group."""
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        d, f = shape.hidden, shape.ffn
+
+        def vq_weight(m, n):
+            s = m * n // WEIGHT_CFG.vector_size
+            codes = torch.randint(0, working_entries, (1, s), generator=g, device=device, dtype=torch.int32)
+            books = (torch.randn((1, WEIGHT_CFG.n_entries, WEIGHT_CFG.vector_size), generator=g, device=device)
+                     * (0.5 / m ** 0.5)).half()
+            return DeviceVQTensor.from_device_codes(codes, (m, n), WEIGHT_CFG, books).relayout("gemv")
+
+        def kv_cache():
+            groups = shape.head_dim // KV_CFG.vector_size
+            books = torch.randn((shape.heads * groups, 256, KV_CFG.vector_size), generator=g, device=device).half()
+            return DeviceVQTensor.empty_cache((batch, shape.heads, capacity, shape.head_dim), KV_CFG, books)
+
+        layers = []
+        for _ in range(shape.layers):
+            layers.append(DecoderLayer(
+                vq_weight(d, 3 * d), vq_weight(d, d), vq_weight(d, 2 * f), vq_weight(f, d),
+                torch.ones(d, dtype=torch.float16, device=device), torch.ones(d, dtype=torch.float16, device=device),
+                kv_cache(), kv_cache()))
+        embed = torch.randn((shape.vocab, d), generator=g, device=device).half()
+        lm_head = (torch.randn((d, shape.vocab), generator=g, device=device) / d ** 0.5).half()
+        return VQLlamaDecoder(shape, layers, embed, torch.ones(d, dtype=torch.float16, device=device), lm_head, batch)
+
+    # -- the step -----------------------------------------------------------------------------
+
+    def _linear(self, w: DeviceVQTensor, x: torch.Tensor) -> torch.Tensor:
+        if x.shape[0] <= 8 and x.shape[0] in (1, 2, 4, 8):
+            return ops.vq_gemv(w, x, out_dtype=torch.float16)
+        return ops.vq_gemm(w, x, out_dtype=torch.float16)
+
+    def step(self) -> torch.Tensor:
+        """One decode step for the current tokens; returns (and stores) the next ones.
+        Device-side only (capturable): the length counter advances first, so every
+        kernel of the step sees the new token's position as d_len - 1."""
+        sh, b = self.shape, self.batch
+        ops.add_len(self.d_len, 1)
+        self.res.copy_(torch.index_select(self.embed, 0, self.tokens))
+        x = None
+        hc = sh.heads * sh.head_dim
+        for L in self.layers:
+            xn = ops.rmsnorm(x, self.res, L.attn_norm, sh.eps)
+            qkv = self._linear(L.qkv, xn)
+            q = ops.qkv_rope(qkv, sh.heads, sh.head_dim, self.d_len, sh.rope_theta)
+            kv = qkv.view(b, 3, sh.heads, 1, sh.head_dim)
+            ops.vq_quantize_kv(L.k_cache, kv[:, 1], d_len=self.d_len)
+            ops.vq_quantize_kv(L.v_cache, kv[:, 2], d_len=self.d_len)
+            a = ops.vq_attention(L.k_cache, L.v_cache, q, out_dtype=torch.float16, d_len=self.d_len)
+            o = self._linear(L.o, a.view(b, hc))
+            xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)
+            gu = self._linear(L.gate_up, xn)
+            x = self._linear(L.down, ops.silu_mul(gu))
+        xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
+        self.logits = xn @ self.lm_head
+        self.tokens.copy_(torch.argmax(self.logits, dim=-1))
+        return self.tokens
+
+    def capture(self) -> None:
+        """Record one step as a CUDA graph. The warm-up step (on the capture stream)
+        and the capture itself advance the length and the tokens, so both are restored;
+        the KV rows they wrote sit at the position the first replay overwrites."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        saved_len, saved_tok = self.d_len.clone(), self.tokens.clone()
+        with torch.cuda.stream(s):
+            self.step()
+            self.d_len.copy_(saved_len)
+            self.tokens.copy_(saved_tok)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.step()
+            self.d_len.copy_(saved_len)
+            self.tokens.copy_(saved_tok)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self._graph = g
+
+    def replay(self) -> None:
+        if self._graph is None:
+            self.capture()
+        self._graph.replay()
+
+    def set_length(self, n: int) -> None:
+        """Pretend n tokens are already cached (benchmarks at a fixed context)."""
+        self.d_len.fill_(int(n))

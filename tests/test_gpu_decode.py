@@ -141,3 +141,135 @@ def test_rmsnorm_rope_silu(dev):
     hmid = ops.silu_mul(gu)
     ref = torch.nn.functional.silu(gu[:, :F].float()) * gu[:, F:].float()
     assert (hmid.float() - ref).abs().max().item() <= 4e-3 * max(1.0, ref.abs().max().item())
+
+
+# ---- end-to-end decode (C5) against a numpy restatement of the same model ------------------------
+
+def _tiny_model(dev, batch, capacity):
+    from paper_2503_02236_b200.codec import Codebook, QuantizedTensor
+    from paper_2503_02236_b200.decode import KV_CFG, WEIGHT_CFG, DecoderLayer, LlamaShape, VQLlamaDecoder
+    _, DeviceVQTensor, _ = _mods()
+    sh = LlamaShape(hidden=256, heads=4, head_dim=64, ffn=512, layers=2, vocab=512)
+    d, f = sh.hidden, sh.ffn
+    rng = np.random.default_rng(0)
+    host = {}
+
+    def weight(name, m, n, seed):
+        codes, books = O.synthetic_codes_books((m, n), 8, 16, 1, 1, seed, working_entries=256)
+        books = O.round_f16(books * (0.5 / m ** 0.5 / 0.1))
+        q = QuantizedTensor(codes, (m, n), WEIGHT_CFG, [Codebook(books[0], 0, 0)], 1)
+        host[name] = O.dequantize(codes, books, (m, n), 8, 1, np.zeros(m * n // 8, np.int64))
+        return DeviceVQTensor.from_quantized(q, device=dev)
+
+    layers, kv_books = [], []
+    for li in range(sh.layers):
+        kb = O.round_f16(rng.standard_normal((sh.heads * sh.head_dim // 2, 256, 2)).astype(np.float32))
+        vb = O.round_f16(rng.standard_normal((sh.heads * sh.head_dim // 2, 256, 2)).astype(np.float32))
+        kv_books.append((kb, vb))
+        cache = lambda books: DeviceVQTensor.empty_cache((batch, sh.heads, capacity, sh.head_dim), KV_CFG,
+                                                         torch.from_numpy(books).to(dev).half())
+        an = O.round_f16(1 + 0.1 * rng.standard_normal(d).astype(np.float32))
+        fn = O.round_f16(1 + 0.1 * rng.standard_normal(d).astype(np.float32))
+        host[f"an{li}"], host[f"fn{li}"] = an, fn
+        layers.append(DecoderLayer(weight(f"qkv{li}", d, 3 * d, 100 + li), weight(f"o{li}", d, d, 200 + li),
+                                   weight(f"gu{li}", d, 2 * f, 300 + li), weight(f"down{li}", f, d, 400 + li),
+                                   torch.from_numpy(an).to(dev).half(), torch.from_numpy(fn).to(dev).half(),
+                                   cache(kb), cache(vb)))
+    embed = O.round_f16(rng.standard_normal((sh.vocab, d)).astype(np.float32))
+    head = O.round_f16((rng.standard_normal((d, sh.vocab)) / d ** 0.5).astype(np.float32))
+    fin = O.round_f16(1 + 0.1 * rng.standard_normal(d).astype(np.float32))
+    host.update(embed=embed, head=head, fin=fin, kv_books=kv_books)
+    dec = VQLlamaDecoder(sh, layers, torch.from_numpy(embed).to(dev).half(), torch.from_numpy(fin).to(dev).half(),
+                         torch.from_numpy(head).to(dev).half(), batch)
+    return sh, dec, host
+
+
+def _np_decode(sh, host, tokens, steps, capacity):
+    """fp32 restatement of VQLlamaDecoder.step with fp16 rounding where the device
+    stores fp16 tensors; KV rows quantized with the oracle's quantize (nearest)."""
+    r16 = O.round_f16
+    b = len(tokens)
+    d, hh, c, f = sh.hidden, sh.heads, sh.head_dim, sh.ffn
+    kv_codes = [[[] for _ in range(2)] for _ in range(sh.layers)]  # per layer: K/V rows (b, h, t, c) dense
+    toks, logits_all = np.array(tokens), []
+
+    def rms(x, w):
+        x = x.astype(np.float32)
+        inv = 1.0 / np.sqrt((x * x).mean(-1, keepdims=True) + sh.eps)
+        return r16(w * r16(x * inv))
+
+    def nearest_rows(rows, books):  # rows (b, h, c) -> dequantized via nearest entry per group
+        out = np.empty_like(rows)
+        for hi in range(hh):
+            for gi in range(c // 2):
+                bk = books[hi * (c // 2) + gi]
+                idx = O.nearest(rows[:, hi, 2 * gi:2 * gi + 2], bk)
+                out[:, hi, 2 * gi:2 * gi + 2] = bk[idx]
+        return out
+
+    for t in range(steps):
+        pos = t
+        inv_freq = 1.0 / (sh.rope_theta ** (np.arange(0, c, 2, dtype=np.float32) / c))
+        ang = pos * inv_freq
+        cos, sin = np.cos(ang), np.sin(ang)
+        res = host["embed"][toks].astype(np.float32)
+        x = None
+        for li in range(sh.layers):
+            if x is not None:
+                res = r16(res + x)
+            xn = rms(res, host[f"an{li}"])
+            qkv = r16(xn @ host[f"qkv{li}"]).reshape(b, 3, hh, c)
+
+            def rope(v):
+                v0, v1 = v[..., : c // 2], v[..., c // 2:]
+                return r16(np.concatenate([v0 * cos - v1 * sin, v1 * cos + v0 * sin], -1))
+
+            q, k, v = rope(qkv[:, 0]), rope(qkv[:, 1]), qkv[:, 2]
+            kb, vb = host["kv_books"][li]
+            kv_codes[li][0].append(nearest_rows(k, kb))
+            kv_codes[li][1].append(nearest_rows(v, vb))
+            kd = np.stack(kv_codes[li][0], axis=2)
+            vd = np.stack(kv_codes[li][1], axis=2)
+            a = r16(O.attention_ref(q, kd, vd)).reshape(b, d)
+            o = r16(a @ host[f"o{li}"])
+            res = r16(res + o)
+            xn = rms(res, host[f"fn{li}"])
+            gu = r16(xn @ host[f"gu{li}"])
+            s = r16(gu[:, :f] / (1 + np.exp(-gu[:, :f])))
+            x = r16(r16(s * gu[:, f:]) @ host[f"down{li}"])
+        res = r16(res + x)
+        logits = rms(res, host["fin"]) @ host["head"]
+        logits_all.append(logits)
+        toks = logits.argmax(-1)
+    return logits_all
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_decode_matches_numpy_model(batch, dev):
+    capacity, steps = 64, 6
+    sh, dec, host = _tiny_model(dev, batch, capacity)
+    tokens = list(range(3, 3 + batch))
+    dec.tokens.copy_(torch.tensor(tokens, device=dev))
+    ref = _np_decode(sh, host, tokens, steps, capacity)
+    for t in range(steps):
+        dec.step()
+        got = dec.logits.float().cpu().numpy()
+        assert O.rel_err(got, ref[t]) <= 3e-2, (t, O.rel_err(got, ref[t]))
+        assert int(dec.d_len.item()) == t + 1
+
+
+def test_decode_graph_replay_matches_eager(dev):
+    capacity, steps = 64, 5
+    sh, dec, host = _tiny_model(dev, 1, capacity)
+    dec.tokens.fill_(7)
+    eager = []
+    for _ in range(steps):
+        dec.step()
+        eager.append(dec.logits.float().clone())
+    sh2, dec2, _ = _tiny_model(dev, 1, capacity)
+    dec2.tokens.fill_(7)
+    dec2.capture()
+    for t in range(steps):
+        dec2.replay()
+        assert torch.equal(dec2.logits.float(), eager[t]), t
+    assert int(dec2.d_len.item()) == steps
