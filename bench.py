@@ -333,6 +333,29 @@ def time_gemv_single(torch, dev, ops, N, label, cfg_args, shape, work=None):
             "fp16_cublas_us": dense_us, "note": "CUDA graphs over > L2 of distinct weights (both arms)"}
 
 
+def time_decode(torch, dev, batch=1, ctx=4096, reps=10):
+    """C5: end-to-end Llama-7B-shaped decode step (VQ weights + CQ-4 KV cache), one
+    CUDA graph per step at a context of `ctx` cached tokens."""
+    from paper_2503_02236_b200.decode import LlamaShape, VQLlamaDecoder
+    dec = VQLlamaDecoder.synthetic(LlamaShape(), batch, ctx, dev, seed=3)
+    dec.set_length(ctx - 1 - reps - 3)
+    dec.capture()
+    for _ in range(3):
+        dec.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        dec.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    del dec
+    torch.cuda.empty_cache()
+    return {"config": f"C5 llama7b decode quip2 weights + cq4 KV, batch {batch}, ctx {ctx}", "batch": batch,
+            "ms_per_step": ms, "tokens_per_s": batch * 1e3 / ms, "data": "synthetic weights/KV (random init)"}
+
+
 def run_impl(args):
     import torch
     import torch.distributed as dist
@@ -438,6 +461,7 @@ def run_impl(args):
             extra["gemv_c1_gptvq2_q_proj"] = time_gemv_single(
                 torch, dev, ops, N, "C1 gptvq2 VQ<4,8,1> tile256 4096x4096 b1", (4, 8, 1, Sharing.per_tile(256, 256)),
                 (4096, 4096))
+            extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 16)]
             extra["gemv_c2_quip2_q_proj"] = time_gemv_single(
                 torch, dev, ops, N, "C2 quip2 VQ<8,16,1> ws256 4096x4096 b1", (8, 16, 1, Sharing.whole_tensor()),
                 (4096, 4096), work=WORK)

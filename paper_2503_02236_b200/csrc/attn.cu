@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   int* s_last = reinterpret_cast<int*>(smem + scratch_off + SM::scratch_bytes - 16);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_launch_dependents();
+  pdl_wait();  // q, the fresh KV codes and the length come from the preceding kernels
   const uint32_t lut_base = smem_u32(lut_s);
   const uint32_t vbook_base = smem_u32(vbook_s);
   constexpr bool aligned = true;  // by construction: single-prmt addressing
@@ -519,8 +521,7 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
   const int U = a.B * a.H * (a.len_ptr ? a.NT_cap : a.NT);  // a device length is bounded by the capacity
   int grid = std::min(U, sm_count());
   if (grid_limit > 0) grid = std::min(grid, grid_limit);
-  kern<<<grid, kAttnThreads, smem, st>>>(a);
-  VQB_LAUNCH_CHECK("attn_cq_kernel");
+  VQB_CUDA_CHECK(launch_pdl(kern, dim3(grid), dim3(kAttnThreads), smem, st, a));
   set_kernel("attn_cq");
   return VQB_OK;
 }

@@ -22,6 +22,8 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const __half* __restrict__ x, __half* __restrict__ res,
                                                           const __half* __restrict__ w, __half* __restrict__ out,
                                                           int dim, float eps) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int row = blockIdx.x;
   const __half* xr = x ? x + (int64_t)row * dim : nullptr;
   __half* rr = res + (int64_t)row * dim;
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const __half* __restri
 
 __global__ void __launch_bounds__(128) qkv_rope_kernel(__half* __restrict__ qkv, __half* __restrict__ q_out, int H,
                                                        int C, const int* __restrict__ d_len, float log2_theta) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.y, hh = blockIdx.x;  // hh in [0, 2H): q heads then k heads
   const int half = C / 2;
   const int pos = __ldg(d_len) - 1;
@@ -98,6 +102,8 @@ __global__ void __launch_bounds__(128) qkv_rope_kernel(__half* __restrict__ qkv,
 
 __global__ void __launch_bounds__(256) silu_mul_kernel(const __half* __restrict__ gu, __half* __restrict__ out,
                                                        int rows, int F) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t n = (int64_t)rows * F;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / F, c = i - r * F;
@@ -109,7 +115,11 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(const __half* __restrict_
   }
 }
 
-__global__ void add_len_kernel(int* d_len, int delta) { *d_len += delta; }
+__global__ void add_len_kernel(int* d_len, int delta) {
+  pdl_launch_dependents();
+  pdl_wait();
+  *d_len += delta;
+}
 
 // ---------------------------------------------------------------------------
 // Nearest-centroid quantization of KV rows into a (B, H, T_cap, C) code stream.
@@ -122,6 +132,8 @@ __global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restri
                                                           const __half* __restrict__ books, const XT* __restrict__ x,
                                                           int64_t xs_b, int64_t xs_h, int64_t xs_t, int n_tok,
                                                           int tok0, const int* __restrict__ d_len) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int warps = blockDim.x / 32;
   const int64_t sv = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);  // sub-vector of the new rows
   const int lane = threadIdx.x & 31;
@@ -190,9 +202,9 @@ using namespace vqb;
 extern "C" int vqb_rmsnorm(const void* d_x, void* d_residual, const void* d_weight, void* d_out, int32_t rows,
                            int32_t dim, float eps, void* stream) {
   if (rows < 1 || dim < 2 || (dim & 1)) return set_error(VQB_ESHAPE, "rmsnorm needs rows >= 1 and an even dim");
-  rmsnorm_kernel<256><<<rows, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const __half*>(d_x), reinterpret_cast<__half*>(d_residual),
-      reinterpret_cast<const __half*>(d_weight), reinterpret_cast<__half*>(d_out), dim, eps);
+  VQB_CUDA_CHECK(launch_pdl(rmsnorm_kernel<256>, dim3(rows), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                            reinterpret_cast<const __half*>(d_x), reinterpret_cast<__half*>(d_residual),
+                            reinterpret_cast<const __half*>(d_weight), reinterpret_cast<__half*>(d_out), dim, eps));
   VQB_LAUNCH_CHECK("rmsnorm_kernel");
   set_kernel("rmsnorm");
   return VQB_OK;
@@ -201,8 +213,9 @@ extern "C" int vqb_rmsnorm(const void* d_x, void* d_residual, const void* d_weig
 extern "C" int vqb_qkv_rope(void* d_qkv, void* d_q_out, int32_t B, int32_t H, int32_t C, const int32_t* d_len,
                             float theta, void* stream) {
   if (B < 1 || H < 1 || C < 2 || (C & 1) || !d_len) return set_error(VQB_ESHAPE, "bad rope arguments");
-  qkv_rope_kernel<<<dim3(2 * H, B), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<__half*>(d_qkv), reinterpret_cast<__half*>(d_q_out), H, C, d_len, log2f(theta));
+  VQB_CUDA_CHECK(launch_pdl(qkv_rope_kernel, dim3(2 * H, B), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream),
+                            reinterpret_cast<__half*>(d_qkv), reinterpret_cast<__half*>(d_q_out), H, C, d_len,
+                            log2f(theta)));
   VQB_LAUNCH_CHECK("qkv_rope_kernel");
   set_kernel("qkv_rope");
   return VQB_OK;
@@ -212,15 +225,15 @@ extern "C" int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, in
   if (rows < 1 || ffn < 1) return set_error(VQB_ESHAPE, "bad silu_mul arguments");
   const int64_t n = (int64_t)rows * ffn;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
-  silu_mul_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const __half*>(d_gate_up), reinterpret_cast<__half*>(d_out), rows, ffn);
+  VQB_CUDA_CHECK(launch_pdl(silu_mul_kernel, dim3(blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                            reinterpret_cast<const __half*>(d_gate_up), reinterpret_cast<__half*>(d_out), rows, ffn));
   VQB_LAUNCH_CHECK("silu_mul_kernel");
   set_kernel("silu_mul");
   return VQB_OK;
 }
 
 extern "C" int vqb_add_len(int32_t* d_len, int32_t delta, void* stream) {
-  add_len_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_len, delta);
+  VQB_CUDA_CHECK(launch_pdl(add_len_kernel, dim3(1), dim3(1), 0, reinterpret_cast<cudaStream_t>(stream), d_len, delta));
   VQB_LAUNCH_CHECK("add_len_kernel");
   return VQB_OK;
 }
@@ -245,11 +258,11 @@ extern "C" int vqb_cq_quantize(const VqbTensor* t, const void* d_x, int32_t x_dt
   void* codes = const_cast<void*>(t->d_codes);
   const __half* books = reinterpret_cast<const __half*>(t->d_codebooks);
   if (x_dtype == VQB_F16)
-    cq_quantize_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>(g, codes, books, reinterpret_cast<const __half*>(d_x),
-                                                                 xs_b, xs_h, xs_t, n_tok, tok0, d_len);
+    VQB_CUDA_CHECK(launch_pdl(cq_quantize_kernel<__half>, dim3((unsigned)blocks), dim3(256), 0, st, g, codes, books,
+                              reinterpret_cast<const __half*>(d_x), xs_b, xs_h, xs_t, n_tok, tok0, d_len));
   else if (x_dtype == VQB_F32)
-    cq_quantize_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, codes, books, reinterpret_cast<const float*>(d_x),
-                                                                xs_b, xs_h, xs_t, n_tok, tok0, d_len);
+    VQB_CUDA_CHECK(launch_pdl(cq_quantize_kernel<float>, dim3((unsigned)blocks), dim3(256), 0, st, g, codes, books,
+                              reinterpret_cast<const float*>(d_x), xs_b, xs_h, xs_t, n_tok, tok0, d_len));
   else
     return set_error(VQB_ECONFIG, "KV quantization takes fp16 or fp32 rows");
   VQB_LAUNCH_CHECK("cq_quantize_kernel");
