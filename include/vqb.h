@@ -20,7 +20,7 @@
  *   vqb_last_error   <- the message of the raised vqforge.errors exception (errors.py:4-25)
  *   vqb_cq_quantize  <- vqforge.codec.quantize / _nearest (codec.py:239-253, 367-389) for KV rows:
  *                       online nearest-centroid quantization of new tokens into a KV cache
- *   vqb_attn_decode_len, vqb_rmsnorm, vqb_qkv_rope, vqb_silu_mul, vqb_add_len
+ *   vqb_attn_decode_len, vqb_rmsnorm, vqb_qkv_rope, vqb_qkv_rope_append, vqb_silu_mul, vqb_add_len
  *                    <- the end-to-end decode step around the fused ops (
  *                       no vqforge counterpart: the reference stops at single fused kernels)
  *
@@ -207,6 +207,10 @@ int vqb_rmsnorm(const void* d_x, void* d_residual, const void* d_weight, void* d
  * output (B, 3*H*C): roped q -> d_q_out (B, H, C), k roped in place. */
 int vqb_qkv_rope(void* d_qkv, void* d_q_out, int32_t B, int32_t H, int32_t C, const int32_t* d_len, float theta,
                  void* stream);
+/* Fused decode front end: vqb_qkv_rope, then online quantization (as vqb_cq_quantize)
+ * of the roped k and the v rows into k_cache / v_cache at position d_len[0]-1. */
+int vqb_qkv_rope_append(const void* d_qkv, void* d_q_out, const VqbTensor* k_cache, const VqbTensor* v_cache,
+                        int32_t B, int32_t H, int32_t C, const int32_t* d_len, float theta, void* stream);
 /* out (rows, F) = silu(gate) * up for a fused [gate | up] (rows, 2F) input. */
 int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, int32_t ffn, void* stream);
 /* d_len[0] += delta on the stream (advances a graph-replayed decode loop). */

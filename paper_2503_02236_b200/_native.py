@@ -36,7 +36,7 @@ EXPORTS = (
     "vqb_abi_version", "vqb_last_error", "vqb_last_kernel", "vqb_dequant", "vqb_workspace_bytes", "vqb_gemv",
     "vqb_gemm", "vqb_attn_decode", "vqb_layout_bytes", "vqb_repack", "vqb_query_usage",
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
-    "vqb_silu_mul", "vqb_add_len",
+    "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append",
 )
 
 
@@ -116,6 +116,7 @@ def lib():
             L.vqb_rmsnorm.argtypes = [vp, vp, vp, vp, i32, i32, f32, vp]
             L.vqb_qkv_rope.argtypes = [vp, vp, i32, i32, i32, vp, f32, vp]
             L.vqb_silu_mul.argtypes = [vp, vp, i32, i32, vp]
+            L.vqb_qkv_rope_append.argtypes = [vp, vp, T, T, i32, i32, i32, vp, f32, vp]
             L.vqb_add_len.argtypes = [vp, i32, vp]
             L.vqb_cq_quantize.argtypes = [T, vp, i32, i64, i64, i64, i32, i32, vp, vp]
             L.vqb_layout_bytes.argtypes = [T, i32]
@@ -126,7 +127,7 @@ def lib():
             L.vqb_debug_smem_base.restype = ctypes.c_int
             for name in ("vqb_dequant", "vqb_gemv", "vqb_gemm", "vqb_attn_decode", "vqb_repack",
                          "vqb_query_usage", "vqb_attn_decode_len", "vqb_rmsnorm", "vqb_qkv_rope",
-                         "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize"):
+                         "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib

@@ -127,34 +127,12 @@ __global__ void add_len_kernel(int* d_len, int delta) {
 // argmin with the lowest index on ties (codec.py:239-253); R levels quantize the
 // running residual (codec.py:376-381).
 
-template <typename XT>
-__global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restrict__ codes,
-                                                          const __half* __restrict__ books, const XT* __restrict__ x,
-                                                          int64_t xs_b, int64_t xs_h, int64_t xs_t, int n_tok,
-                                                          int tok0, const int* __restrict__ d_len) {
-  pdl_launch_dependents();
-  pdl_wait();
-  const int warps = blockDim.x / 32;
-  const int64_t sv = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);  // sub-vector of the new rows
-  const int lane = threadIdx.x & 31;
-  const int B = (int)g.dims[0], H = (int)g.dims[1];
-  const int G = (int)g.gpr, V = g.v;
-  const int64_t total = (int64_t)B * H * n_tok * G;
-  if (sv >= total) return;
-  const int gi = (int)(sv % G);
-  int64_t rest = sv / G;
-  const int t = (int)(rest % n_tok);
-  rest /= n_tok;
-  const int h = (int)(rest % H);
-  const int b = (int)(rest / H);
-  const int p0 = d_len ? __ldg(d_len) - n_tok : tok0;  // decode: the rows end at the current length
-  const int tok = p0 + t;
-  const XT* xp = x + b * xs_b + h * xs_h + t * xs_t + gi * V;
-  double res[16];
-  for (int j = 0; j < V; ++j) res[j] = (double)to_f32<XT>(xp[j]);
-  // sub-vector index in the reference's row-major order over (B, H, T_cap, C)
-  const int64_t row = ((int64_t)b * H + h) * g.d_T + tok;
-  const int64_t s = row * G + gi;
+// One sub-vector s of a KV tensor: R levels of nearest centroid on the running
+// residual res[0..v) (float64), code written into the tensor's stream. Warp-wide.
+__device__ __forceinline__ void quantize_subvector(const Geom& g, void* __restrict__ codes,
+                                                   const __half* __restrict__ books, double* res, int64_t s,
+                                                   int lane) {
+  const int V = g.v;
   const int region = region_of(g, s);
   for (int r = 0; r < g.R; ++r) {
     const __half* book = books + (int64_t)(r * g.n_regions + region) * g.K * V;
@@ -195,6 +173,91 @@ __global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restri
   }
 }
 
+template <typename XT>
+__global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restrict__ codes,
+                                                          const __half* __restrict__ books, const XT* __restrict__ x,
+                                                          int64_t xs_b, int64_t xs_h, int64_t xs_t, int n_tok,
+                                                          int tok0, const int* __restrict__ d_len) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int warps = blockDim.x / 32;
+  const int64_t sv = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);  // sub-vector of the new rows
+  const int lane = threadIdx.x & 31;
+  const int B = (int)g.dims[0], H = (int)g.dims[1];
+  const int G = (int)g.gpr, V = g.v;
+  const int64_t total = (int64_t)B * H * n_tok * G;
+  if (sv >= total) return;
+  const int gi = (int)(sv % G);
+  int64_t rest = sv / G;
+  const int t = (int)(rest % n_tok);
+  rest /= n_tok;
+  const int h = (int)(rest % H);
+  const int b = (int)(rest / H);
+  const int p0 = d_len ? __ldg(d_len) - n_tok : tok0;  // decode: the rows end at the current length
+  const int tok = p0 + t;
+  const XT* xp = x + b * xs_b + h * xs_h + t * xs_t + gi * V;
+  double res[16];
+  for (int j = 0; j < V; ++j) res[j] = (double)to_f32<XT>(xp[j]);
+  // sub-vector index in the reference's row-major order over (B, H, T_cap, C)
+  const int64_t row = ((int64_t)b * H + h) * g.d_T + tok;
+  quantize_subvector(g, codes, books, res, row * G + gi, lane);
+}
+
+// Fused decode-step front end, one warp per work item (so the float64 nearest-
+// centroid searches of every K and V sub-vector run in parallel): per (batch row,
+// head), G warps rope + quantize k sub-vectors, G warps quantize v sub-vectors and
+// one warp ropes q into the contiguous buffer the attention reads. One launch
+// instead of three (rope, quantize K, quantize V); codes land at d_len[0]-1.
+__device__ __forceinline__ float rope_channel(const __half* x, int c, int C, float log2_theta, int pos) {
+  const int half = C / 2;
+  const int i = c < half ? c : c - half;
+  const float inv_freq = exp2f(-log2_theta * (2.0f * i) / (float)C);
+  float sn, cs;
+  sincosf((float)pos * inv_freq, &sn, &cs);
+  const float x0 = __half2float(x[i]), x1 = __half2float(x[i + half]);
+  return c < half ? x0 * cs - x1 * sn : x1 * cs + x0 * sn;
+}
+
+__global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __restrict__ qkv, __half* __restrict__ q_out,
+                                                              Geom gk, void* __restrict__ kcodes,
+                                                              const __half* __restrict__ kbooks, Geom gv,
+                                                              void* __restrict__ vcodes,
+                                                              const __half* __restrict__ vbooks, int B, int H, int C,
+                                                              const int* __restrict__ d_len, float log2_theta) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int G = C / gk.v;
+  const int per_head = 2 * G + 1;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (int64_t)B * H * per_head) return;
+  const int lane = threadIdx.x & 31;
+  const int role = (int)(w % per_head);
+  const int h = (int)((w / per_head) % H), b = (int)(w / per_head / H);
+  const int pos = __ldg(d_len) - 1;
+  const __half* row = qkv + (int64_t)b * 3 * H * C;
+  if (role == 2 * G) {  // q: rope into the contiguous (B, H, C) buffer
+    const __half* q = row + (int64_t)h * C;
+    __half* dst = q_out + ((int64_t)b * H + h) * C;
+    for (int c = lane; c < C; c += 32) dst[c] = __float2half_rn(rope_channel(q, c, C, log2_theta, pos));
+    return;
+  }
+  const bool is_k = role < G;
+  const Geom& g = is_k ? gk : gv;
+  const int gi = is_k ? role : role - G;
+  double res[16];
+  if (is_k) {
+    // the roped k is an fp16 tensor in the reference step: round before quantizing
+    const __half* k = row + (int64_t)(H + h) * C;
+    for (int j = 0; j < g.v; ++j)
+      res[j] = (double)__half2float(__float2half_rn(rope_channel(k, gi * g.v + j, C, log2_theta, pos)));
+  } else {
+    const __half* v = row + (int64_t)(2 * H + h) * C;
+    for (int j = 0; j < g.v; ++j) res[j] = (double)__half2float(v[gi * g.v + j]);
+  }
+  const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
+  quantize_subvector(g, is_k ? kcodes : vcodes, is_k ? kbooks : vbooks, res, s, lane);
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -218,6 +281,36 @@ extern "C" int vqb_qkv_rope(void* d_qkv, void* d_q_out, int32_t B, int32_t H, in
                             log2f(theta)));
   VQB_LAUNCH_CHECK("qkv_rope_kernel");
   set_kernel("qkv_rope");
+  return VQB_OK;
+}
+
+extern "C" int vqb_qkv_rope_append(const void* d_qkv, void* d_q_out, const VqbTensor* k_cache,
+                                   const VqbTensor* v_cache, int32_t B, int32_t H, int32_t C, const int32_t* d_len,
+                                   float theta, void* stream) {
+  Geom gk, gv;
+  int s = make_geom(k_cache, &gk);
+  if (s) return s;
+  s = make_geom(v_cache, &gv);
+  if (s) return s;
+  if (!d_len || C < 2 || (C & 1)) return set_error(VQB_ESHAPE, "bad rope/append arguments");
+  for (const Geom* g : {&gk, &gv}) {
+    if (g->ndim != 4 || g->dims[0] != B || g->dims[1] != H || g->cols != C)
+      return set_error(VQB_ESHAPE, "KV cache shape does not match (B, H, *, C) = (%d, %d, *, %d)", B, H, C);
+    if (g->v > 16 || (g->layout != VQB_LAYOUT_KV_IL && g->layout != VQB_LAYOUT_PLAIN))
+      return set_error(VQB_ECONFIG, "KV append writes the KV_IL or PLAIN layout");
+  }
+  if (gk.v != gv.v) return set_error(VQB_ECONFIG, "K and V caches need one vector size");
+  if (k_cache->codebook_dtype != VQB_F16 || v_cache->codebook_dtype != VQB_F16)
+    return set_error(VQB_ECONFIG, "KV append needs fp16 codebooks");
+  const int64_t warps = (int64_t)B * H * (2 * (C / gk.v) + 1);
+  VQB_CUDA_CHECK(launch_pdl(qkv_rope_append_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0,
+                            reinterpret_cast<cudaStream_t>(stream),
+                            reinterpret_cast<const __half*>(d_qkv), reinterpret_cast<__half*>(d_q_out), gk,
+                            const_cast<void*>(k_cache->d_codes),
+                            reinterpret_cast<const __half*>(k_cache->d_codebooks), gv,
+                            const_cast<void*>(v_cache->d_codes),
+                            reinterpret_cast<const __half*>(v_cache->d_codebooks), B, H, C, d_len, log2f(theta)));
+  set_kernel("qkv_rope_append");
   return VQB_OK;
 }
 

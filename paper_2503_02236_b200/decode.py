@@ -118,10 +118,7 @@ class VQLlamaDecoder:
         for L in self.layers:
             xn = ops.rmsnorm(x, self.res, L.attn_norm, sh.eps)
             qkv = self._linear(L.qkv, xn)
-            q = ops.qkv_rope(qkv, sh.heads, sh.head_dim, self.d_len, sh.rope_theta)
-            kv = qkv.view(b, 3, sh.heads, 1, sh.head_dim)
-            ops.vq_quantize_kv(L.k_cache, kv[:, 1], d_len=self.d_len)
-            ops.vq_quantize_kv(L.v_cache, kv[:, 2], d_len=self.d_len)
+            q = ops.qkv_rope_append(qkv, L.k_cache, L.v_cache, self.d_len, sh.rope_theta)
             a = ops.vq_attention(L.k_cache, L.v_cache, q, out_dtype=torch.float16, d_len=self.d_len)
             o = self._linear(L.o, a.view(b, hc))
             xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)

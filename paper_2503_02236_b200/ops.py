@@ -154,6 +154,17 @@ def qkv_rope(qkv: torch.Tensor, heads: int, head_dim: int, d_len: torch.Tensor, 
     return q_out
 
 
+def qkv_rope_append(qkv: torch.Tensor, k_cache: DeviceVQTensor, v_cache: DeviceVQTensor, d_len: torch.Tensor,
+                    theta: float = 10000.0, q_out=None) -> torch.Tensor:
+    """Fused qkv_rope + online quantization of the roped k and v rows into the caches
+    at position d_len[0]-1; returns the roped q (B, H, C)."""
+    b, h, _, c = k_cache.shape
+    q_out = torch.empty((b, h, c), dtype=qkv.dtype, device=qkv.device) if q_out is None else q_out
+    N.check(N.lib().vqb_qkv_rope_append(qkv.data_ptr(), q_out.data_ptr(), k_cache.struct(), v_cache.struct(), b, h, c,
+                                        d_len.data_ptr(), float(theta), _stream(qkv.device)))
+    return q_out
+
+
 def silu_mul(gate_up: torch.Tensor, out=None) -> torch.Tensor:
     rows, f2 = gate_up.shape
     out = torch.empty((rows, f2 // 2), dtype=gate_up.dtype, device=gate_up.device) if out is None else out

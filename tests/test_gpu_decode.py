@@ -273,3 +273,25 @@ def test_decode_graph_replay_matches_eager(dev):
         dec2.replay()
         assert torch.equal(dec2.logits.float(), eager[t]), t
     assert int(dec2.d_len.item()) == steps
+
+
+def test_qkv_rope_append_matches_separate_kernels(dev):
+    """The fused front end (rope + K/V quantization in one launch) writes the same
+    codes and q as qkv_rope followed by two vq_quantize_kv calls."""
+    from paper_2503_02236_b200.decode import KV_CFG
+    _, DeviceVQTensor, ops = _mods()
+    B, H, C, T = 2, 4, 128, 64
+    g = torch.Generator(device=dev).manual_seed(9)
+    books = [torch.randn((H * C // 2, 256, 2), generator=g, device=dev).half() for _ in range(2)]
+    caches = [[DeviceVQTensor.empty_cache((B, H, T, C), KV_CFG, bk) for bk in books] for _ in range(2)]
+    d_len = torch.full((1,), 37, dtype=torch.int32, device=dev)
+    qkv = torch.randn((B, 3 * H * C), generator=g, device=dev).half()
+    q1 = ops.qkv_rope_append(qkv.clone(), caches[0][0], caches[0][1], d_len)
+    qkv2 = qkv.clone()
+    q2 = ops.qkv_rope(qkv2, H, C, d_len)
+    kv = qkv2.view(B, 3, H, 1, C)
+    ops.vq_quantize_kv(caches[1][0], kv[:, 1], d_len=d_len)
+    ops.vq_quantize_kv(caches[1][1], kv[:, 2], d_len=d_len)
+    assert torch.equal(q1, q2)
+    for i in range(2):
+        assert torch.equal(caches[0][i].codes, caches[1][i].codes)

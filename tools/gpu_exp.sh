@@ -1,3 +1,2 @@
 timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; tail -3 gpurun_out/pytest_gpu.txt
 timeout 900 python tools/decode_bench.py 1 16 64 2>&1 | tail -3
-python tools/attn_bench.py
