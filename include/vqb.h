@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define VQB_ABI_VERSION 1
+#define VQB_ABI_VERSION 2
 
 /* ---- status codes (errors.py:4-25) ---- */
 #define VQB_OK 0
@@ -103,6 +103,9 @@ typedef struct VqbTensor {
   const void* d_codebooks;  /* (R*n_regions, K, v) contiguous, level-major (codec.py:208-209) */
   int32_t max_code;         /* largest code in the stream if known (from the upload-time range
                                check / profiling), else -1; lets a kernel drop its global tier */
+  const void* d_codebooks_t;  /* optional (may be NULL): channel-group books of a (B, H, T, C) KV
+                               tensor re-laid per head as [H][K][C/v][v] (same dtype), so the
+                               attention kernel pulls a head's books with one bulk copy each */
 } VqbTensor;
 
 /* Launch knobs from the planner (FusedPlans, sim.py:229-236). Zero-initialise

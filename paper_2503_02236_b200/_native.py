@@ -58,6 +58,7 @@ class VqbTensor(ctypes.Structure):
         ("codebook_dtype", ctypes.c_int32),
         ("d_codebooks", ctypes.c_void_p),
         ("max_code", ctypes.c_int32),
+        ("d_codebooks_t", ctypes.c_void_p),
     ]
 
 

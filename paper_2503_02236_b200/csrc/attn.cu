@@ -47,6 +47,8 @@ struct AttnArgs {
   const uint8_t* vc;
   const __half* kb;
   const __half* vb;
+  const __half* kbt;  // optional per-head [H][256][G][V] copies: one bulk copy per head
+  const __half* vbt;
   const void* q;
   int q_dtype;
   void* out;
@@ -57,7 +59,16 @@ struct AttnArgs {
   int T_cap, NT_cap;      // cache capacity (layout stride) and its chunk count
   const int* len_ptr;     // optional device-resident valid length (decode loops in CUDA graphs)
   float scale_log2;
+  unsigned long long* trace;  // debug (VqbLaunch.flags & 32): per-CTA phase timestamps, 8 per CTA
 };
+
+__device__ __forceinline__ void attn_trace(const AttnArgs& a, int slot) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 8 + slot] = t;
+  }
+}
 
 template <int V, int GPL>
 struct AttnSmem {
@@ -250,10 +261,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   float* lut_s = reinterpret_cast<float*>(smem + lut_off);
   float* scratch = reinterpret_cast<float*>(smem + scratch_off);
   int* s_last = reinterpret_cast<int*>(smem + scratch_off + SM::scratch_bytes - 16);
+  // mbarrier for the bulk-copied books (8-byte aligned slot at the end of the scratch)
+  const uint32_t book_bar = smem_u32(smem + ((scratch_off + SM::scratch_bytes - 8) & ~7u));
+  const bool bulk_books = (V == 2) && a.kbt != nullptr && a.vbt != nullptr;
+  uint32_t book_phase = 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (bulk_books && threadIdx.x == 0) {
+    mbar_init(book_bar, 1);
+    mbar_fence_init();
+  }
   pdl_launch_dependents();
+  attn_trace(a, 0);
   pdl_wait();  // q, the fresh KV codes and the length come from the preceding kernels
+  attn_trace(a, 1);
   const uint32_t lut_base = smem_u32(lut_s);
   const uint32_t vbook_base = smem_u32(vbook_s);
   constexpr bool aligned = true;  // by construction: single-prmt addressing
@@ -288,6 +309,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     float qv[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) qv[j] = load_as_f32(a.q, a.q_dtype, (int64_t)bh * C + g * V + j) * a.scale_log2;
+    if (bulk_books) {
+      // ---- books by bulk copy: the head's K book lands in the LUT region and its V
+      // book in the V-book region, both already [e][g]; the LUT is then computed in
+      // place (an fp16 pair and its fp32 logit term occupy the same 4 bytes)
+      __syncthreads();  // previous span finished with books / LUT / scratch
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bytes = 256u * G * EPB;
+        mbar_arrive_expect_tx(book_bar, switch_h ? 2 * bytes : bytes);
+        tma_load_1d(smem_u32(lut_s), a.kbt + (int64_t)h * 256 * G * V, bytes, book_bar);
+        if (switch_h) tma_load_1d(smem_u32(vbook_s), a.vbt + (int64_t)h * 256 * G * V, bytes, book_bar);
+      }
+      cur_h = h;
+      mbar_wait(book_bar, book_phase);
+      book_phase ^= 1;
+      uint32_t* lw = reinterpret_cast<uint32_t*>(lut_s);
+      for (int idx = tid; idx < 256 * G; idx += kAttnThreads) {  // idx % G == g for every idx of a thread
+        const uint32_t w = lw[idx];
+        const float k0 = __half2float(__ushort_as_half((unsigned short)(w & 0xffff)));
+        const float k1 = __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+        lut_s[idx] = fmaf(qv[1], k1, qv[0] * k0);
+      }
+      __syncthreads();
+    } else {
     const __half* kbk = a.kb + (int64_t)(h * G + g) * 256 * V;
     uint4 wk[KPER];
 #pragma unroll
@@ -340,7 +385,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       }
     }
     __syncthreads();
-
+    }
+    attn_trace(a, 2);
     float m_w = -INFINITY, l_lane = 0.f;
     float acc[GPL][V];
 #pragma unroll
@@ -352,6 +398,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     if (aligned) attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
     else attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
 
+    attn_trace(a, 3);
     // ---- merge the warps of this span
     float l_w = l_lane;
 #pragma unroll
@@ -403,28 +450,69 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
         __threadfence();
         if (tid < C) {
           const float* base = a.part + (int64_t)bh * a.NT_cap * (C + 3);
-          float MM = -INFINITY;
-          for (int tc = 0; tc < NT;) {
-            const float* r = base + (int64_t)tc * (C + 3);
-            MM = fmaxf(MM, __ldcg(r));
-            tc += (int)__ldcg(r + 2);
+          // The spans of this (b, h) start where CTA ranges start (u0(k) = k*U/grid), so
+          // every record is addressed up front and loaded in parallel (a dependent
+          // walk over the span lengths costs one L2 round trip per span).
+          const int base_u = (h * a.B + b) * NT;
+          auto u0_of = [&](int k) { return (int)((int64_t)k * U / gridDim.x); };
+          int kf = (int)((int64_t)base_u * gridDim.x / U);
+          while (kf > 0 && u0_of(kf) > base_u) --kf;
+          while (kf + 1 < (int)gridDim.x && u0_of(kf + 1) <= base_u) ++kf;
+          constexpr int MAXS = 16;
+          float mi[MAXS], li[MAXS], ai[MAXS];
+          int n_sp = 0;
+#pragma unroll
+          for (int i = 0; i < MAXS; ++i) {
+            const int st = (i == 0) ? base_u : ((kf + i < (int)gridDim.x) ? u0_of(kf + i) : base_u + NT);
+            const bool ok = (i == 0) || (st < base_u + NT);
+            mi[i] = -INFINITY;
+            li[i] = 0.f;
+            ai[i] = 0.f;
+            if (ok) {
+              const float* r = base + (int64_t)(st - base_u) * (C + 3);
+              mi[i] = __ldcg(r);
+              li[i] = __ldcg(r + 1);
+              ai[i] = __ldcg(r + 3 + tid);
+              n_sp = i + 1;
+            }
           }
-          float L = 0.f, A = 0.f;
-          for (int tc = 0; tc < NT;) {
-            const float* r = base + (int64_t)tc * (C + 3);
-            const float mi = __ldcg(r);
-            const float sc = (mi == -INFINITY) ? 0.f : fast_exp2(mi - MM);
-            L += sc * __ldcg(r + 1);
-            A += sc * __ldcg(r + 3 + tid);
-            tc += (int)__ldcg(r + 2);
+          float MM = -INFINITY, L = 0.f, A = 0.f;
+          const bool fits = (kf + MAXS >= (int)gridDim.x) || (u0_of(kf + MAXS) >= base_u + NT);
+          if (fits) {
+#pragma unroll
+            for (int i = 0; i < MAXS; ++i)
+              if (i < n_sp) MM = fmaxf(MM, mi[i]);
+#pragma unroll
+            for (int i = 0; i < MAXS; ++i)
+              if (i < n_sp) {
+                const float sc = (mi[i] == -INFINITY) ? 0.f : fast_exp2(mi[i] - MM);
+                L += sc * li[i];
+                A += sc * ai[i];
+              }
+          } else {  // more spans than MAXS: walk the records
+            for (int tc = 0; tc < NT;) {
+              const float* r = base + (int64_t)tc * (C + 3);
+              MM = fmaxf(MM, __ldcg(r));
+              tc += (int)__ldcg(r + 2);
+            }
+            for (int tc = 0; tc < NT;) {
+              const float* r = base + (int64_t)tc * (C + 3);
+              const float m = __ldcg(r);
+              const float sc = (m == -INFINITY) ? 0.f : fast_exp2(m - MM);
+              L += sc * __ldcg(r + 1);
+              A += sc * __ldcg(r + 3 + tid);
+              tc += (int)__ldcg(r + 2);
+            }
           }
           store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, A / L);
         }
         if (tid == 0) a.counters[bh] = 0;
       }
     }
+    attn_trace(a, 4);
     u = span_end;
   }
+  attn_trace(a, 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -557,6 +645,8 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.vc = reinterpret_cast<const uint8_t*>(v->d_codes);
     a.kb = reinterpret_cast<const __half*>(k->d_codebooks);
     a.vb = reinterpret_cast<const __half*>(v->d_codebooks);
+    a.kbt = reinterpret_cast<const __half*>(k->d_codebooks_t);
+    a.vbt = reinterpret_cast<const __half*>(v->d_codebooks_t);
     a.q = q;
     a.q_dtype = q_dtype;
     a.out = out;
@@ -570,6 +660,8 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.T_cap = T_cap;
     a.NT_cap = (int)ceil_div(T_cap, kAttnChunk);
     a.len_ptr = d_len;
+    a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + 8192)
+                                     : nullptr;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)C);
     const int gl = L ? L->grid_limit : 0;
     const int gpl = (int)(gk.gpr / 32);

@@ -201,7 +201,24 @@ class DeviceVQTensor:
         s.codebook_dtype = _ENUM[self.codebooks.dtype]
         s.d_codebooks = self.codebooks.data_ptr()
         s.max_code = int(self.max_code)
+        bt = self.books_per_head()
+        s.d_codebooks_t = bt.data_ptr() if bt is not None else None
         return s
+
+    def books_per_head(self):
+        """Channel-group books of a KV cache re-laid [H][K][C/v][v] (cached): the
+        attention kernel loads a head's K or V books with one bulk copy (64 KB at
+        CQ-4, C = 128) instead of a strided gather-and-transpose."""
+        cfg = self.config
+        if (len(self.shape) != 4 or cfg.sharing.kind != "channel_group" or cfg.sharing.group_width != cfg.vector_size
+                or cfg.residuals != 1 or self.layout != "kv" or self.codebooks.dtype != torch.float16):
+            return None
+        bt = self.__dict__.get("_books_t")
+        if bt is None or bt.data_ptr() == 0:
+            h, c, v = self.shape[1], self.shape[3], cfg.vector_size
+            bt = self.codebooks.view(h, c // v, cfg.n_entries, v).permute(0, 2, 1, 3).contiguous()
+            self.__dict__["_books_t"] = bt
+        return bt
 
     def relayout(self, layout: str) -> "DeviceVQTensor":
         if layout == self.layout:

@@ -25,7 +25,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert set(declared) == set(N.EXPORTS), (declared, N.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.vqb_abi_version() == 1
+    assert lib.vqb_abi_version() == 2
     nm = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True, text=True).stdout
     for name in declared:
         assert re.search(rf"\bT {name}$", nm, re.M), name
