@@ -120,6 +120,15 @@ def main():
         arrays[f"qz_codes_{name}"] = qq.codes.astype(np.int32)
         meta["quantize"][name] = {"data_sha": sha(data), "codes_sha": sha(qq.codes.astype(np.int32))}
 
+    # VQLF containers (V/container.py:25-49) of a few cases, byte for byte
+    from vqforge.container import dump_quantized
+    meta["vqlf"] = {}
+    for name in ("aqlm3", "gptvq2_edge", "cg2d", "v16r3"):
+        q, cfg, seed, work = qts[name]
+        blob = dump_quantized(q)
+        arrays[f"vqlf_{name}"] = np.frombuffer(blob, dtype=np.uint8)
+        meta["vqlf"][name] = {"sha": hashlib.sha256(blob).hexdigest(), "len": len(blob)}
+
     # planner outputs at the reference's own configs and the BASELINE configs
     ops = {
         "gemm": lambda cfg: ComputeOp.gemm(4096, 4096, 256, residuals=cfg.residuals),
