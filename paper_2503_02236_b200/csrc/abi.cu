@@ -1,3 +1,4 @@
+#include <algorithm>
 // abi.cu — C-ABI plumbing, tensor validation, bit-exact dequantization and
 // code-layout repacking.
 //
@@ -335,12 +336,17 @@ int vqb_query_usage(int32_t kind, const VqbTensor* t, VqbUsage* out) {
 namespace vqb {
 int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L);
 int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH);
+int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows);
 }  // namespace vqb
 
 extern "C" int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t rows, const VqbLaunch* launch) {
   switch (kind) {
-    case VQB_KERNEL_GEMV:
-    case VQB_KERNEL_GEMM: return vqb::gemv_ws_bytes(t, rows, launch);
+    case VQB_KERNEL_GEMV: return vqb::gemv_ws_bytes(t, rows, launch);
+    case VQB_KERNEL_GEMM: {
+      const int64_t a = vqb::gemv_ws_bytes(t, rows, launch);
+      if (a < 0) return a;
+      return std::max(a, vqb::gemm_ws_bytes(t, rows));  // split-K partials, or the generic fallback
+    }
     case VQB_KERNEL_ATTN: return vqb::attn_ws_bytes(t, rows);
     case VQB_KERNEL_DEQUANT: return 0;
     default: return vqb::set_error(VQB_ECONFIG, "unknown kernel kind %d", kind);

@@ -9,6 +9,7 @@
 // lowest-index tie rule (codec.py:239-253), evaluated on the GPU (the paper's KV
 // online quantization).
 #include <cfloat>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -129,30 +130,52 @@ __global__ void add_len_kernel(int* d_len, int delta) {
 
 // One sub-vector s of a KV tensor: R levels of nearest centroid on the running
 // residual res[0..v) (float64), code written into the tensor's stream. Warp-wide.
+template <int V>
 __device__ __forceinline__ void quantize_subvector(const Geom& g, void* __restrict__ codes,
                                                    const __half* __restrict__ books, double* res, int64_t s,
                                                    int lane) {
-  const int V = g.v;
   const int region = region_of(g, s);
   for (int r = 0; r < g.R; ++r) {
     const __half* book = books + (int64_t)(r * g.n_regions + region) * g.K * V;
     // d = (-2 * p.c + |c|^2) + |p|^2 in the reference's float64 operation order,
     // no FMA contraction (codec.py:241-251)
     double pn = 0.0;
+#pragma unroll
     for (int j = 0; j < V; ++j) pn = __dadd_rn(pn, __dmul_rn(res[j], res[j]));
     double best = DBL_MAX;
     int best_e = 0x7fffffff;
-    for (int e = lane; e < g.K; e += 32) {
+    auto consider = [&](int e, const float* c) {
       double dot = 0.0, cn = 0.0;
+#pragma unroll
       for (int j = 0; j < V; ++j) {
-        const double c = (double)__half2float(book[(int64_t)e * V + j]);
-        dot = __dadd_rn(dot, __dmul_rn(res[j], c));
-        cn = __dadd_rn(cn, __dmul_rn(c, c));
+        const double cj = (double)c[j];
+        dot = __dadd_rn(dot, __dmul_rn(res[j], cj));
+        cn = __dadd_rn(cn, __dmul_rn(cj, cj));
       }
       const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
       if (d < best) {
         best = d;
         best_e = e;
+      }
+    };
+    if (V == 2 && g.K == 256) {
+      // the CQ case: all eight of this lane's entries are loaded before any distance,
+      // so the warp pays one L2 round trip instead of eight
+      uint32_t w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = __ldg(reinterpret_cast<const uint32_t*>(book) + lane + 32 * k);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float c[2] = {__half2float(__ushort_as_half((unsigned short)(w[k] & 0xffff))),
+                            __half2float(__ushort_as_half((unsigned short)(w[k] >> 16)))};
+        consider(lane + 32 * k, c);
+      }
+    } else {
+      for (int e = lane; e < g.K; e += 32) {
+        float c[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) c[j] = __half2float(book[(int64_t)e * V + j]);
+        consider(e, c);
       }
     }
 #pragma unroll
@@ -169,7 +192,19 @@ __device__ __forceinline__ void quantize_subvector(const Geom& g, void* __restri
       if (g.code_bytes == 1) reinterpret_cast<uint8_t*>(codes)[off] = (uint8_t)best_e;
       else reinterpret_cast<uint16_t*>(codes)[off] = (uint16_t)best_e;
     }
+#pragma unroll
     for (int j = 0; j < V; ++j) res[j] -= (double)__half2float(book[(int64_t)best_e * V + j]);
+  }
+}
+
+// runtime vector size -> compile-time register arrays
+template <typename F>
+__device__ __forceinline__ void with_v(int v, F&& f) {
+  switch (v) {
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    default: f(std::integral_constant<int, 16>{}); break;
   }
 }
 
@@ -196,11 +231,15 @@ __global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restri
   const int p0 = d_len ? __ldg(d_len) - n_tok : tok0;  // decode: the rows end at the current length
   const int tok = p0 + t;
   const XT* xp = x + b * xs_b + h * xs_h + t * xs_t + gi * V;
-  double res[16];
-  for (int j = 0; j < V; ++j) res[j] = (double)to_f32<XT>(xp[j]);
   // sub-vector index in the reference's row-major order over (B, H, T_cap, C)
   const int64_t row = ((int64_t)b * H + h) * g.d_T + tok;
-  quantize_subvector(g, codes, books, res, row * G + gi, lane);
+  with_v(V, [&](auto vc) {
+    constexpr int VV = decltype(vc)::value;
+    double res[VV];
+#pragma unroll
+    for (int j = 0; j < VV; ++j) res[j] = (double)to_f32<XT>(xp[j]);
+    quantize_subvector<VV>(g, codes, books, res, row * G + gi, lane);
+  });
 }
 
 // Fused decode-step front end, one warp per work item (so the float64 nearest-
@@ -244,18 +283,23 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
   const bool is_k = role < G;
   const Geom& g = is_k ? gk : gv;
   const int gi = is_k ? role : role - G;
-  double res[16];
-  if (is_k) {
-    // the roped k is an fp16 tensor in the reference step: round before quantizing
-    const __half* k = row + (int64_t)(H + h) * C;
-    for (int j = 0; j < g.v; ++j)
-      res[j] = (double)__half2float(__float2half_rn(rope_channel(k, gi * g.v + j, C, log2_theta, pos)));
-  } else {
-    const __half* v = row + (int64_t)(2 * H + h) * C;
-    for (int j = 0; j < g.v; ++j) res[j] = (double)__half2float(v[gi * g.v + j]);
-  }
   const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
-  quantize_subvector(g, is_k ? kcodes : vcodes, is_k ? kbooks : vbooks, res, s, lane);
+  with_v(g.v, [&](auto vc) {
+    constexpr int VV = decltype(vc)::value;
+    double res[VV];
+    if (is_k) {
+      // the roped k is an fp16 tensor in the reference step: round before quantizing
+      const __half* k = row + (int64_t)(H + h) * C;
+#pragma unroll
+      for (int j = 0; j < VV; ++j)
+        res[j] = (double)__half2float(__float2half_rn(rope_channel(k, gi * VV + j, C, log2_theta, pos)));
+    } else {
+      const __half* v = row + (int64_t)(2 * H + h) * C;
+#pragma unroll
+      for (int j = 0; j < VV; ++j) res[j] = (double)__half2float(v[gi * VV + j]);
+    }
+    quantize_subvector<VV>(g, is_k ? kcodes : vcodes, is_k ? kbooks : vbooks, res, s, lane);
+  });
 }
 
 }  // namespace vqb

@@ -52,6 +52,8 @@ struct GemmArgs {
   void* y;
   int y_dtype;
   int rows, M, N, G, K, n_sh;
+  int splits;            // split-K factor (CTAs per output tile); > 1 writes fp32 partials
+  float* part;           // (splits, rows, N) fp32 partials when splits > 1
 };
 
 // ---- tcgen05 / TMA PTX wrappers ----------------------------------------------
@@ -150,9 +152,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_tiles_n = a.N / kTileN;
-  const int tile_n = blockIdx.x % n_tiles_n, tile_m = blockIdx.x / n_tiles_n;
+  // split-K (small row counts): CTA (tile, ks) reduces K stages [it_lo, it_hi) of its tile
+  const int tile = blockIdx.x / a.splits, ks = blockIdx.x % a.splits;
+  const int tile_n = tile % n_tiles_n, tile_m = tile / n_tiles_n;
   const int row0 = tile_m * kTileM, n0 = tile_n * kTileN;
-  const int k_iters = a.M / kTileK;
+  const int k_total = a.M / kTileK;
+  const int it_lo = ks * k_total / a.splits, it_hi = (ks + 1) * k_total / a.splits;
+  const int k_iters = it_hi - it_lo;  // stages of this CTA; local stage j = it - it_lo
 
   // ---- setup: barriers, TMEM, replicated shared codebook
   if (warp == 0 && lane == 0) {
@@ -189,7 +195,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         const int s = it % STG;
         mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
         mbar_arrive_expect_tx(full_a0 + 8 * s, kABytes);
-        tma_load_2d(smem_u32(sa + s * kABytes), &tmap_x, it * kTileK, row0, full_a0 + 8 * s);
+        tma_load_2d(smem_u32(sa + s * kABytes), &tmap_x, (it_lo + it) * kTileK, row0, full_a0 + 8 * s);
       }
     }
   } else if (warp == 1) {
@@ -247,7 +253,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           const int grp = item % (kTileN / 8), blk = item / (kTileN / 8);
           // column-blocked GEMV_IL: 32 groups (256 columns) per block, blocks of M/RPL row groups
           const int gg = n0 / 8 + grp, cb = gg / 32, gi = gg % 32, wb = min(32, a.G - cb * 32);
-          const int64_t word = ((int64_t)cb * 32 * (a.M / RPL) + (int64_t)(it * kTileK / RPL + blk) * wb + gi) * 16;
+          const int64_t word =
+              ((int64_t)cb * 32 * (a.M / RPL) + (int64_t)((it_lo + it) * kTileK / RPL + blk) * wb + gi) * 16;
 #pragma unroll
           for (int r = 0; r < R; ++r) cw[r][i] = ldg_stream(a.codes + r * a.level_bytes + word);
         }
@@ -356,7 +363,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
               "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < a.rows) store_row32<OutT>(a.y, a.y_dtype, (int64_t)row * a.N + n0 + cc * 32, v);
+        if (row < a.rows) {
+          if (a.splits == 1) store_row32<OutT>(a.y, a.y_dtype, (int64_t)row * a.N + n0 + cc * 32, v);
+          else store_row32<float>(a.part + (int64_t)ks * a.rows * a.N, VQB_F32, (int64_t)row * a.N + n0 + cc * 32, v);
+        }
       }
     }
   }
@@ -393,6 +403,42 @@ static size_t gemm_smem(int R) {
   return (size_t)R * kBookBytes + gemm_stages(R) * (kABytes + kBBytes) + (3 * gemm_stages(R) + 1) * 8 + 16;
 }
 
+// split-K epilogue: y = sum over splits of the fp32 partials, in split order
+__global__ void __launch_bounds__(256) gemm_splitk_reduce_kernel(const float* __restrict__ part, int splits,
+                                                                 int64_t n_out, void* __restrict__ y, int y_dtype) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n_out; o += stride) {
+    float acc = 0.f;
+    for (int k = 0; k < splits; ++k) acc += part[(int64_t)k * n_out + o];
+    store_from_f32(y, y_dtype, o, acc);
+  }
+}
+
+// K splits for a grid of `tiles` output tiles (one CTA per SM): minimise the waves a
+// split grid needs per unit of work, ceil(tiles * s / SMs) / s, at least 4 stages per
+// split; ties to the smaller split (fewer partials)
+static int gemm_splits(int tiles, int k_total) {
+  const int sms = sm_count();
+  if (tiles >= sms) return 1;
+  int best = 1;
+  double best_t = 1e30;
+  for (int sp = 1; sp <= std::min(16, std::max(1, k_total / 4)); ++sp) {
+    const double t = (double)((tiles * sp + sms - 1) / sms) / sp;
+    if (t < best_t - 1e-9) { best_t = t; best = sp; }
+  }
+  return best;
+}
+
+int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows) {
+  Geom g;
+  if (make_geom(w, &g)) return 0;
+  const int tiles = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
+  const int sp = g.cols % kTileN == 0 && g.rows % kTileK == 0 ? gemm_splits(std::max(tiles, 1), (int)(g.rows / kTileK)) : 1;
+  return sp > 1 ? VQB_WS_COUNTER_BYTES + (int64_t)sp * rows * g.cols * 4 : 0;
+}
+
 static bool gemm_fast_ok(const Geom& g, const VqbTensor* w, int x_dtype, const VqbLaunch* L) {
   if (L && (L->flags & VQB_FLAG_FORCE_GENERIC)) return false;
   if (w->layout != VQB_LAYOUT_GEMV_IL || g.v != 8 || g.sharing != VQB_SHARE_WHOLE) return false;
@@ -414,6 +460,12 @@ static int launch_gemm_t(const CUtensorMap& map, const GemmArgs& a, int grid, cu
   if (attr_err != cudaSuccess) return cuda_error(attr_err, "cudaFuncSetAttribute(gemm_tc_kernel)");
   kern<<<grid, kGemmThreads, smem, st>>>(map, a);
   VQB_LAUNCH_CHECK("gemm_tc_kernel");
+  if (a.splits > 1) {
+    const int64_t n_out = (int64_t)a.rows * a.N;
+    const int blocks = (int)std::min<int64_t>(ceil_div(n_out, 256), (int64_t)sm_count() * 4);
+    VQB_CUDA_CHECK(launch_pdl(gemm_splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st,
+                              static_cast<const float*>(a.part), a.splits, n_out, a.y, a.y_dtype));
+  }
   set_kernel("gemm_tc");
   return VQB_OK;
 }
@@ -470,7 +522,18 @@ extern "C" int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, in
     a.G = (int)g.gpr;
     a.K = g.K;
     a.n_sh = std::min(g.K, kBookEntries);
-    const int grid = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
+    const int tiles = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
+    a.splits = gemm_splits(tiles, (int)(g.rows / kTileK));
+    a.part = nullptr;
+    if (a.splits > 1) {
+      const int64_t need = VQB_WS_COUNTER_BYTES + (int64_t)a.splits * rows * g.cols * 4;
+      if (!d_ws || (int64_t)ws_bytes < need) {
+        a.splits = 1;  // no room for partials: one CTA per tile
+      } else {
+        a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_ws) + VQB_WS_COUNTER_BYTES);
+      }
+    }
+    const int grid = tiles * a.splits;
     const bool bf = w->codebook_dtype == VQB_BF16;
     if (g.bits == 16) return bf ? launch_gemm_out<2, 1, true>(map, a, grid, st) : launch_gemm_out<2, 1, false>(map, a, grid, st);
     if (g.R == 1) return bf ? launch_gemm_out<1, 1, true>(map, a, grid, st) : launch_gemm_out<1, 1, false>(map, a, grid, st);
