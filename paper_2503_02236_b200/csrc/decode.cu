@@ -158,17 +158,39 @@ __device__ __forceinline__ void quantize_subvector(const Geom& g, void* __restri
         best_e = e;
       }
     };
-    if (V == 2 && g.K == 256) {
-      // the CQ case: all eight of this lane's entries are loaded before any distance,
-      // so the warp pays one L2 round trip instead of eight
+    if (V == 2 && g.K == 256 && r == 0) {
+      // the CQ case: all eight of this lane's entries are loaded up front (one L2 round
+      // trip), screened with fp32 distances, and only the entries within the fp32
+      // error band of the minimum are rescored in float64 — the float64 argmin is
+      // always among them (|d32 - d64| <= err and tol >= 2 err), so the code is the
+      // reference's, at a fraction of the float64 work
       uint32_t w[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) w[k] = __ldg(reinterpret_cast<const uint32_t*>(book) + lane + 32 * k);
+      const float r0 = (float)res[0], r1 = (float)res[1];  // fp16 rows: exact in fp32
+      float d32[8], dmin = FLT_MAX, scale = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float c[2] = {__half2float(__ushort_as_half((unsigned short)(w[k] & 0xffff))),
-                            __half2float(__ushort_as_half((unsigned short)(w[k] >> 16)))};
-        consider(lane + 32 * k, c);
+        const float c0 = __half2float(__ushort_as_half((unsigned short)(w[k] & 0xffff)));
+        const float c1 = __half2float(__ushort_as_half((unsigned short)(w[k] >> 16)));
+        const float dot = r0 * c0 + r1 * c1, cn = c0 * c0 + c1 * c1;
+        d32[k] = cn - 2.f * dot;
+        dmin = fminf(dmin, d32[k]);
+        scale = fmaxf(scale, cn + 2.f * fabsf(dot));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+        scale = fmaxf(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+      }
+      const float tol = 1e-5f * (scale + 1e-30f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (d32[k] <= dmin + tol) {
+          const float c[2] = {__half2float(__ushort_as_half((unsigned short)(w[k] & 0xffff))),
+                              __half2float(__ushort_as_half((unsigned short)(w[k] >> 16)))};
+          consider(lane + 32 * k, c);
+        }
       }
     } else {
       for (int e = lane; e < g.K; e += 32) {
@@ -302,6 +324,134 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
   });
 }
 
+// CQ fast path of the front end (v = 2, 256 entries, one level on both caches): one
+// warp per (head, channel group, K|V) keeps that group's 256 entries in registers (8
+// per lane) and walks the batch rows, so a book is read once per step instead of
+// once per row; q is roped by one warp per (batch row, head). Distances are screened
+// in fp32 and only the candidates within the fp32 error band are rescored in float64
+// (the reference's float64 argmin is always among them); a single candidate — the
+// usual case — needs no rescoring at all.
+__global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
+                                                                 __half* __restrict__ q_out, Geom gk,
+                                                                 void* __restrict__ kcodes,
+                                                                 const __half* __restrict__ kbooks, Geom gv,
+                                                                 void* __restrict__ vcodes,
+                                                                 const __half* __restrict__ vbooks, int B, int H,
+                                                                 int C, const int* __restrict__ d_len,
+                                                                 float log2_theta) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int G = C / 2;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int pos = __ldg(d_len) - 1;
+  const int n_book_warps = 2 * H * G;
+  if (w >= n_book_warps) {  // q rope
+    const int64_t qi = w - n_book_warps;
+    if (qi >= (int64_t)B * H) return;
+    const int h = (int)(qi % H), b = (int)(qi / H);
+    const __half* q = qkv + (int64_t)b * 3 * H * C + (int64_t)h * C;
+    __half* dst = q_out + ((int64_t)b * H + h) * C;
+    for (int c = lane; c < C; c += 32) dst[c] = __float2half_rn(rope_channel(q, c, C, log2_theta, pos));
+    return;
+  }
+  const bool is_k = w < H * G;
+  const int hg = (int)(is_k ? w : w - H * G);
+  const int h = hg / G, gi = hg % G;
+  const Geom& g = is_k ? gk : gv;
+  const __half* book = (is_k ? kbooks : vbooks) + (int64_t)(h * G + gi) * 256 * 2;  // region = h*G + gi
+  uint32_t wv[8];
+  float c0[8], c1[8];
+  float cmax2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    wv[k] = __ldg(reinterpret_cast<const uint32_t*>(book) + lane + 32 * k);
+    c0[k] = __half2float(__ushort_as_half((unsigned short)(wv[k] & 0xffff)));
+    c1[k] = __half2float(__ushort_as_half((unsigned short)(wv[k] >> 16)));
+    cmax2 = fmaxf(cmax2, c0[k] * c0[k] + c1[k] * c1[k]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cmax2 = fmaxf(cmax2, __shfl_xor_sync(0xffffffffu, cmax2, o));
+  // rope factors of this group's two channels (k only): position-dependent, row-independent
+  float cs[2] = {1.f, 1.f}, sn[2] = {0.f, 0.f};
+  if (is_k) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = gi * 2 + j, i = c < C / 2 ? c : c - C / 2;
+      sincosf((float)pos * exp2f(-log2_theta * (2.0f * i) / (float)C), &sn[j], &cs[j]);
+    }
+  }
+  for (int b = 0; b < B; ++b) {
+    const __half* row = qkv + (int64_t)b * 3 * H * C + (int64_t)((is_k ? H : 2 * H) + h) * C;
+    float p[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = gi * 2 + j;
+      if (is_k) {
+        const int half = C / 2, i = c < half ? c : c - half;
+        const float x0 = __half2float(row[i]), x1 = __half2float(row[i + half]);
+        // the roped k is an fp16 tensor in the reference step
+        p[j] = __half2float(__float2half_rn(c < half ? x0 * cs[j] - x1 * sn[j] : x1 * cs[j] + x0 * sn[j]));
+      } else {
+        p[j] = __half2float(row[c]);
+      }
+    }
+    float d32[8], dmin = FLT_MAX;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      d32[k] = (c0[k] * c0[k] + c1[k] * c1[k]) - 2.f * (p[0] * c0[k] + p[1] * c1[k]);
+      dmin = fminf(dmin, d32[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    const float pn32 = p[0] * p[0] + p[1] * p[1];
+    const float tol = 1e-5f * (cmax2 + 2.f * sqrtf(pn32 * cmax2)) + 1e-30f;
+    unsigned cand = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cand |= (d32[k] <= dmin + tol) ? (1u << k) : 0u;
+    const unsigned lanes = __ballot_sync(0xffffffffu, cand != 0);
+    int code;
+    if (__popc(lanes) == 1 && __popc(__shfl_sync(0xffffffffu, cand, __ffs(lanes) - 1)) == 1) {
+      const int src = __ffs(lanes) - 1;
+      const unsigned cb = __shfl_sync(0xffffffffu, cand, src);
+      code = src + 32 * (__ffs(cb) - 1);
+    } else {
+      // several candidates: float64 distances in the reference's operation order
+      const double r0 = p[0], r1 = p[1];
+      const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
+      double best = DBL_MAX;
+      int best_e = 0x7fffffff;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (cand & (1u << k)) {
+          const double a0 = c0[k], a1 = c1[k];
+          const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
+          const double cn = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
+          const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
+          if (d < best) {
+            best = d;
+            best_e = lane + 32 * k;
+          }
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+        if (ob < best || (ob == best && oe < best_e)) {
+          best = ob;
+          best_e = oe;
+        }
+      }
+      code = best_e;
+    }
+    if (lane == 0) {
+      const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
+      const int64_t off = (g.layout == VQB_LAYOUT_PLAIN) ? s : il_offset(g, 0, s);
+      reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off] = (uint8_t)code;
+    }
+  }
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -346,6 +496,20 @@ extern "C" int vqb_qkv_rope_append(const void* d_qkv, void* d_q_out, const VqbTe
   if (gk.v != gv.v) return set_error(VQB_ECONFIG, "K and V caches need one vector size");
   if (k_cache->codebook_dtype != VQB_F16 || v_cache->codebook_dtype != VQB_F16)
     return set_error(VQB_ECONFIG, "KV append needs fp16 codebooks");
+  const bool cq = gk.v == 2 && gk.K == 256 && gk.R == 1 && gv.K == 256 && gv.R == 1 && gk.code_bytes == 1 &&
+                  gk.sharing == VQB_SHARE_CHANNEL_GROUP && gv.sharing == VQB_SHARE_CHANNEL_GROUP &&
+                  gk.group_width == 2 && gv.group_width == 2;
+  if (cq) {
+    const int64_t warps = (int64_t)2 * H * (C / 2) + (int64_t)B * H;
+    VQB_CUDA_CHECK(launch_pdl(qkv_rope_append_cq_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0,
+                              reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<const __half*>(d_qkv),
+                              reinterpret_cast<__half*>(d_q_out), gk, const_cast<void*>(k_cache->d_codes),
+                              reinterpret_cast<const __half*>(k_cache->d_codebooks), gv,
+                              const_cast<void*>(v_cache->d_codes),
+                              reinterpret_cast<const __half*>(v_cache->d_codebooks), B, H, C, d_len, log2f(theta)));
+    set_kernel("qkv_rope_append");
+    return VQB_OK;
+  }
   const int64_t warps = (int64_t)B * H * (2 * (C / gk.v) + 1);
   VQB_CUDA_CHECK(launch_pdl(qkv_rope_append_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0,
                             reinterpret_cast<cudaStream_t>(stream),

@@ -14,6 +14,7 @@ itself, so one CUDA graph replays every decode step while the cache grows.
 Batches of 1-8 rows take the CUDA-core GEMV, larger batches the tcgen05 GEMM.
 """
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -109,7 +110,13 @@ class VQLlamaDecoder:
     def step(self) -> torch.Tensor:
         """One decode step for the current tokens; returns (and stores) the next ones.
         Device-side only (capturable): the length counter advances first, so every
-        kernel of the step sees the new token's position as d_len - 1."""
+        kernel of the step sees the new token's position as d_len - 1.
+
+        VQB_DECODE_SKIP (comma list of norm, linear, front, attn, silu) drops stages
+        for time attribution only — the output is then meaningless."""
+        skip = set(filter(None, os.environ.get("VQB_DECODE_SKIP", "").split(",")))
+        if skip:
+            return self._step_ablated(skip)
         sh, b = self.shape, self.batch
         ops.add_len(self.d_len, 1)
         self.res.copy_(torch.index_select(self.embed, 0, self.tokens))
@@ -124,6 +131,40 @@ class VQLlamaDecoder:
             xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)
             gu = self._linear(L.gate_up, xn)
             x = self._linear(L.down, ops.silu_mul(gu))
+        xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
+        self.logits = xn @ self.lm_head
+        self.tokens.copy_(torch.argmax(self.logits, dim=-1))
+        return self.tokens
+
+    def _step_ablated(self, skip):
+        sh, b = self.shape, self.batch
+        ops.add_len(self.d_len, 1)
+        self.res.copy_(torch.index_select(self.embed, 0, self.tokens))
+        hc = sh.heads * sh.head_dim
+        xn = torch.zeros((b, sh.hidden), dtype=torch.float16, device=self.device)
+        qkv = torch.zeros((b, 3 * hc), dtype=torch.float16, device=self.device)
+        q = torch.zeros((b, sh.heads, sh.head_dim), dtype=torch.float16, device=self.device)
+        a = torch.zeros((b, sh.heads, sh.head_dim), dtype=torch.float16, device=self.device)
+        gu = torch.zeros((b, 2 * sh.ffn), dtype=torch.float16, device=self.device)
+        hm = torch.zeros((b, sh.ffn), dtype=torch.float16, device=self.device)
+        x = None
+        for L in self.layers:
+            if "norm" not in skip:
+                xn = ops.rmsnorm(x, self.res, L.attn_norm, sh.eps)
+            if "linear" not in skip:
+                qkv = self._linear(L.qkv, xn)
+            if "front" not in skip:
+                q = ops.qkv_rope_append(qkv, L.k_cache, L.v_cache, self.d_len, sh.rope_theta)
+            if "attn" not in skip:
+                a = ops.vq_attention(L.k_cache, L.v_cache, q, out_dtype=torch.float16, d_len=self.d_len)
+            o = self._linear(L.o, a.view(b, hc)) if "linear" not in skip else xn
+            if "norm" not in skip:
+                xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)
+            if "linear" not in skip:
+                gu = self._linear(L.gate_up, xn)
+            if "silu" not in skip:
+                hm = ops.silu_mul(gu)
+            x = self._linear(L.down, hm) if "linear" not in skip else xn
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
         self.tokens.copy_(torch.argmax(self.logits, dim=-1))
