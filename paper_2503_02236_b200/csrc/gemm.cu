@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           const uint64_t bdesc = umma_desc(b_base + k * 4096, 1024, 2048);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (h == 1 && row0 + 128 >= a.rows) break;  // the second 128-row half is all padding
             // A: K-major SW128 rows of 128 B; SBO = 8-row-group stride (1 KB); K step = 32 B
             const uint64_t adesc = umma_desc(a_base + h * 16384 + k * 32, 16, 1024);
             umma_f16(tmem_base + h * kTileN, adesc, bdesc, idesc, (it | k) != 0);
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     const int cc0 = ((warp - 2) / 4) * CPW;                  // warps sharing a quarter split the columns
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      if (h == 1 && row0 + 128 >= a.rows) break;  // never computed: padding rows only
       const int row = row0 + h * 128 + quarter * 32 + lane;
 #pragma unroll
       for (int c2 = 0; c2 < CPW; ++c2) {
