@@ -24,6 +24,12 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const __half* __restri
                                                           const __half* __restrict__ w, __half* __restrict__ out,
                                                           int dim, float eps) {
   pdl_launch_dependents();
+  // the weight does not depend on the previous kernel: fetch it before waiting
+  constexpr int PER = 8;  // halves per 16-byte vector
+  const int nvec = dim / PER;
+  uint4 wv[4], hv[4];
+  int nv = 0;
+  for (int i = threadIdx.x; i < nvec && nv < 4; i += THREADS, ++nv) wv[nv] = __ldg(reinterpret_cast<const uint4*>(w) + i);
   pdl_wait();
   const int row = blockIdx.x;
   const __half* xr = x ? x + (int64_t)row * dim : nullptr;
@@ -31,16 +37,28 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const __half* __restri
   __half* orow = out + (int64_t)row * dim;
   __shared__ float red[THREADS / 32];
   float ss = 0.f;
-  for (int i = threadIdx.x * 2; i < dim; i += THREADS * 2) {
-    float2 h = __half22float2(*reinterpret_cast<const __half2*>(rr + i));
+  nv = 0;
+  for (int i = threadIdx.x; i < nvec && nv < 4; i += THREADS, ++nv) {
+    uint4 h = reinterpret_cast<const uint4*>(rr)[i];
     if (xr) {
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(xr + i));
       // the residual stream is fp16: round the sum like the fp16 reference add
-      const __half2 hs = __floats2half2_rn(h.x + a.x, h.y + a.y);
-      *reinterpret_cast<__half2*>(rr + i) = hs;
-      h = __half22float2(hs);
+      const uint4 a = reinterpret_cast<const uint4*>(xr)[i];
+      __half2* hp = reinterpret_cast<__half2*>(&h);
+      const __half2* ap = reinterpret_cast<const __half2*>(&a);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(hp[j]), g = __half22float2(ap[j]);
+        hp[j] = __floats2half2_rn(f.x + g.x, f.y + g.y);
+      }
+      reinterpret_cast<uint4*>(rr)[i] = h;
     }
-    ss += h.x * h.x + h.y * h.y;
+    hv[nv] = h;
+    const __half2* hp = reinterpret_cast<const __half2*>(&h);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(hp[j]);
+      ss += f.x * f.x + f.y * f.y;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -54,13 +72,20 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_kernel(const __half* __restri
   }
   __syncthreads();
   const float inv = rsqrtf(red[0] / (float)dim + eps);
-  for (int i = threadIdx.x * 2; i < dim; i += THREADS * 2) {
-    const float2 h = __half22float2(*reinterpret_cast<const __half2*>(rr + i));
-    const float2 ww = __half22float2(*reinterpret_cast<const __half2*>(w + i));
-    // HF: weight * (h * inv).to(fp16)
-    const __half2 hn = __floats2half2_rn(h.x * inv, h.y * inv);
-    const float2 hf = __half22float2(hn);
-    *reinterpret_cast<__half2*>(orow + i) = __floats2half2_rn(ww.x * hf.x, ww.y * hf.y);
+  nv = 0;
+  for (int i = threadIdx.x; i < nvec && nv < 4; i += THREADS, ++nv) {
+    const __half2* hp = reinterpret_cast<const __half2*>(&hv[nv]);
+    const __half2* wp = reinterpret_cast<const __half2*>(&wv[nv]);
+    uint4 o;
+    __half2* op = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(hp[j]), ww = __half22float2(wp[j]);
+      // HF: weight * (h * inv).to(fp16)
+      const float2 hf = __half22float2(__floats2half2_rn(f.x * inv, f.y * inv));
+      op[j] = __floats2half2_rn(ww.x * hf.x, ww.y * hf.y);
+    }
+    reinterpret_cast<uint4*>(orow)[i] = o;
   }
 }
 
@@ -458,8 +483,9 @@ using namespace vqb;
 
 extern "C" int vqb_rmsnorm(const void* d_x, void* d_residual, const void* d_weight, void* d_out, int32_t rows,
                            int32_t dim, float eps, void* stream) {
-  if (rows < 1 || dim < 2 || (dim & 1)) return set_error(VQB_ESHAPE, "rmsnorm needs rows >= 1 and an even dim");
-  VQB_CUDA_CHECK(launch_pdl(rmsnorm_kernel<256>, dim3(rows), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+  if (rows < 1 || dim < 8 || (dim % 8) || dim > 8 * 4 * 512)
+    return set_error(VQB_ESHAPE, "rmsnorm needs rows >= 1 and dim a multiple of 8 up to 16384");
+  VQB_CUDA_CHECK(launch_pdl(rmsnorm_kernel<512>, dim3(rows), dim3(512), 0, reinterpret_cast<cudaStream_t>(stream),
                             reinterpret_cast<const __half*>(d_x), reinterpret_cast<__half*>(d_residual),
                             reinterpret_cast<const __half*>(d_weight), reinterpret_cast<__half*>(d_out), dim, eps));
   VQB_LAUNCH_CHECK("rmsnorm_kernel");
