@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider -k "decode or rmsnorm" > gpurun_out/pytest_gpu.txt 2>&1; tail -2 gpurun_out/pytest_gpu.txt
-timeout 900 python tools/decode_bench.py 1 16 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; tail -20 gpurun_out/pytest_gpu.txt
+timeout 300 python bench.py --steps 10 --warmup 3 --no-extra --no-cpu 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['clocks'])"
