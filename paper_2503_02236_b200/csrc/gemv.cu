@@ -50,7 +50,7 @@ namespace vqb {
 __host__ __device__ constexpr int gemv_warps(int B) { return B >= 8 ? 8 : 16; }
 // rows a warp handles per chunk: 16 (one 16-byte code word of u8 codes, two of u16) —
 // 8-row slabs double the per-chunk overhead and measured slower
-__host__ __device__ constexpr int gemv_slab_rows(int cbytes) { return 16; }
+__host__ __device__ constexpr int gemv_slab_rows(int cbytes) { return 32; }
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
 // chunk rows: the warps along M each take one 16-row slab (WG = warps across N)
 __host__ __device__ constexpr int gemv_chunk_rows(int WG, int B, int cbytes) {

@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; tail -20 gpurun_out/pytest_gpu.txt
-timeout 300 python bench.py --steps 10 --warmup 3 --no-extra --no-cpu 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['clocks'])"
+timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "gemv or full" > gpurun_out/pytest_gpu.txt 2>&1; tail -1 gpurun_out/pytest_gpu.txt
+timeout 300 python tools/gemv_sweep.py --cfg quip2 --shapes 4096x4096,4096x12288,4096x22016,11008x4096 2>&1 | tail -4
+timeout 300 python tools/gemv_sweep.py --cfg aqlm2x8 --shapes 8192x8192 2>&1 | tail -1
+timeout 300 python tools/gemv_sweep.py --cfg gptvq2 --shapes 4096x4096 2>&1 | tail -1
