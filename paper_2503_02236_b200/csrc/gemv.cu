@@ -48,8 +48,9 @@ namespace vqb {
 // looked-up entry feeds B FMAs, so fewer warps with more registers do (16 at B=4,
 // 8 at B=8, which keeps the B x V fp32 accumulators in registers).
 __host__ __device__ constexpr int gemv_warps(int B) { return B >= 8 ? 8 : 16; }
-// rows a warp handles per chunk: 16 (one 16-byte code word of u8 codes, two of u16) —
-// 8-row slabs double the per-chunk overhead and measured slower
+// rows a warp handles per chunk: 32 (two 16-byte code words of u8 codes, four of u16).
+// Measured: 8-row slabs double the per-chunk overhead; 16-row slabs leave half the
+// code words in flight; 64-row slabs no longer fit the ring with the codebook.
 __host__ __device__ constexpr int gemv_slab_rows(int cbytes) { return 32; }
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
 // chunk rows: the warps along M each take one 16-row slab (WG = warps across N)
