@@ -25,9 +25,10 @@
 //  * online softmax (flash-decode) in the exp2 domain; V is dequantised in
 //    registers and fused into fp32 accumulators with fma.rn.f32.f16.
 //  * the next 32-token batch's codes are loaded while the current one computes.
-//  * split-T partials (m, l, acc) per contiguous span are merged by the last
-//    arriving CTA in fixed T order (deterministic), like the reference's split
-//    reduction (sim.py:604-620).
+//  * split-T partials (m, l, acc) of a (b, h) cut across CTAs travel as tagged
+//    64-bit words (no fence, no counter) to the CTA holding its first chunk, which
+//    merges them in T order (deterministic), like the reference's split reduction
+//    (sim.py:604-620).
 // Generic path: dequantise K and V to fp32 (vqb_dequant) and run a plain fp32
 // decode attention; covers every other configuration.
 #include <cfloat>
@@ -41,6 +42,7 @@ int launch_dequant(const Geom& g, const VqbTensor* t, void* out, int out_dtype, 
 constexpr int kAttnWarps = 12;  // 12 x 32 threads leave 168 registers for the double-buffered code stream
 constexpr int kAttnThreads = kAttnWarps * 32;
 constexpr int kAttnChunk = 512;  // tokens per work unit
+constexpr int64_t kAttnSlotOffset = 65536;  // tagged span slots in the self-resetting workspace head
 
 struct AttnArgs {
   const uint8_t* kc;
@@ -53,13 +55,32 @@ struct AttnArgs {
   int q_dtype;
   void* out;
   int out_dtype;
-  float* part;   // (B*H, NT, C + 3)
-  int* counters; // B*H
+  unsigned long long* slots;  // (grid, C + 2) tagged {m, l, acc} of a CTA's leading partial span; zero between launches
   int B, H, T, NT;       // valid tokens and 512-token chunks (when len_ptr is null)
   int T_cap, NT_cap;      // cache capacity (layout stride) and its chunk count
   const int* len_ptr;     // optional device-resident valid length (decode loops in CUDA graphs)
   float scale_log2;
   unsigned long long* trace;  // debug (VqbLaunch.flags & 32): per-CTA phase timestamps, 8 per CTA
+};
+
+// per-CTA phase sums: slot 2 prologue (books + LUT), 3 streaming, 4 merge, 6 spans
+struct AttnPhase {
+  unsigned long long t = 0, sum[3] = {0, 0, 0};
+  int spans = 0;
+  __device__ __forceinline__ void mark(const AttnArgs& a, int phase) {
+    if (a.trace && threadIdx.x == 0) {
+      const unsigned long long n = gtimer();
+      if (phase >= 0) sum[phase] += n - t;
+      else ++spans;
+      t = n;
+    }
+  }
+  __device__ __forceinline__ void flush(const AttnArgs& a) {
+    if (a.trace && threadIdx.x == 0) {
+      for (int i = 0; i < 3; ++i) a.trace[blockIdx.x * 8 + 2 + i] = sum[i];
+      a.trace[blockIdx.x * 8 + 6] = spans;
+    }
+  }
 };
 
 __device__ __forceinline__ void attn_trace(const AttnArgs& a, int slot) {
@@ -260,7 +281,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   uint8_t* vbook_s = smem + lut_off + SM::region;
   float* lut_s = reinterpret_cast<float*>(smem + lut_off);
   float* scratch = reinterpret_cast<float*>(smem + scratch_off);
-  int* s_last = reinterpret_cast<int*>(smem + scratch_off + SM::scratch_bytes - 16);
   // mbarrier for the bulk-copied books (8-byte aligned slot at the end of the scratch)
   const uint32_t book_bar = smem_u32(smem + ((scratch_off + SM::scratch_bytes - 8) & ~7u));
   const bool bulk_books = (V == 2) && a.kbt != nullptr && a.vbt != nullptr;
@@ -287,7 +307,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
 
   int cur_h = -1;
+  AttnPhase ph;
   for (int u = u0; u < u1;) {
+    ph.mark(a, -1);
     const int h = u / BNT;
     const int b = (u / NT) % a.B;
     const int tc0 = u % NT;
@@ -386,7 +408,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     }
     __syncthreads();
     }
-    attn_trace(a, 2);
+    ph.mark(a, 0);
     float m_w = -INFINITY, l_lane = 0.f;
     float acc[GPL][V];
 #pragma unroll
@@ -398,7 +420,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     if (aligned) attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
     else attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
 
-    attn_trace(a, 3);
+    ph.mark(a, 1);
     // ---- merge the warps of this span
     float l_w = l_lane;
 #pragma unroll
@@ -414,25 +436,31 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       for (int i = 0; i < V; ++i) my[2 + (lane + 32 * j) * V + i] = acc[j][i];
     __syncthreads();
     const bool whole = (tc0 == 0 && tc1 == NT);
-    float* rec = a.part + ((int64_t)bh * a.NT_cap + tc0) * (C + 3);
+    // A (b, h) split across CTAs is finished by the CTA holding its chunk 0 (for that
+    // CTA it is the last span of its range); the later parts are the first spans of
+    // the following CTAs, which publish {m, l, acc} as tagged 64-bit words in their
+    // own slot — no fence, no counter, no extra launch (the GEMV's scheme).
+    const bool finisher = (tc0 == 0 && !whole);
+    unsigned long long* slots = a.slots;
+    float M = -INFINITY, val = 0.f;
     if (tid <= C) {
-      float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, scratch[w * (C + 2)]);
-      float val = 0.f;
       for (int w = 0; w < kAttnWarps; ++w) {
         const float mw = scratch[w * (C + 2)];
         const float sc = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
         val += sc * (tid < C ? scratch[w * (C + 2) + 2 + tid] : scratch[w * (C + 2) + 1]);
       }
-      if (whole) {
-        scratch[kAttnWarps * (C + 2) + tid] = val;  // the span is the whole (b, h): no partials
-      } else if (tid < C) {
-        rec[3 + tid] = val;
+      if (whole || finisher) {
+        scratch[kAttnWarps * (C + 2) + tid] = val;
       } else {
-        rec[0] = M;
-        rec[1] = val;
-        rec[2] = (float)(tc1 - tc0);
+        unsigned long long* my_slot = slots + (int64_t)blockIdx.x * (C + 2);
+        if (tid < C) {
+          st_relaxed_u64(my_slot + 2 + tid, tag_partial(val));
+        } else {
+          st_relaxed_u64(my_slot, tag_partial(M));
+          st_relaxed_u64(my_slot + 1, tag_partial(val));
+        }
       }
     }
     __syncthreads();
@@ -441,78 +469,59 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
         const float L = scratch[kAttnWarps * (C + 2) + C];
         store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, scratch[kAttnWarps * (C + 2) + tid] / L);
       }
-    } else {
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) *s_last = (atomicAdd(a.counters + bh, tc1 - tc0) + (tc1 - tc0) == NT);
-      __syncthreads();
-      if (*s_last) {
-        __threadfence();
-        if (tid < C) {
-          const float* base = a.part + (int64_t)bh * a.NT_cap * (C + 3);
-          // The spans of this (b, h) start where CTA ranges start (u0(k) = k*U/grid), so
-          // every record is addressed up front and loaded in parallel (a dependent
-          // walk over the span lengths costs one L2 round trip per span).
-          const int base_u = (h * a.B + b) * NT;
-          auto u0_of = [&](int k) { return (int)((int64_t)k * U / gridDim.x); };
-          int kf = (int)((int64_t)base_u * gridDim.x / U);
-          while (kf > 0 && u0_of(kf) > base_u) --kf;
-          while (kf + 1 < (int)gridDim.x && u0_of(kf + 1) <= base_u) ++kf;
-          constexpr int MAXS = 16;
-          float mi[MAXS], li[MAXS], ai[MAXS];
-          int n_sp = 0;
+    } else if (finisher) {
+      // the CTAs after this one whose ranges start inside (b, h)
+      const int bh_end = u - tc0 + NT;  // first unit past this (b, h)
+      int k_end = blockIdx.x + 1;
+      while (k_end < (int)gridDim.x && (int)((int64_t)k_end * U / gridDim.x) < bh_end) ++k_end;
+      const int n_later = k_end - blockIdx.x - 1;
+      if (tid < C) {
+        float Mr = M, L = scratch[kAttnWarps * (C + 2) + C], A = scratch[kAttnWarps * (C + 2) + tid];
+        constexpr int PF = 4;  // slots in flight
+        for (int j0 = 0; j0 < n_later; j0 += PF) {
+          unsigned long long wm[PF], wl[PF], wa[PF];
 #pragma unroll
-          for (int i = 0; i < MAXS; ++i) {
-            const int st = (i == 0) ? base_u : ((kf + i < (int)gridDim.x) ? u0_of(kf + i) : base_u + NT);
-            const bool ok = (i == 0) || (st < base_u + NT);
-            mi[i] = -INFINITY;
-            li[i] = 0.f;
-            ai[i] = 0.f;
-            if (ok) {
-              const float* r = base + (int64_t)(st - base_u) * (C + 3);
-              mi[i] = __ldcg(r);
-              li[i] = __ldcg(r + 1);
-              ai[i] = __ldcg(r + 3 + tid);
-              n_sp = i + 1;
+          for (int j = 0; j < PF; ++j) {
+            const unsigned long long* sp = slots + (int64_t)(blockIdx.x + 1 + j0 + j) * (C + 2);
+            wm[j] = wl[j] = wa[j] = 1ull << 32;
+            if (j0 + j < n_later) {
+              wm[j] = ld_relaxed_u64(sp);
+              wl[j] = ld_relaxed_u64(sp + 1);
+              wa[j] = ld_relaxed_u64(sp + 2 + tid);
             }
           }
-          float MM = -INFINITY, L = 0.f, A = 0.f;
-          const bool fits = (kf + MAXS >= (int)gridDim.x) || (u0_of(kf + MAXS) >= base_u + NT);
-          if (fits) {
 #pragma unroll
-            for (int i = 0; i < MAXS; ++i)
-              if (i < n_sp) MM = fmaxf(MM, mi[i]);
-#pragma unroll
-            for (int i = 0; i < MAXS; ++i)
-              if (i < n_sp) {
-                const float sc = (mi[i] == -INFINITY) ? 0.f : fast_exp2(mi[i] - MM);
-                L += sc * li[i];
-                A += sc * ai[i];
-              }
-          } else {  // more spans than MAXS: walk the records
-            for (int tc = 0; tc < NT;) {
-              const float* r = base + (int64_t)tc * (C + 3);
-              MM = fmaxf(MM, __ldcg(r));
-              tc += (int)__ldcg(r + 2);
-            }
-            for (int tc = 0; tc < NT;) {
-              const float* r = base + (int64_t)tc * (C + 3);
-              const float m = __ldcg(r);
-              const float sc = (m == -INFINITY) ? 0.f : fast_exp2(m - MM);
-              L += sc * __ldcg(r + 1);
-              A += sc * __ldcg(r + 3 + tid);
-              tc += (int)__ldcg(r + 2);
+          for (int j = 0; j < PF; ++j) {
+            if (j0 + j < n_later) {
+              unsigned long long* sp = slots + (int64_t)(blockIdx.x + 1 + j0 + j) * (C + 2);
+              while ((wm[j] >> 32) == 0) wm[j] = ld_relaxed_u64(sp);
+              while ((wl[j] >> 32) == 0) wl[j] = ld_relaxed_u64(sp + 1);
+              while ((wa[j] >> 32) == 0) wa[j] = ld_relaxed_u64(sp + 2 + tid);
+              const float mj = __uint_as_float((uint32_t)wm[j]);
+              const float Mn = fmaxf(Mr, mj);
+              const float s0 = fast_exp2(Mr - Mn);
+              const float s1 = (mj == -INFINITY) ? 0.f : fast_exp2(mj - Mn);
+              L = L * s0 + __uint_as_float((uint32_t)wl[j]) * s1;
+              A = A * s0 + __uint_as_float((uint32_t)wa[j]) * s1;
+              Mr = Mn;
+              st_relaxed_u64(sp + 2 + tid, 0ull);  // slots reset for the next launch
             }
           }
-          store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, A / L);
         }
-        if (tid == 0) a.counters[bh] = 0;
+        store_from_f32(a.out, a.out_dtype, (int64_t)bh * C + tid, A / L);
+      }
+      __syncthreads();  // every thread has read m and l
+      for (int j = tid; j < n_later; j += kAttnThreads) {
+        unsigned long long* sp = slots + (int64_t)(blockIdx.x + 1 + j) * (C + 2);
+        st_relaxed_u64(sp, 0ull);
+        st_relaxed_u64(sp + 1, 0ull);
       }
     }
-    attn_trace(a, 4);
+    ph.mark(a, 2);
     u = span_end;
   }
   attn_trace(a, 5);
+  ph.flush(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -590,7 +599,8 @@ int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH) {
   if (s) return s;
   const int64_t T = g.dims[2], C = g.cols;
   const int64_t NT = ceil_div(T, kAttnChunk);
-  const int64_t fast = VQB_WS_COUNTER_BYTES + BH * NT * (C + 3) * 4;
+  (void)NT;
+  const int64_t fast = VQB_WS_COUNTER_BYTES;
   const int64_t generic = VQB_WS_COUNTER_BYTES + a256(2 * BH * T * C * 4) + BH * T * 4;
   return std::max(fast, generic);
 }
@@ -635,7 +645,8 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
   const int64_t need = attn_ws_bytes(k, BH);
   if ((int64_t)ws_bytes < need || !ws)
     return set_error(VQB_ECAPACITY, "attention workspace too small: %zu < %lld", ws_bytes, (long long)need);
-  const bool fast = attn_fast_ok(gk, gv, k, v, T_cap, L) && BH * 4 <= VQB_WS_COUNTER_BYTES;
+  const bool fast = attn_fast_ok(gk, gv, k, v, T_cap, L) &&
+                    kAttnSlotOffset + (int64_t)sm_count() * (C + 2) * 8 <= VQB_WS_COUNTER_BYTES;
   if (used_fast) *used_fast = fast;
   if (!fast && d_len)
     return set_error(VQB_ECONFIG, "a device-resident KV length needs the fast attention configuration");
@@ -651,8 +662,7 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.q_dtype = q_dtype;
     a.out = out;
     a.out_dtype = out_dtype;
-    a.counters = reinterpret_cast<int*>(ws);
-    a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);
+    a.slots = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + kAttnSlotOffset);
     a.B = B;
     a.H = H;
     a.T = T;

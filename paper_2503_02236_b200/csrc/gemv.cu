@@ -88,29 +88,9 @@ struct GemvFastArgs {
   unsigned long long* trace;  // optional per-CTA phase timestamps (debug flag 32), 8 per CTA
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
   if (tr) tr[blockIdx.x * 8 + slot] = gtimer();
 }
-// A partial travels as one 64-bit word {fp32 value, tag}: an aligned 8-byte store
-// is single-copy atomic, so a reader that sees the tag also sees the value — no
-// fence or flag round trip between producer and consumer.
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long tag_partial(float v) {
-  return (1ull << 32) | (unsigned long long)__float_as_uint(v);
-}
-
 // Persistent stream-K decode GEMV. Work units are (column block, chunk of CR rows),
 // ordered column-block major; CTA i owns the contiguous unit range
 // [i*U/grid, (i+1)*U/grid) and walks it as "spans" (maximal runs inside one column

@@ -29,8 +29,9 @@ def main(B=1, H=32, T=4096, C=128, v=2):
     t0 = int(tr[:, 0].min())
     rel = (tr[:, :6] - t0).double() / 1e3
     q_ = lambda c: [round(float(rel[:, c].quantile(p)), 2) for p in (0.0, 0.5, 1.0)]
-    print(json.dumps({"B": B, "T": T, "start": q_(0), "pdl_ok": q_(1), "lut_ready": q_(2), "streamed": q_(3),
-                      "merged": q_(4), "end": q_(5)}))
+    sm = lambda c: [round(float((tr[:, c].double() / 1e3).quantile(p)), 2) for p in (0.0, 0.5, 1.0)]
+    print(json.dumps({"B": B, "T": T, "start": q_(0), "pdl_ok": q_(1), "end": q_(5),
+                      "sum_prologue": sm(2), "sum_stream": sm(3), "sum_merge": sm(4), "spans": [int(tr[:, 6].min()), int(tr[:, 6].max())]}))
 
 
 if __name__ == "__main__":
