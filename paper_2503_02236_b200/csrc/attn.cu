@@ -307,6 +307,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
 
   int cur_h = -1;
+  bool books_inflight = false;
+  auto issue_books = [&](int hh, bool with_v) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bytes = 256u * G * EPB;
+    mbar_arrive_expect_tx(book_bar, with_v ? 2 * bytes : bytes);
+    tma_load_1d(smem_u32(lut_s), a.kbt + (int64_t)hh * 256 * G * V, bytes, book_bar);
+    if (with_v) tma_load_1d(smem_u32(vbook_s), a.vbt + (int64_t)hh * 256 * G * V, bytes, book_bar);
+  };
   AttnPhase ph;
   for (int u = u0; u < u1;) {
     ph.mark(a, -1);
@@ -334,14 +342,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     if (bulk_books) {
       // ---- books by bulk copy: the head's K book lands in the LUT region and its V
       // book in the V-book region, both already [e][g]; the LUT is then computed in
-      // place (an fp16 pair and its fp32 logit term occupy the same 4 bytes)
-      __syncthreads();  // previous span finished with books / LUT / scratch
-      if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t bytes = 256u * G * EPB;
-        mbar_arrive_expect_tx(book_bar, switch_h ? 2 * bytes : bytes);
-        tma_load_1d(smem_u32(lut_s), a.kbt + (int64_t)h * 256 * G * V, bytes, book_bar);
-        if (switch_h) tma_load_1d(smem_u32(vbook_s), a.vbt + (int64_t)h * 256 * G * V, bytes, book_bar);
+      // place (an fp16 pair and its fp32 logit term occupy the same 4 bytes). After
+      // the first span the copies were issued at the end of the previous span.
+      if (!books_inflight) {
+        __syncthreads();  // previous span finished with books / LUT / scratch
+        if (tid == 0) issue_books(h, switch_h);
       }
       cur_h = h;
       mbar_wait(book_bar, book_phase);
@@ -435,6 +440,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
 #pragma unroll
       for (int i = 0; i < V; ++i) my[2 + (lane + 32 * j) * V + i] = acc[j][i];
     __syncthreads();
+    // every warp is done with the LUT and the V book: fetch the next span's books now,
+    // so the copy overlaps this span's merge
+    books_inflight = bulk_books && span_end < u1;
+    if (books_inflight && tid == 0) issue_books(span_end / BNT, span_end / BNT != h);
     const bool whole = (tc0 == 0 && tc1 == NT);
     // A (b, h) split across CTAs is finished by the CTA holding its chunk 0 (for that
     // CTA it is the last span of its range); the later parts are the first spans of

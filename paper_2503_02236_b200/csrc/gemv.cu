@@ -43,10 +43,11 @@
 
 namespace vqb {
 
-// Every warp computes; thread 0 also feeds the TMA ring. 32 warps (one 1024-thread
-// CTA per SM) hide the shared-memory gather latency at batch 1-2; at larger batch each
-// looked-up entry feeds B FMAs, so fewer warps with more registers do (16 at B=4,
-// 8 at B=8, which keeps the B x V fp32 accumulators in registers).
+// Every warp computes; thread 0 also feeds the TMA ring. 16 warps (one 512-thread
+// CTA per SM) hide the shared-memory gather latency at batch 1-4; at batch 8 each
+// looked-up entry feeds 8 FMAs, so 8 warps with more registers keep the B x V fp32
+// accumulators in registers. Measured: 8 warps at batch 1 with two CTAs per SM (so
+// the next launch's prologue could overlap this one's tail) is 6 % slower.
 __host__ __device__ constexpr int gemv_warps(int B) { return B >= 8 ? 8 : 16; }
 // rows a warp handles per chunk: 32 (two 16-byte code words of u8 codes, four of u16).
 // Measured: 8-row slabs double the per-chunk overhead; 16-row slabs leave half the
