@@ -24,7 +24,8 @@
 //    shuffle+add pairs with no selects, leaving lane l with token l's logit.
 //  * online softmax (flash-decode) in the exp2 domain; V is dequantised in
 //    registers and fused into fp32 accumulators with fma.rn.f32.f16.
-//  * the next 32-token batch's codes are loaded while the current one computes.
+//  * the next 32-token batch's K codes load during the V phase, its V codes during
+//    the next K phase (one register set, 16 warps), with L2 bulk prefetch ahead.
 //  * split-T partials (m, l, acc) of a (b, h) cut across CTAs travel as tagged
 //    64-bit words (no fence, no counter) to the CTA holding its first chunk, which
 //    merges them in T order (deterministic), like the reference's split reduction
@@ -39,7 +40,7 @@ namespace vqb {
 
 int launch_dequant(const Geom& g, const VqbTensor* t, void* out, int out_dtype, cudaStream_t st);
 
-constexpr int kAttnWarps = 12;  // 12 x 32 threads leave 168 registers for the double-buffered code stream
+constexpr int kAttnWarps = 16;  // 16 x 32 threads: 128 registers with one code register set per stream
 constexpr int kAttnThreads = kAttnWarps * 32;
 constexpr int kAttnChunk = 512;  // tokens per work unit
 constexpr int64_t kAttnSlotOffset = 65536;  // tagged span slots in the self-resetting workspace head
@@ -166,17 +167,9 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     cbK[j] = (lut_base & 0xffff0000u) | colK[j];
     cbV[j] = (vbook_base & 0xffff0000u) | colV[j];
   }
-  auto load = [&](uint4 (&kc)[Q], uint4 (&vc)[Q], int t0) {
-    const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      kc[q] = ldg_stream(kbase + off + q * 512);
-      vc[q] = ldg_stream(vbase + off + q * 512);
-    }
-  };
   // L2 prefetch of a later batch (one bulk prefetch of each 2*GPL x 512-byte run):
-  // the register double buffer alone keeps too few bytes in flight to cover the HBM
-  // latency, so the batches PF_AHEAD strides ahead are pulled into L2 meanwhile
+  // the register set alone keeps too few bytes in flight to cover the HBM latency,
+  // so the batches PF_AHEAD strides ahead are pulled into L2 meanwhile
   auto prefetch = [&](int t0) {
     if (lane == 0 && t0 < tok1) {
       const int64_t off = (int64_t)(t0 / 32) * 32 * G;
@@ -184,8 +177,10 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vbase + off), "r"(Q * 512) : "memory");
     }
   };
-  auto batch = [&](const uint4 (&kc)[Q], const uint4 (&vc)[Q], int tb) {
-    // K phase: lane partial logits for the 32 slots (slot i = token i ^ lane)
+  // K phase + online-softmax update of one 32-token batch; returns this lane's
+  // token probability (fp16 bits) for the V phase
+  auto kphase = [&](const uint4 (&kc)[Q], int tb) -> uint32_t {
+    // lane partial logits for the 32 slots (slot i = token i ^ lane)
     auto partial = [&](int i) {
       float acc_s = 0.f;
 #pragma unroll
@@ -224,8 +219,10 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     for (int j = 0; j < GPL; ++j)
 #pragma unroll
       for (int c = 0; c < V; ++c) acc[j][c] *= corr;
-    const uint32_t ph = (uint32_t)__half_as_ushort(__float2half_rn(p));
-    // V phase: slot i holds token i ^ lane, whose probability lives on that lane
+    return (uint32_t)__half_as_ushort(__float2half_rn(p));
+  };
+  // V phase: slot i holds token i ^ lane, whose probability lives on that lane
+  auto vphase = [&](const uint4 (&vc)[Q], uint32_t ph) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const uint16_t pk = (uint16_t)__shfl_sync(0xffffffffu, ph, i ^ lane);
@@ -248,24 +245,31 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
       }
     }
   };
-  // warp w takes 32-token batches w, w+kAttnWarps, ... of the span, double-buffered;
-  // the first batch (ka, va) was loaded by the caller before the span prologue
+  auto load_k = [&](uint4 (&kc)[Q], int t0) {
+    const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) kc[q] = ldg_stream(kbase + off + q * 512);
+  };
+  auto load_v = [&](uint4 (&vc)[Q], int t0) {
+    const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) vc[q] = ldg_stream(vbase + off + q * 512);
+  };
+  // warp w takes 32-token batches w, w+kAttnWarps, ... of the span. One register set
+  // per stream: the next batch's K codes load during this batch's V phase and its V
+  // codes during the next K phase (the first batch (ka, va) was loaded by the caller).
   int t0 = tok0 + warp * 32;
   if (t0 >= tok1) return;
   constexpr int STRIDE = kAttnWarps * 32;
-  uint4 kb[Q], vb[Q];
   constexpr int PF_AHEAD = 3;
-  for (int p = 2; p <= PF_AHEAD; ++p) prefetch(t0 + p * STRIDE);
-  for (; t0 < tok1; t0 += 2 * STRIDE) {
-    const bool has_b = t0 + STRIDE < tok1;
-    if (has_b) load(kb, vb, t0 + STRIDE);
+  for (int p = 1; p <= PF_AHEAD; ++p) prefetch(t0 + p * STRIDE);
+  for (; t0 < tok1; t0 += STRIDE) {
+    const int tn = t0 + STRIDE;
     prefetch(t0 + (PF_AHEAD + 1) * STRIDE);
-    batch(ka, va, t0);
-    if (has_b) {
-      if (t0 + 2 * STRIDE < tok1) load(ka, va, t0 + 2 * STRIDE);
-      prefetch(t0 + (PF_AHEAD + 2) * STRIDE);
-      batch(kb, vb, t0 + STRIDE);
-    }
+    const uint32_t ph = kphase(ka, t0);
+    if (tn < tok1) load_k(ka, tn);
+    vphase(va, ph);
+    if (tn < tok1) load_v(va, tn);
   }
 }
 
