@@ -261,7 +261,7 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
   int t0 = tok0 + warp * 32;
   if (t0 >= tok1) return;
   constexpr int STRIDE = kAttnWarps * 32;
-  constexpr int PF_AHEAD = 3;
+  constexpr int PF_AHEAD = 2;
   for (int p = 1; p <= PF_AHEAD; ++p) prefetch(t0 + p * STRIDE);
   for (; t0 < tok1; t0 += STRIDE) {
     const int tn = t0 + STRIDE;
