@@ -12,7 +12,8 @@ from .errors import (CapacityError, CodeRangeError, ConfigError, ForgeError, Ker
                      MappingError, ShapeError)
 
 LIB_NAME = "libvqb.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# VQB_LIB_PATH: load another build of the same ABI (A/B timing of kernel revisions)
+LIB_PATH = os.environ.get("VQB_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 # status codes / enums (vqb.h)
 OK, ESHAPE, ECONFIG, ECODERANGE, ECAPACITY, EMAPPING, ECUDA = 0, -1, -2, -3, -4, -5, -10

@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
 // in fp32 and only the candidates within the fp32 error band are rescored in float64
 // (the reference's float64 argmin is always among them); a single candidate — the
 // usual case — needs no rescoring at all.
-__global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
+__global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
                                                                  __half* __restrict__ q_out, Geom gk,
                                                                  void* __restrict__ kcodes,
                                                                  const __half* __restrict__ kbooks, Geom gv,
@@ -406,73 +406,95 @@ __global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* _
       sincosf((float)pos * exp2f(-log2_theta * (2.0f * i) / (float)C), &sn[j], &cs[j]);
     }
   }
-  for (int b = 0; b < B; ++b) {
-    const __half* row = qkv + (int64_t)b * 3 * H * C + (int64_t)((is_k ? H : 2 * H) + h) * C;
-    float p[2];
+  // rows in groups of RB: the row loads and the warp min-reductions of a group are
+  // independent, so their latencies overlap instead of chaining row after row
+  constexpr int RB = 4;
+  for (int b0 = 0; b0 < B; b0 += RB) {
+    float p0[RB], p1[RB];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c = gi * 2 + j;
-      if (is_k) {
-        const int half = C / 2, i = c < half ? c : c - half;
-        const float x0 = __half2float(row[i]), x1 = __half2float(row[i + half]);
-        // the roped k is an fp16 tensor in the reference step
-        p[j] = __half2float(__float2half_rn(c < half ? x0 * cs[j] - x1 * sn[j] : x1 * cs[j] + x0 * sn[j]));
-      } else {
-        p[j] = __half2float(row[c]);
+    for (int r = 0; r < RB; ++r) {
+      const int b = min(b0 + r, B - 1);
+      const __half* row = qkv + (int64_t)b * 3 * H * C + (int64_t)((is_k ? H : 2 * H) + h) * C;
+      float pj[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = gi * 2 + j;
+        if (is_k) {
+          const int half = C / 2, i = c < half ? c : c - half;
+          const float x0 = __half2float(row[i]), x1 = __half2float(row[i + half]);
+          // the roped k is an fp16 tensor in the reference step
+          pj[j] = __half2float(__float2half_rn(c < half ? x0 * cs[j] - x1 * sn[j] : x1 * cs[j] + x0 * sn[j]));
+        } else {
+          pj[j] = __half2float(row[c]);
+        }
       }
+      p0[r] = pj[0];
+      p1[r] = pj[1];
     }
-    float d32[8], dmin = FLT_MAX;
+    float dmin[RB];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      d32[k] = (c0[k] * c0[k] + c1[k] * c1[k]) - 2.f * (p[0] * c0[k] + p[1] * c1[k]);
-      dmin = fminf(dmin, d32[k]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
-    const float pn32 = p[0] * p[0] + p[1] * p[1];
-    const float tol = 1e-5f * (cmax2 + 2.f * sqrtf(pn32 * cmax2)) + 1e-30f;
-    unsigned cand = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) cand |= (d32[k] <= dmin + tol) ? (1u << k) : 0u;
-    const unsigned lanes = __ballot_sync(0xffffffffu, cand != 0);
-    int code;
-    if (__popc(lanes) == 1 && __popc(__shfl_sync(0xffffffffu, cand, __ffs(lanes) - 1)) == 1) {
-      const int src = __ffs(lanes) - 1;
-      const unsigned cb = __shfl_sync(0xffffffffu, cand, src);
-      code = src + 32 * (__ffs(cb) - 1);
-    } else {
-      // several candidates: float64 distances in the reference's operation order
-      const double r0 = p[0], r1 = p[1];
-      const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
-      double best = DBL_MAX;
-      int best_e = 0x7fffffff;
+    for (int r = 0; r < RB; ++r) {
+      dmin[r] = FLT_MAX;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (cand & (1u << k)) {
-          const double a0 = c0[k], a1 = c1[k];
-          const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
-          const double cn = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
-          const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
-          if (d < best) {
-            best = d;
-            best_e = lane + 32 * k;
+        dmin[r] = fminf(dmin[r], (c0[k] * c0[k] + c1[k] * c1[k]) - 2.f * (p0[r] * c0[k] + p1[r] * c1[k]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) dmin[r] = fminf(dmin[r], __shfl_xor_sync(0xffffffffu, dmin[r], o));
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int b = b0 + r;
+      if (b >= B) break;  // warp-uniform
+      const float pn32 = p0[r] * p0[r] + p1[r] * p1[r];
+      const float tol = 1e-5f * (cmax2 + 2.f * sqrtf(pn32 * cmax2)) + 1e-30f;
+      unsigned cand = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float d = (c0[k] * c0[k] + c1[k] * c1[k]) - 2.f * (p0[r] * c0[k] + p1[r] * c1[k]);
+        cand |= (d <= dmin[r] + tol) ? (1u << k) : 0u;
+      }
+      const unsigned lanes = __ballot_sync(0xffffffffu, cand != 0);
+      int code;
+      if (__popc(lanes) == 1 && __popc(__shfl_sync(0xffffffffu, cand, __ffs(lanes) - 1)) == 1) {
+        const int src = __ffs(lanes) - 1;
+        const unsigned cb = __shfl_sync(0xffffffffu, cand, src);
+        code = src + 32 * (__ffs(cb) - 1);
+      } else {
+        // several candidates: float64 distances in the reference's operation order
+        const double r0 = p0[r], r1 = p1[r];
+        const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
+        double best = DBL_MAX;
+        int best_e = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (cand & (1u << k)) {
+            const double a0 = c0[k], a1 = c1[k];
+            const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
+            const double cn = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
+            const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
+            if (d < best) {
+              best = d;
+              best_e = lane + 32 * k;
+            }
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+          if (ob < best || (ob == best && oe < best_e)) {
+            best = ob;
+            best_e = oe;
           }
         }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
-        if (ob < best || (ob == best && oe < best_e)) {
-          best = ob;
-          best_e = oe;
-        }
+        code = best_e;
       }
-      code = best_e;
-    }
-    if (lane == 0) {
-      const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
-      const int64_t off = (g.layout == VQB_LAYOUT_PLAIN) ? s : il_offset(g, 0, s);
-      reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off] = (uint8_t)code;
+      if (lane == 0) {
+        const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
+        const int64_t off = (g.layout == VQB_LAYOUT_PLAIN) ? s : il_offset(g, 0, s);
+        reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off] = (uint8_t)code;
+      }
     }
   }
 }
