@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
 // in fp32 and only the candidates within the fp32 error band are rescored in float64
 // (the reference's float64 argmin is always among them); a single candidate — the
 // usual case — needs no rescoring at all.
-__global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
+__global__ void __launch_bounds__(256, 2) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
                                                                  __half* __restrict__ q_out, Geom gk,
                                                                  void* __restrict__ kcodes,
                                                                  const __half* __restrict__ kbooks, Geom gv,
@@ -386,14 +386,15 @@ __global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half
   const Geom& g = is_k ? gk : gv;
   const __half* book = (is_k ? kbooks : vbooks) + (int64_t)(h * G + gi) * 256 * 2;  // region = h*G + gi
   uint32_t wv[8];
-  float c0[8], c1[8];
+  float c0[8], c1[8], cn[8];
   float cmax2 = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     wv[k] = __ldg(reinterpret_cast<const uint32_t*>(book) + lane + 32 * k);
     c0[k] = __half2float(__ushort_as_half((unsigned short)(wv[k] & 0xffff)));
     c1[k] = __half2float(__ushort_as_half((unsigned short)(wv[k] >> 16)));
-    cmax2 = fmaxf(cmax2, c0[k] * c0[k] + c1[k] * c1[k]);
+    cn[k] = c0[k] * c0[k] + c1[k] * c1[k];
+    cmax2 = fmaxf(cmax2, cn[k]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cmax2 = fmaxf(cmax2, __shfl_xor_sync(0xffffffffu, cmax2, o));
@@ -406,6 +407,11 @@ __global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half
       sincosf((float)pos * exp2f(-log2_theta * (2.0f * i) / (float)C), &sn[j], &cs[j]);
     }
   }
+  // the code's address is linear in the batch row in both layouts (PLAIN and KV_IL
+  // differ only inside a (b, h) block): one 64-bit index computation per warp
+  const int64_t s00 = ((int64_t)h * g.d_T + pos) * G + gi;
+  const int64_t off0 = (g.layout == VQB_LAYOUT_PLAIN) ? s00 : il_offset(g, 0, s00);
+  const int64_t bstride = (int64_t)H * g.d_T * G;
   // rows in groups of RB: the row loads and the warp min-reductions of a group are
   // independent, so their latencies overlap instead of chaining row after row
   constexpr int RB = 4;
@@ -431,13 +437,15 @@ __global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half
       p0[r] = pj[0];
       p1[r] = pj[1];
     }
-    float dmin[RB];
+    float dmin[RB], d32[RB][8];
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
       dmin[r] = FLT_MAX;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        dmin[r] = fminf(dmin[r], (c0[k] * c0[k] + c1[k] * c1[k]) - 2.f * (p0[r] * c0[k] + p1[r] * c1[k]));
+      for (int k = 0; k < 8; ++k) {
+        d32[r][k] = fmaf(-2.f * p0[r], c0[k], fmaf(-2.f * p1[r], c1[k], cn[k]));
+        dmin[r] = fminf(dmin[r], d32[r][k]);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -447,14 +455,13 @@ __global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half
     for (int r = 0; r < RB; ++r) {
       const int b = b0 + r;
       if (b >= B) break;  // warp-uniform
+      // screen tolerance: a bound on the fp32 rounding of |c|^2 - 2 p.c relative to the
+      // float64 distance (2 sqrt(|p|^2 |c|^2) <= |p|^2 + |c|^2 keeps it sqrt-free)
       const float pn32 = p0[r] * p0[r] + p1[r] * p1[r];
-      const float tol = 1e-5f * (cmax2 + 2.f * sqrtf(pn32 * cmax2)) + 1e-30f;
+      const float tol = 2e-5f * (cmax2 + pn32) + 1e-30f;
       unsigned cand = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float d = (c0[k] * c0[k] + c1[k] * c1[k]) - 2.f * (p0[r] * c0[k] + p1[r] * c1[k]);
-        cand |= (d <= dmin[r] + tol) ? (1u << k) : 0u;
-      }
+      for (int k = 0; k < 8; ++k) cand |= (d32[r][k] <= dmin[r] + tol) ? (1u << k) : 0u;
       const unsigned lanes = __ballot_sync(0xffffffffu, cand != 0);
       int code;
       if (__popc(lanes) == 1 && __popc(__shfl_sync(0xffffffffu, cand, __ffs(lanes) - 1)) == 1) {
@@ -490,11 +497,7 @@ __global__ void __launch_bounds__(256, 3) qkv_rope_append_cq_kernel(const __half
         }
         code = best_e;
       }
-      if (lane == 0) {
-        const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
-        const int64_t off = (g.layout == VQB_LAYOUT_PLAIN) ? s : il_offset(g, 0, s);
-        reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off] = (uint8_t)code;
-      }
+      if (lane == 0) reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off0 + (int64_t)b * bstride] = (uint8_t)code;
     }
   }
 }
