@@ -350,24 +350,29 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
 }
 
 // CQ fast path of the front end (v = 2, 256 entries, one level on both caches): one
-// warp per (head, channel group, K|V) keeps that group's 256 entries in registers (8
-// per lane) and walks the batch rows, so a book is read once per step instead of
-// once per row; q is roped by one warp per (batch row, head). Distances are screened
-// in fp32 and only the candidates within the fp32 error band are rescored in float64
-// (the reference's float64 argmin is always among them); a single candidate — the
-// usual case — needs no rescoring at all.
-__global__ void __launch_bounds__(256, 2) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
-                                                                 __half* __restrict__ q_out, Geom gk,
-                                                                 void* __restrict__ kcodes,
-                                                                 const __half* __restrict__ kbooks, Geom gv,
-                                                                 void* __restrict__ vcodes,
-                                                                 const __half* __restrict__ vbooks, int B, int H,
-                                                                 int C, const int* __restrict__ d_len,
-                                                                 float log2_theta) {
+// warp per (head, channel group, K|V) stages that group's 256 entries in shared memory
+// ({c0, c1, |c|^2} per entry) and quantizes every batch row of the step; q is roped by
+// one warp per (batch row, head). The warp's lanes are (row, split) pairs: S = 32 / B'
+// lanes share a row (B' = batch rounded up to a power of two, at most 32) and each
+// scans every S-th entry, so a batch of 16 scans 128 entries per lane instead of the
+// whole warp reducing over each row in turn. Distances are screened in fp32 (best and
+// second best per lane, merged over the row's lanes); only rows whose best two lie
+// within the fp32 error band rescore their candidates in float64 (the reference's
+// float64 argmin, lowest index on ties, is always among them).
+__global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
+                                                               __half* __restrict__ q_out, Geom gk,
+                                                               void* __restrict__ kcodes,
+                                                               const __half* __restrict__ kbooks, Geom gv,
+                                                               void* __restrict__ vcodes,
+                                                               const __half* __restrict__ vbooks, int B, int H,
+                                                               int C, const int* __restrict__ d_len,
+                                                               float log2_theta) {
+  __shared__ float4 books_s[8][256];  // per warp: {c0, c1, |c|^2, 0}
   pdl_launch_dependents();
   pdl_wait();
   const int G = C / 2;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wl = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + wl;
   const int lane = threadIdx.x & 31;
   const int pos = __ldg(d_len) - 1;
   const int n_book_warps = 2 * H * G;
@@ -385,19 +390,20 @@ __global__ void __launch_bounds__(256, 2) qkv_rope_append_cq_kernel(const __half
   const int h = hg / G, gi = hg % G;
   const Geom& g = is_k ? gk : gv;
   const __half* book = (is_k ? kbooks : vbooks) + (int64_t)(h * G + gi) * 256 * 2;  // region = h*G + gi
-  uint32_t wv[8];
-  float c0[8], c1[8], cn[8];
+  float4* bk = books_s[wl];
   float cmax2 = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    wv[k] = __ldg(reinterpret_cast<const uint32_t*>(book) + lane + 32 * k);
-    c0[k] = __half2float(__ushort_as_half((unsigned short)(wv[k] & 0xffff)));
-    c1[k] = __half2float(__ushort_as_half((unsigned short)(wv[k] >> 16)));
-    cn[k] = c0[k] * c0[k] + c1[k] * c1[k];
-    cmax2 = fmaxf(cmax2, cn[k]);
+    const uint32_t wv = __ldg(reinterpret_cast<const uint32_t*>(book) + lane + 32 * k);
+    const float c0 = __half2float(__ushort_as_half((unsigned short)(wv & 0xffff)));
+    const float c1 = __half2float(__ushort_as_half((unsigned short)(wv >> 16)));
+    const float cn = c0 * c0 + c1 * c1;
+    bk[lane + 32 * k] = make_float4(c0, c1, cn, 0.f);
+    cmax2 = fmaxf(cmax2, cn);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cmax2 = fmaxf(cmax2, __shfl_xor_sync(0xffffffffu, cmax2, o));
+  __syncwarp();
   // rope factors of this group's two channels (k only): position-dependent, row-independent
   float cs[2] = {1.f, 1.f}, sn[2] = {0.f, 0.f};
   if (is_k) {
@@ -412,14 +418,16 @@ __global__ void __launch_bounds__(256, 2) qkv_rope_append_cq_kernel(const __half
   const int64_t s00 = ((int64_t)h * g.d_T + pos) * G + gi;
   const int64_t off0 = (g.layout == VQB_LAYOUT_PLAIN) ? s00 : il_offset(g, 0, s00);
   const int64_t bstride = (int64_t)H * g.d_T * G;
-  // rows in groups of RB: the row loads and the warp min-reductions of a group are
-  // independent, so their latencies overlap instead of chaining row after row
-  constexpr int RB = 4;
-  for (int b0 = 0; b0 < B; b0 += RB) {
-    float p0[RB], p1[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const int b = min(b0 + r, B - 1);
+  int rows = 1;  // B' = rows per pass (power of two <= 32)
+  while (rows < B && rows < 32) rows <<= 1;
+  const int S = 32 / rows;  // lanes per row
+  const int split = lane & (S - 1), rl = lane / S;
+  const int n_e = 256 / S;
+  for (int b0 = 0; b0 < B; b0 += rows) {
+    const int b = b0 + rl;
+    const bool valid = b < B;
+    float p0 = 0.f, p1 = 0.f;
+    if (valid) {
       const __half* row = qkv + (int64_t)b * 3 * H * C + (int64_t)((is_k ? H : 2 * H) + h) * C;
       float pj[2];
 #pragma unroll
@@ -434,71 +442,73 @@ __global__ void __launch_bounds__(256, 2) qkv_rope_append_cq_kernel(const __half
           pj[j] = __half2float(row[c]);
         }
       }
-      p0[r] = pj[0];
-      p1[r] = pj[1];
+      p0 = pj[0];
+      p1 = pj[1];
     }
-    float dmin[RB], d32[RB][8];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      dmin[r] = FLT_MAX;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        d32[r][k] = fmaf(-2.f * p0[r], c0[k], fmaf(-2.f * p1[r], c1[k], cn[k]));
-        dmin[r] = fminf(dmin[r], d32[r][k]);
+    // fp32 screen: best (lowest index among equals) and second-best distance
+    const float m0 = -2.f * p0, m1 = -2.f * p1;
+    float d1 = FLT_MAX, d2 = FLT_MAX;
+    int e1 = 0x7fffffff;
+#pragma unroll 8
+    for (int i = 0; i < n_e; ++i) {
+      const int e = i * S + split;
+      const float4 c = bk[e];
+      const float d = fmaf(m0, c.x, fmaf(m1, c.y, c.z));
+      if (d < d1) {
+        d2 = d1;
+        d1 = d;
+        e1 = e;
+      } else if (d < d2) {
+        d2 = d;
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int r = 0; r < RB; ++r) dmin[r] = fminf(dmin[r], __shfl_xor_sync(0xffffffffu, dmin[r], o));
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const int b = b0 + r;
-      if (b >= B) break;  // warp-uniform
-      // screen tolerance: a bound on the fp32 rounding of |c|^2 - 2 p.c relative to the
-      // float64 distance (2 sqrt(|p|^2 |c|^2) <= |p|^2 + |c|^2 keeps it sqrt-free)
-      const float pn32 = p0[r] * p0[r] + p1[r] * p1[r];
-      const float tol = 2e-5f * (cmax2 + pn32) + 1e-30f;
-      unsigned cand = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) cand |= (d32[r][k] <= dmin[r] + tol) ? (1u << k) : 0u;
-      const unsigned lanes = __ballot_sync(0xffffffffu, cand != 0);
-      int code;
-      if (__popc(lanes) == 1 && __popc(__shfl_sync(0xffffffffu, cand, __ffs(lanes) - 1)) == 1) {
-        const int src = __ffs(lanes) - 1;
-        const unsigned cb = __shfl_sync(0xffffffffu, cand, src);
-        code = src + 32 * (__ffs(cb) - 1);
-      } else {
-        // several candidates: float64 distances in the reference's operation order
-        const double r0 = p0[r], r1 = p1[r];
+    for (int o = 1; o < S; o <<= 1) {  // merge the row's lanes
+      const float od1 = __shfl_xor_sync(0xffffffffu, d1, o), od2 = __shfl_xor_sync(0xffffffffu, d2, o);
+      const int oe1 = __shfl_xor_sync(0xffffffffu, e1, o);
+      d2 = fminf(fmaxf(d1, od1), fminf(d2, od2));
+      if (od1 < d1 || (od1 == d1 && oe1 < e1)) {
+        d1 = od1;
+        e1 = oe1;
+      }
+    }
+    // screen tolerance: a bound on the fp32 rounding of |c|^2 - 2 p.c relative to the
+    // float64 distance (2 sqrt(|p|^2 |c|^2) <= |p|^2 + |c|^2 keeps it sqrt-free)
+    const float tol = 2e-5f * (cmax2 + p0 * p0 + p1 * p1) + 1e-30f;
+    const bool need64 = valid && (d2 - d1 <= tol);
+    int code = e1;
+    if (__any_sync(0xffffffffu, need64)) {
+      // several candidates: float64 distances in the reference's operation order
+      double best = DBL_MAX;
+      int be = 0x7fffffff;
+      if (need64) {
+        const double r0 = p0, r1 = p1;
         const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
-        double best = DBL_MAX;
-        int best_e = 0x7fffffff;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (cand & (1u << k)) {
-            const double a0 = c0[k], a1 = c1[k];
+        for (int i = 0; i < n_e; ++i) {
+          const int e = i * S + split;
+          const float4 c = bk[e];
+          if (fmaf(m0, c.x, fmaf(m1, c.y, c.z)) <= d1 + tol) {
+            const double a0 = c.x, a1 = c.y;
             const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
             const double cn = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
             const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
-            if (d < best) {
+            if (d < best) {  // entries ascend: the first minimum is the lowest index
               best = d;
-              best_e = lane + 32 * k;
+              be = e;
             }
           }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
-          if (ob < best || (ob == best && oe < best_e)) {
-            best = ob;
-            best_e = oe;
-          }
         }
-        code = best_e;
       }
-      if (lane == 0) reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off0 + (int64_t)b * bstride] = (uint8_t)code;
+      for (int o = 1; o < S; o <<= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (ob < best || (ob == best && oe < be)) {
+          best = ob;
+          be = oe;
+        }
+      }
+      if (need64) code = be;
     }
+    if (valid && split == 0) reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off0 + (int64_t)b * bstride] = (uint8_t)code;
   }
 }
 
