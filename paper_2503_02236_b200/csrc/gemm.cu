@@ -421,9 +421,12 @@ __global__ void __launch_bounds__(256) gemm_splitk_reduce_kernel(const float* __
 // K splits for a grid of `tiles` output tiles (one CTA per SM): minimise the waves a
 // split grid needs per unit of work, ceil(tiles * s / SMs) / s, at least 4 stages per
 // split; ties to the smaller split (fewer partials)
+// split-K factor minimising the wave-quantised time. Only for a single row tile
+// (decode batches up to 256 rows): there the fp32 partials are small, while at
+// prefill sizes they would cost more HBM traffic than the quantisation saves.
 static int gemm_splits(int tiles, int k_total) {
   const int sms = sm_count();
-  if (tiles >= sms) return 1;
+  if (tiles >= 2 * sms) return 1;
   int best = 1;
   double best_t = 1e30;
   for (int sp = 1; sp <= std::min(16, std::max(1, k_total / 4)); ++sp) {
@@ -437,7 +440,9 @@ int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows) {
   Geom g;
   if (make_geom(w, &g)) return 0;
   const int tiles = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
-  const int sp = g.cols % kTileN == 0 && g.rows % kTileK == 0 ? gemm_splits(std::max(tiles, 1), (int)(g.rows / kTileK)) : 1;
+  const int sp = g.cols % kTileN == 0 && g.rows % kTileK == 0 && rows <= kTileM
+                     ? gemm_splits(std::max(tiles, 1), (int)(g.rows / kTileK))
+                     : 1;
   return sp > 1 ? VQB_WS_COUNTER_BYTES + (int64_t)sp * rows * g.cols * 4 : 0;
 }
 
@@ -525,7 +530,7 @@ extern "C" int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, in
     a.K = g.K;
     a.n_sh = std::min(g.K, kBookEntries);
     const int tiles = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
-    a.splits = gemm_splits(tiles, (int)(g.rows / kTileK));
+    a.splits = rows <= kTileM ? gemm_splits(tiles, (int)(g.rows / kTileK)) : 1;
     a.part = nullptr;
     if (a.splits > 1) {
       const int64_t need = VQB_WS_COUNTER_BYTES + (int64_t)a.splits * rows * g.cols * 4;
