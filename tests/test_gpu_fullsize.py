@@ -69,10 +69,12 @@ def test_full_size_gemv(label, shape, v, bits, r, sharing, work, dev):
     assert _rel(y + y2, y12) <= 2e-3
 
 
-@pytest.mark.parametrize("rows", [16, 1024])
-def test_full_size_gemm(rows, dev):
+@pytest.mark.parametrize("rows,n", [(16, 12288), (1024, 12288), (16, 22016), (64, 22016)])
+def test_full_size_gemm(rows, n, dev):
+    """qkv and gate_up shapes: split-K below one wave of tiles (96 tiles) and between
+    one and two waves (172 tiles), no split at prefill size."""
     N, ops, *_ = _mods()
-    w = _weight(dev, (4096, 12288), 8, 16, 1, "whole", 256, seed=2)
+    w = _weight(dev, (4096, n), 8, 16, 1, "whole", 256, seed=2)
     dense = ops.vq_dequantize(w)
     g = torch.Generator(device=dev).manual_seed(3)
     x = torch.randn((rows, 4096), generator=g, device=dev).half()
