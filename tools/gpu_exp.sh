@@ -1,4 +1,7 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x 2>&1 | tail -2
-for lib in ab/base.so paper_2503_02236_b200/libvqb.so; do echo $lib; VQB_LIB_PATH=$PWD/$lib python tools/decode_bench.py 16 64; done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base function -k regex:"gemm" -s 6 -c 6 python tools/decode_bench.py 16 --layers 2 --reps 3 2>&1 | grep -E "gemm|duration"
+SECONDS=0; timeout 600 python bench.py > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo "bench wall $SECONDS s"
+python -c "
+import json; d=json.load(open('gpurun_out/bench1.json'))
+print(d['value'], d['ms_per_step'], d['e2e']['value'], d['clocks'])
+print(d['attention_c4']['us_per_call'], [x['tokens_per_s'] for x in d['decode_c5']])"
