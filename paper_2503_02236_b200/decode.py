@@ -102,8 +102,10 @@ class VQLlamaDecoder:
 
     # -- the step -----------------------------------------------------------------------------
 
+    gemv_max_rows = 8  # batches up to this take the CUDA-core GEMV, larger ones the tcgen05 GEMM
+
     def _linear(self, w: DeviceVQTensor, x: torch.Tensor) -> torch.Tensor:
-        if x.shape[0] <= 8 and x.shape[0] in (1, 2, 4, 8):
+        if x.shape[0] <= self.gemv_max_rows and x.shape[0] in (1, 2, 4, 8):
             return ops.vq_gemv(w, x, out_dtype=torch.float16)
         return ops.vq_gemm(w, x, out_dtype=torch.float16)
 

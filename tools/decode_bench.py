@@ -23,11 +23,14 @@ def main():
     ap.add_argument("--ctx", type=int, default=4096)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--gemv-max-rows", type=int, default=None)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     for b in args.batch:
         sh = LlamaShape(layers=args.layers)
         dec = VQLlamaDecoder.synthetic(sh, b, args.ctx, dev)
+        if args.gemv_max_rows is not None:
+            dec.gemv_max_rows = args.gemv_max_rows
         dec.set_length(args.ctx - 1 - args.reps - 3)
         dec.capture()
         for _ in range(3):
