@@ -125,6 +125,8 @@ typedef struct VqbLaunch {
 #define VQB_FLAG_NO_PDL 4        /* launch without programmatic dependent launch */
 #define VQB_FLAG_EXACT_ACCUM 8   /* GEMV: fp32 accumulation of every product (mixed-precision
                                     FMA, quarter rate) instead of 8-row fp16x2 windows */
+#define VQB_FLAG_NO_MMA 16       /* GEMV batch 4-8: CUDA-core FMAs instead of the tensor-core
+                                    (mma.sync) inner product */
 
 /* Kernel resource usage (KernelUsage, gpumodel.py:30-36) measured with
  * cudaFuncGetAttributes on the loaded cubin. */

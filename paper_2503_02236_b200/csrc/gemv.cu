@@ -48,30 +48,31 @@ namespace vqb {
 // looked-up entry feeds 8 FMAs, so 8 warps with more registers keep the B x V fp32
 // accumulators in registers. Measured: 8 warps at batch 1 with two CTAs per SM (so
 // the next launch's prologue could overlap this one's tail) is 6 % slower.
-__host__ __device__ constexpr int gemv_warps(int B) { return B >= 8 ? 8 : 16; }
+// The tensor-core path (batch 4-8) keeps 16 warps: its accumulators do not grow with B.
+__host__ __device__ constexpr int gemv_warps(int B, bool mma = false) { return (B >= 8 && !mma) ? 8 : 16; }
 // rows a warp handles per chunk: 32 (two 16-byte code words of u8 codes, four of u16).
 // Measured: 8-row slabs double the per-chunk overhead; 16-row slabs leave half the
 // code words in flight; 64-row slabs no longer fit the ring with the codebook.
 __host__ __device__ constexpr int gemv_slab_rows(int cbytes) { return 32; }
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
 // chunk rows: the warps along M each take one 16-row slab (WG = warps across N)
-__host__ __device__ constexpr int gemv_chunk_rows(int WG, int B, int cbytes) {
-  return gemv_slab_rows(cbytes) * (gemv_warps(B) / WG);
+__host__ __device__ constexpr int gemv_chunk_rows(int WG, int B, int cbytes, bool mma = false) {
+  return gemv_slab_rows(cbytes) * (gemv_warps(B, mma) / WG);
 }
 // bytes of one chunk's codes: R levels x chunk rows x 32*WG columns
-__host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG, int B) {
-  return R * cbytes * WG * gemv_chunk_rows(WG, B, cbytes) * 32;
+__host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG, int B, bool mma = false) {
+  return R * cbytes * WG * gemv_chunk_rows(WG, B, cbytes, mma) * 32;
 }
 // a ring stage also carries the chunk's activations: B rows x chunk rows fp16
-__host__ __device__ constexpr int stage_total(int R, int cbytes, int WG, int B) {
-  return stage_bytes(R, cbytes, WG, B) + B * gemv_chunk_rows(WG, B, cbytes) * 2;
+__host__ __device__ constexpr int stage_total(int R, int cbytes, int WG, int B, bool mma = false) {
+  return stage_bytes(R, cbytes, WG, B, mma) + B * gemv_chunk_rows(WG, B, cbytes, mma) * 2;
 }
 // ring depth: ~96 KB of code loads in flight per SM (HBM latency x per-SM share of
 // the bandwidth), 3..12 stages
-__host__ __device__ constexpr int gemv_stages(int R, int cbytes, int WG, int B) {
-  return (98304 / stage_total(R, cbytes, WG, B)) < 3    ? 3
-         : (98304 / stage_total(R, cbytes, WG, B)) > 12 ? 12
-                                                        : 98304 / stage_total(R, cbytes, WG, B);
+__host__ __device__ constexpr int gemv_stages(int R, int cbytes, int WG, int B, bool mma = false) {
+  return (98304 / stage_total(R, cbytes, WG, B, mma)) < 3    ? 3
+         : (98304 / stage_total(R, cbytes, WG, B, mma)) > 12 ? 12
+                                                             : 98304 / stage_total(R, cbytes, WG, B, mma);
 }
 
 struct GemvFastArgs {
@@ -101,15 +102,23 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // later CTAs' fp32 partials (computed at the start of their ranges, so normally
 // already published) in chunk order: deterministic, like the reference's ordered
 // split reduction (sim.py:735), with no atomics and no extra launch.
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, bool H2>
-__global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
-  constexpr int kGemvWarps = gemv_warps(B);
+// ACC selects the inner product: 0 exact fp32 (FHFMA, parity mode), 1 fp16x2 windows
+// (HFMA2, batch 1-2), 2 tensor cores (mma.sync m16n8k16, batch 4-8): the looked-up
+// entries become A fragments through ldmatrix.trans straight from the replicated
+// shared codebook (W^T: 16 columns x 16 rows per column pair), the activations the
+// B fragment (16 rows x 8 batch rows), fp32 accumulation.
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC>
+__global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
+  constexpr bool H2 = ACC == 1;
+  constexpr bool MMA = ACC == 2;
+  static_assert(!MMA || (V == 8 && WG == 1 && !GTIER && !TILE), "tensor-core GEMV: v = 8, codes in shared memory");
+  constexpr int kGemvWarps = gemv_warps(B, MMA);
   constexpr int kGemvThreads = kGemvWarps * 32;
   constexpr int EB = V * 2;              // fp16 entry bytes
   constexpr int REP = 128 / EB;          // replicas per bank row
   constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code word
   constexpr int WM = kGemvWarps / WG;    // warps along M
-  constexpr int CR = gemv_chunk_rows(WG, B, CBYTES);
+  constexpr int CR = gemv_chunk_rows(WG, B, CBYTES, MMA);
   constexpr int kSlabRows = gemv_slab_rows(CBYTES);
   constexpr int LOADS = kSlabRows / RPL;  // code words per lane per level per chunk
   constexpr int COLS = 32 * WG * V;      // output columns per column block (256)
@@ -124,12 +133,12 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
   // replica offset (the book base and the half fold into the LDS addressing).
   constexpr bool WIDE = !GTIER && R * NBUF <= 2;
   static_assert(LOADS >= 1, "bad tiling");
-  static_assert(gemv_stages(R, CBYTES, WG, B) >= 3, "the ring refill lags two units");
+  static_assert(gemv_stages(R, CBYTES, WG, B, MMA) >= 3, "the ring refill lags two units");
   constexpr int STAGEB = R * LEVB;
-  static_assert(STAGEB == stage_bytes(R, CBYTES, WG, B), "stage size");
+  static_assert(STAGEB == stage_bytes(R, CBYTES, WG, B, MMA), "stage size");
   constexpr int XROWB = CR * 2;          // one batch row's activations per chunk
-  constexpr int STG = stage_total(R, CBYTES, WG, B);
-  constexpr int kStages = gemv_stages(R, CBYTES, WG, B);
+  constexpr int STG = stage_total(R, CBYTES, WG, B, MMA);
+  constexpr int kStages = gemv_stages(R, CBYTES, WG, B, MMA);
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -256,11 +265,17 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
   __syncthreads();
   if (tid == 0) trace_at(a.trace, 1);
 
-  float acc[B][V];
+  float acc[MMA ? 1 : B][V];
 #pragma unroll
-  for (int b = 0; b < B; ++b)
+  for (int b = 0; b < (MMA ? 1 : B); ++b)
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
+  // MMA: D fragments (16 columns x 8 batch rows) of the block's 16 column pairs
+  float cacc[MMA ? 16 : 1][4];
+#pragma unroll
+  for (int q = 0; q < (MMA ? 16 : 1); ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cacc[q][j] = 0.f;
 
   int cur_buf = 0;
   int span_first = u0;  // first unit of the current span
@@ -294,7 +309,41 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
     const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
     const int region = region_of(u);
     const bool active = wm * kSlabRows < unit_rows(u);  // the last chunk may be partial
-    if (active) {
+    if (MMA && active) {
+      // per 16-row k-block: the activations' B fragment (lane: batch row lane/4, rows
+      // 2(lane%4)+{0,1}, +8), then per column pair one ldmatrix.x4.trans whose 32 row
+      // addresses are looked-up entries (lane: matrix lane/8 = (column half, k half),
+      // row lane%8; replica lane%8 keeps each 8-lane phase conflict-free)
+      const int j4 = lane >> 3, rr = lane & 7, bn = lane >> 2;
+#pragma unroll
+      for (int kb = 0; kb < kSlabRows / 16; ++kb) {
+        uint32_t xb0 = 0u, xb1 = 0u;
+        if (bn < B) {
+          const uint8_t* xr = xs + bn * XROWB + (kb * 16 + 2 * (lane & 3)) * 2;
+          xb0 = *reinterpret_cast<const uint32_t*>(xr);
+          xb1 = *reinterpret_cast<const uint32_t*>(xr + 16);
+        }
+        const int row = kb * 16 + (j4 >> 1) * 8 + rr;  // this lane's row of the slab
+        const uint8_t* cbase = st + (wm * LOADS + row / RPL) * RGB + (row % RPL) * CBYTES + (j4 & 1) * 16;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const uint8_t* cp = cbase + r * LEVB + q * 32;
+            const uint32_t code = CBYTES == 2 ? (uint32_t)*reinterpret_cast<const uint16_t*>(cp) : (uint32_t)*cp;
+            const uint32_t addr = WIDE ? smem_u32(books_s) + (code << 8) + (R == 2 ? r : cur_buf) * 128 + rep_off
+                                       : smem_u32(bsm) + (uint32_t)(r * a.n_sh * 128) + (code << 7);
+            uint32_t a0, a1, a2, a3;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(addr));
+            asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                         "{%8, %9}, {%0, %1, %2, %3};"
+                         : "+f"(cacc[q][0]), "+f"(cacc[q][1]), "+f"(cacc[q][2]), "+f"(cacc[q][3])
+                         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(xb0), "r"(xb1));
+          }
+        }
+      }
+    } else if (active) {
       // code words of this warp's slab (LOADS x R 16-byte words per lane)
       uint4 cw[LOADS][R];
 #pragma unroll
@@ -455,11 +504,28 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
       float keep[B];
 #pragma unroll
       for (int b = 0; b < B; ++b) {
+        if constexpr (MMA) {
+          // D fragment: lane holds columns 16q + lane/4 (+8) of batch rows 2(lane%4) + {0, 1}
+          // (the column index goes through an opaque shift: nvcc otherwise folds
+          // 4 * (lane >> 2) into lane - (b >> 1) under the predicate and emitted
+          // misaligned stores for the batch-8 instance)
+          uint32_t cq;
+          asm("shr.b32 %0, %1, 2;" : "=r"(cq) : "r"((uint32_t)lane));
+          float* rp = red + (size_t)wm * COLS + cq;
+          if ((lane & 3) == (b >> 1)) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              rp[16 * q] = cacc[q][b & 1];
+              rp[16 * q + 8] = cacc[q][2 + (b & 1)];
+            }
+          }
+        } else {
         // partials stored [w][q][g][4]: each lane's float4 stores are conflict-free
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
           *reinterpret_cast<float4*>(red + (size_t)wm * COLS + (q * GC + g_local) * 4) =
               make_float4(acc[b][4 * q], acc[b][4 * q + 1], acc[b][4 * q + 2], acc[b][4 * q + 3]);
+        }
         __syncthreads();
         keep[b] = 0.f;
         if (tid < COLS) {
@@ -468,7 +534,7 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
 #pragma unroll
           for (int w = 0; w < WM; ++w) sum += red[(size_t)w * COLS + o];
           const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
-          const int col = g * V + q * 4 + c;
+          const int col = MMA ? o : g * V + q * 4 + c;
           if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * COLS + col, sum);
           else if (finisher) keep[b] = sum;
           else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + b) * COLS + col, tag_partial(sum));
@@ -485,7 +551,7 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
         if (tid < COLS) {
           const int o = tid;
           const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
-          const int col = g * V + q * 4 + c;
+          const int col = MMA ? o : g * V + q * 4 + c;
 #pragma unroll
           for (int b = 0; b < B; ++b) {
             float sum = keep[b];
@@ -513,9 +579,13 @@ __global__ void __launch_bounds__(gemv_warps(B) * 32, 1) gemv_fast_kernel(GemvFa
         if (tid == 0) trace_at(a.trace, 5);
       }
 #pragma unroll
-      for (int b = 0; b < B; ++b)
+      for (int b = 0; b < (MMA ? 1 : B); ++b)
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
+#pragma unroll
+      for (int q = 0; q < (MMA ? 16 : 1); ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cacc[q][j] = 0.f;
       span_first = u + 1;
       cb += 1;
       span_end = min(u1, (cb + 1) * a.n_chunks);
@@ -589,7 +659,7 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
 struct FastPlan {
   bool ok = false;
   int V = 0, cbytes = 0, R = 0, WG = 1;
-  bool tile = false, gtier = true, h2 = true;
+  bool tile = false, gtier = true, h2 = true, mma = false;
   int n_sh = 0, n_cblk = 0, n_chunks = 0, threads = 0;
   size_t smem = 0;
 };
@@ -626,13 +696,19 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   if (!p.gtier) n_sh = std::min(n_sh, 256);
   p.n_sh = n_sh;
   p.h2 = !(L && (L->flags & VQB_FLAG_EXACT_ACCUM));
+  // batch 4-8: tensor-core inner product (every entry resident in shared memory).
+  // Measured (quip2 4096x12288 / 4096x4096): batch 8 22.0 / 13.7 us vs 28.1 / 20.1 on
+  // CUDA cores, batch 4 about even, batch 2 slower (the mma path reads its codes with a
+  // 2-way bank conflict per 16-row k-block of the GEMV_IL words).
+  p.mma = p.h2 && !p.gtier && !p.tile && g.v == 8 && rows >= 4 && !(L && (L->flags & VQB_FLAG_NO_MMA));
+  const int CRm = gemv_chunk_rows(p.WG, rows, p.cbytes, p.mma);
   p.n_cblk = (int)(g.cols / cols_per_cta);
-  p.n_chunks = (int)((g.rows + CR - 1) / CR);
-  p.threads = gemv_warps(rows) * 32;
-  const int nst = gemv_stages(p.R, p.cbytes, p.WG, rows);
-  const int WM = gemv_warps(rows) / p.WG;
+  p.n_chunks = (int)((g.rows + CRm - 1) / CRm);
+  p.threads = gemv_warps(rows, p.mma) * 32;
+  const int nst = gemv_stages(p.R, p.cbytes, p.WG, rows, p.mma);
+  const int WM = gemv_warps(rows, p.mma) / p.WG;
   const bool wide = !p.gtier && p.R * (p.tile ? 2 : 1) <= 2;  // mirrors the kernel's WIDE layout
-  p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows) +
+  p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows, p.mma) +
            (wide ? (size_t)65536 : (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128) + (size_t)WM * cols_per_cta * 4 +
            2 * nst * 8 + 16;
   p.ok = true;
@@ -697,30 +773,34 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
   return VQB_OK;
 }
 
+template <int V, int CBYTES, int R, int B, int WG, bool TILE>
+static GemvKernel pick_acc(bool gtier, bool h2, bool mma) {
+  if constexpr (V == 8 && WG == 1 && !TILE && B >= 2)
+    if (mma && !gtier) return gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, 2>;
+  return gtier ? (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, 1>
+                     : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, 0>)
+               : (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, 1>
+                     : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, 0>);
+}
+
 template <int V, int CBYTES, int R, int WG, bool TILE>
-static GemvKernel pick_kernel(int rows, bool gtier, bool h2) {
-#define VQB_K(B)                                                                        \
-  (gtier ? (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, true>                  \
-               : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, false>)                \
-         : (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, true>                 \
-               : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, false>))
+static GemvKernel pick_kernel(int rows, bool gtier, bool h2, bool mma) {
   switch (rows) {
-    case 1: return VQB_K(1);
-    case 2: return VQB_K(2);
-    case 4: return VQB_K(4);
-    default: return VQB_K(8);
+    case 1: return pick_acc<V, CBYTES, R, 1, WG, TILE>(gtier, h2, mma);
+    case 2: return pick_acc<V, CBYTES, R, 2, WG, TILE>(gtier, h2, mma);
+    case 4: return pick_acc<V, CBYTES, R, 4, WG, TILE>(gtier, h2, mma);
+    default: return pick_acc<V, CBYTES, R, 8, WG, TILE>(gtier, h2, mma);
   }
-#undef VQB_K
 }
 
 static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
   // (V, code bytes, R, WG, tile-shared) combinations covering the BASELINE configs
-  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier, p.h2);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier, p.h2);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier, p.h2);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier, p.h2);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier, p.h2);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier, p.h2);
+  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier, p.h2, p.mma);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier, p.h2, p.mma);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier, p.h2, p.mma);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier, p.h2, p.mma);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier, p.h2, p.mma);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier, p.h2, p.mma);
   return nullptr;
 }
 

@@ -163,6 +163,27 @@ def test_gemv_fast_kernel(label, shape, v, bits, r, sharing, tile, work, rows, d
     assert torch.equal(y, y2), "split reduction must be deterministic"
 
 
+@pytest.mark.parametrize("rows", [4, 8])
+@pytest.mark.parametrize("label,shape,v,bits,r,sharing,tile,work", [c for c in FAST_GEMV if c[2] == 8 and c[5] == "whole"])
+def test_gemv_cuda_core_path_at_mma_batches(label, shape, v, bits, r, sharing, tile, work, rows, dev):
+    """Batch 4-8 default to the tensor-core inner product; VQB_FLAG_NO_MMA keeps the
+    CUDA-core path reachable and equally exact."""
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    cfg = VQConfig(v, bits, r, Sharing.whole_tensor())
+    codes, books, nreg, dense = _big_weight(shape, v, bits, r, sharing, tile, work)
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev)
+    x = torch.from_numpy(O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))).to(dev).half()
+    ref = O.matmul_ref(x.float().cpu().numpy(), dense)
+    L = ops.launch_struct()
+    L.flags = N.FLAG_NO_MMA
+    y_fma = ops.vq_gemv(d, x, launch=L)
+    y_mma = ops.vq_gemv(d, x)
+    assert N.last_kernel() == "gemv_fast"
+    assert O.rel_err(y_fma.cpu().numpy(), ref) <= TOL_F16
+    assert O.rel_err(y_mma.cpu().numpy(), ref) <= TOL_F16
+
+
 def test_gemv_fast_fp16_output_and_plans(dev):
     from paper_2503_02236_b200.codec import VQConfig
     N, DeviceVQTensor, ops = _mods()
