@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   const size_t book_bytes = (size_t)R * a.n_sh * 128;
   const size_t book_region = WIDE ? 65536 : NBUF * book_bytes;
   float* red = reinterpret_cast<float*>(books_s + book_region);  // WM x COLS cross-warp partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + WM * COLS);       // full[kStages], empty[kStages]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + (MMA ? 2 : 1) * WM * COLS);  // full[kStages], empty[kStages]
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
 
   const int U = a.n_cblk * a.n_chunks;
@@ -501,9 +501,14 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
       const int cl = u - cb * a.n_chunks;           // last chunk
       const bool whole = (cf == 0 && cl == a.n_chunks - 1);
       const bool finisher = (cf == 0 && !whole);
+      // MMA: a D fragment holds two batch rows, so each pass reduces two rows with all
+      // 512 threads (thread half t / COLS takes row b + half); keep[b] then holds
+      // this thread's row b + half
+      constexpr int BP = MMA ? 2 : 1;
+      const int half = MMA ? tid / COLS : 0;
       float keep[B];
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
+      for (int b = 0; b < B; b += BP) {
         if constexpr (MMA) {
           // D fragment: lane holds columns 16q + lane/4 (+8) of batch rows 2(lane%4) + {0, 1}
           // (the column index goes through an opaque shift: nvcc otherwise folds
@@ -515,8 +520,10 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
           if ((lane & 3) == (b >> 1)) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              rp[16 * q] = cacc[q][b & 1];
-              rp[16 * q + 8] = cacc[q][2 + (b & 1)];
+              rp[16 * q] = cacc[q][0];
+              rp[16 * q + 8] = cacc[q][2];
+              rp[WM * COLS + 16 * q] = cacc[q][1];
+              rp[WM * COLS + 16 * q + 8] = cacc[q][3];
             }
           }
         } else {
@@ -528,16 +535,16 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
         }
         __syncthreads();
         keep[b] = 0.f;
-        if (tid < COLS) {
-          const int o = tid;
+        if (tid < BP * COLS) {
+          const int o = tid % COLS, bb = b + half;
           float sum = 0.f;
 #pragma unroll
-          for (int w = 0; w < WM; ++w) sum += red[(size_t)w * COLS + o];
+          for (int w = 0; w < WM; ++w) sum += red[(size_t)(half * WM + w) * COLS + o];
           const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
           const int col = MMA ? o : g * V + q * 4 + c;
-          if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * COLS + col, sum);
+          if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)bb * a.N + (int64_t)cb * COLS + col, sum);
           else if (finisher) keep[b] = sum;
-          else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + b) * COLS + col, tag_partial(sum));
+          else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + bb) * COLS + col, tag_partial(sum));
         }
         __syncthreads();
       }
@@ -548,13 +555,14 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
         int k_end = blockIdx.x + 1;
         while (k_end < (int)gridDim.x && (int)((int64_t)k_end * U / gridDim.x) < (cb + 1) * a.n_chunks) ++k_end;
         const int n_later = k_end - blockIdx.x - 1;
-        if (tid < COLS) {
-          const int o = tid;
+        if (tid < BP * COLS) {
+          const int o = tid % COLS;
           const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
           const int col = MMA ? o : g * V + q * 4 + c;
 #pragma unroll
-          for (int b = 0; b < B; ++b) {
-            float sum = keep[b];
+          for (int b0 = 0; b0 < B; b0 += BP) {
+            const int b = b0 + half;
+            float sum = keep[b0];
             constexpr int PF = 8;  // partial loads in flight
             for (int j0 = 0; j0 < n_later; j0 += PF) {
               unsigned long long pv[PF];
@@ -709,7 +717,8 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   const int WM = gemv_warps(rows, p.mma) / p.WG;
   const bool wide = !p.gtier && p.R * (p.tile ? 2 : 1) <= 2;  // mirrors the kernel's WIDE layout
   p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows, p.mma) +
-           (wide ? (size_t)65536 : (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128) + (size_t)WM * cols_per_cta * 4 +
+           (wide ? (size_t)65536 : (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128) +
+           (size_t)(p.mma ? 2 : 1) * WM * cols_per_cta * 4 +
            2 * nst * 8 + 16;
   p.ok = true;
   return p;
