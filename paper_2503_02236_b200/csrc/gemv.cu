@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   const size_t book_bytes = (size_t)R * a.n_sh * 128;
   const size_t book_region = WIDE ? 65536 : NBUF * book_bytes;
   float* red = reinterpret_cast<float*>(books_s + book_region);  // WM x COLS cross-warp partials
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + (MMA ? 2 : 1) * WM * COLS);  // full[kStages], empty[kStages]
+  constexpr int RED_ROWS = (B >= 2 && kGemvThreads >= 2 * COLS) ? 2 : 1;  // batch rows per epilogue pass
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + RED_ROWS * WM * COLS);  // full[kStages], empty[kStages]
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
 
   const int U = a.n_cblk * a.n_chunks;
@@ -501,11 +502,12 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
       const int cl = u - cb * a.n_chunks;           // last chunk
       const bool whole = (cf == 0 && cl == a.n_chunks - 1);
       const bool finisher = (cf == 0 && !whole);
-      // MMA: a D fragment holds two batch rows, so each pass reduces two rows with all
-      // 512 threads (thread half t / COLS takes row b + half); keep[b] then holds
-      // this thread's row b + half
-      constexpr int BP = MMA ? 2 : 1;
-      const int half = MMA ? tid / COLS : 0;
+      // with 512 threads each pass reduces two batch rows (thread half t / COLS takes
+      // row b + half; a D fragment of the MMA path holds two rows anyway); keep[b] then
+      // holds this thread's row b + half
+      constexpr int BP = (B >= 2 && kGemvThreads >= 2 * COLS) ? 2 : 1;
+      static_assert(!MMA || BP == 2, "the MMA epilogue writes two rows per pass");
+      const int half = BP == 2 ? tid / COLS : 0;
       float keep[B];
 #pragma unroll
       for (int b = 0; b < B; b += BP) {
@@ -529,9 +531,11 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
         } else {
         // partials stored [w][q][g][4]: each lane's float4 stores are conflict-free
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          *reinterpret_cast<float4*>(red + (size_t)wm * COLS + (q * GC + g_local) * 4) =
-              make_float4(acc[b][4 * q], acc[b][4 * q + 1], acc[b][4 * q + 2], acc[b][4 * q + 3]);
+        for (int h = 0; h < BP; ++h)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            *reinterpret_cast<float4*>(red + (size_t)(h * WM + wm) * COLS + (q * GC + g_local) * 4) =
+                make_float4(acc[b + h][4 * q], acc[b + h][4 * q + 1], acc[b + h][4 * q + 2], acc[b + h][4 * q + 3]);
         }
         __syncthreads();
         keep[b] = 0.f;
@@ -718,7 +722,7 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   const bool wide = !p.gtier && p.R * (p.tile ? 2 : 1) <= 2;  // mirrors the kernel's WIDE layout
   p.smem = (size_t)nst * stage_total(p.R, p.cbytes, p.WG, rows, p.mma) +
            (wide ? (size_t)65536 : (size_t)(p.tile ? 2 : 1) * p.R * p.n_sh * 128) +
-           (size_t)(p.mma ? 2 : 1) * WM * cols_per_cta * 4 +
+           (size_t)((rows >= 2 && p.threads >= 2 * cols_per_cta) ? 2 : 1) * WM * cols_per_cta * 4 +
            2 * nst * 8 + 16;
   p.ok = true;
   return p;
