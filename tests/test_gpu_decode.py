@@ -244,7 +244,7 @@ def _np_decode(sh, host, tokens, steps, capacity):
     return logits_all
 
 
-@pytest.mark.parametrize("batch", [1, 2])
+@pytest.mark.parametrize("batch", [1, 2, 4, 8])  # 4 and 8: tensor-core GEMV
 def test_decode_matches_numpy_model(batch, dev):
     capacity, steps = 64, 6
     sh, dec, host = _tiny_model(dev, batch, capacity)
@@ -275,12 +275,13 @@ def test_decode_graph_replay_matches_eager(dev):
     assert int(dec2.d_len.item()) == steps
 
 
-def test_qkv_rope_append_matches_separate_kernels(dev):
+@pytest.mark.parametrize("B", [2, 5, 16, 64])  # lanes per row 16 / 4 / 2 / 1 (two passes)
+def test_qkv_rope_append_matches_separate_kernels(B, dev):
     """The fused front end (rope + K/V quantization in one launch) writes the same
     codes and q as qkv_rope followed by two vq_quantize_kv calls."""
     from paper_2503_02236_b200.decode import KV_CFG
     _, DeviceVQTensor, ops = _mods()
-    B, H, C, T = 2, 4, 128, 64
+    H, C, T = 4, 128, 64
     g = torch.Generator(device=dev).manual_seed(9)
     books = [torch.randn((H * C // 2, 256, 2), generator=g, device=dev).half() for _ in range(2)]
     caches = [[DeviceVQTensor.empty_cache((B, H, T, C), KV_CFG, bk) for bk in books] for _ in range(2)]
