@@ -462,7 +462,7 @@ def run_impl(args):
             extra["gemv_c1_gptvq2_q_proj"] = time_gemv_single(
                 torch, dev, ops, N, "C1 gptvq2 VQ<4,8,1> tile256 4096x4096 b1", (4, 8, 1, Sharing.per_tile(256, 256)),
                 (4096, 4096))
-            extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 16, 64)]  # BASELINE C5 sweep
+            extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 8, 16, 64)]  # BASELINE C5 sweep
             extra["gemv_c2_quip2_q_proj"] = time_gemv_single(
                 torch, dev, ops, N, "C2 quip2 VQ<8,16,1> ws256 4096x4096 b1", (8, 16, 1, Sharing.whole_tensor()),
                 (4096, 4096), work=WORK)
