@@ -20,7 +20,8 @@
  *   vqb_last_error   <- the message of the raised vqforge.errors exception (errors.py:4-25)
  *   vqb_cq_quantize  <- vqforge.codec.quantize / _nearest (codec.py:239-253, 367-389) for KV rows:
  *                       online nearest-centroid quantization of new tokens into a KV cache
- *   vqb_attn_decode_len, vqb_rmsnorm, vqb_qkv_rope, vqb_qkv_rope_append, vqb_silu_mul, vqb_add_len
+ *   vqb_attn_decode_len, vqb_rmsnorm, vqb_qkv_rope, vqb_qkv_rope_append, vqb_silu_mul, vqb_add_len,
+ *   vqb_take_device_error
  *                    <- the end-to-end decode step around the fused ops (
  *                       no vqforge counterpart: the reference stops at single fused kernels)
  *
@@ -220,6 +221,10 @@ int vqb_qkv_rope_append(const void* d_qkv, void* d_q_out, const VqbTensor* k_cac
 int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, int32_t ffn, void* stream);
 /* d_len[0] += delta on the stream (advances a graph-replayed decode loop). */
 int vqb_add_len(int32_t* d_len, int32_t delta, void* stream);
+/* Read and clear the device error word (synchronises the device): bit 0 = a KV
+ * append (vqb_cq_quantize / vqb_qkv_rope_append with a device length) found its
+ * write position outside [0, capacity) and skipped the write. */
+int vqb_take_device_error(int32_t* out);
 
 /* Convert a PACKED stream (src, layout must be VQB_LAYOUT_PACKED) into
  * `dst_layout`, writing into d_dst (dst_bytes available). Bytes needed are

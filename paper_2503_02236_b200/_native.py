@@ -38,7 +38,7 @@ EXPORTS = (
     "vqb_abi_version", "vqb_last_error", "vqb_last_kernel", "vqb_dequant", "vqb_workspace_bytes", "vqb_gemv",
     "vqb_gemm", "vqb_attn_decode", "vqb_layout_bytes", "vqb_repack", "vqb_query_usage",
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
-    "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append",
+    "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error",
 )
 
 
@@ -121,6 +121,7 @@ def lib():
             L.vqb_silu_mul.argtypes = [vp, vp, i32, i32, vp]
             L.vqb_qkv_rope_append.argtypes = [vp, vp, T, T, i32, i32, i32, vp, f32, vp]
             L.vqb_add_len.argtypes = [vp, i32, vp]
+            L.vqb_take_device_error.argtypes = [P(i32)]
             L.vqb_cq_quantize.argtypes = [T, vp, i32, i64, i64, i64, i32, i32, vp, vp]
             L.vqb_layout_bytes.argtypes = [T, i32]
             L.vqb_layout_bytes.restype = i64
@@ -130,7 +131,8 @@ def lib():
             L.vqb_debug_smem_base.restype = ctypes.c_int
             for name in ("vqb_dequant", "vqb_gemv", "vqb_gemm", "vqb_attn_decode", "vqb_repack",
                          "vqb_query_usage", "vqb_attn_decode_len", "vqb_rmsnorm", "vqb_qkv_rope",
-                         "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append"):
+                         "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append",
+                         "vqb_take_device_error"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -145,6 +147,13 @@ def last_kernel() -> str:
     """Name of the last kernel launched by this thread (proves which path ran)."""
     k = lib().vqb_last_kernel()
     return k.decode() if k else ""
+
+
+def take_device_error() -> int:
+    """Read and clear the device error word (bit 0: a KV append out of capacity)."""
+    v = ctypes.c_int32(0)
+    check(lib().vqb_take_device_error(ctypes.byref(v)))
+    return int(v.value)
 
 
 def check(status: int) -> int:

@@ -307,8 +307,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   const int NT = (T + kAttnChunk - 1) / kAttnChunk;
   const int BNT = a.B * NT;
   const int U = a.H * BNT;
-  const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
-  const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+  // The grid is sized from the capacity; a shorter device length leaves fewer units
+  // than CTAs. Only the first GE = min(grid, U) CTAs take part, so every
+  // participating CTA owns at least one unit and publishes the partial a finisher
+  // counts on (an empty range would never publish: the finisher would spin forever).
+  const int GE = min((int)gridDim.x, U);
+  if ((int)blockIdx.x >= GE) return;
+  const int u0 = (int)((int64_t)blockIdx.x * U / GE);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / GE);
 
   int cur_h = -1;
   bool books_inflight = false;
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       // the CTAs after this one whose ranges start inside (b, h)
       const int bh_end = u - tc0 + NT;  // first unit past this (b, h)
       int k_end = blockIdx.x + 1;
-      while (k_end < (int)gridDim.x && (int)((int64_t)k_end * U / gridDim.x) < bh_end) ++k_end;
+      while (k_end < GE && (int)((int64_t)k_end * U / GE) < bh_end) ++k_end;
       const int n_later = k_end - blockIdx.x - 1;
       if (tid < C) {
         float Mr = M, L = scratch[kAttnWarps * (C + 2) + C], A = scratch[kAttnWarps * (C + 2) + tid];
@@ -590,32 +596,40 @@ __global__ void __launch_bounds__(256) attn_dense_kernel(const float* __restrict
 // ---------------------------------------------------------------------------
 // dispatch
 
+// the per-tensor half of the fast-path test (K and V are checked separately)
+static bool attn_fast_tensor_ok(const Geom& g, const VqbTensor* t) {
+  if (t->layout != VQB_LAYOUT_KV_IL || t->codebook_dtype != VQB_F16) return false;
+  if (g.sharing != VQB_SHARE_CHANNEL_GROUP || g.group_width != g.v || g.R != 1 || g.bits != 8) return false;
+  if (!(g.v == 2 || g.v == 4) || !(g.gpr == 32 || g.gpr == 64)) return false;
+  if (g.v * g.gpr > 128) return false;  // C <= 128: books fit the 64 KB regions
+  return g.ndim == 4 && g.dims[2] % 32 == 0;
+}
+
 static bool attn_fast_ok(const Geom& gk, const Geom& gv, const VqbTensor* k, const VqbTensor* v, int T,
                          const VqbLaunch* L) {
   if (L && (L->flags & VQB_FLAG_FORCE_GENERIC)) return false;
-  if (k->layout != VQB_LAYOUT_KV_IL || v->layout != VQB_LAYOUT_KV_IL) return false;
-  if (k->codebook_dtype != VQB_F16 || v->codebook_dtype != VQB_F16) return false;
-  for (const Geom* g : {&gk, &gv}) {
-    if (g->sharing != VQB_SHARE_CHANNEL_GROUP || g->group_width != g->v || g->R != 1 || g->bits != 8) return false;
-    if (!(g->v == 2 || g->v == 4) || !(g->gpr == 32 || g->gpr == 64)) return false;
-    if (g->v * g->gpr > 128) return false;  // C <= 128: books fit the 64 KB regions
-  }
+  if (!attn_fast_tensor_ok(gk, k) || !attn_fast_tensor_ok(gv, v)) return false;
   if (gk.v != gv.v || T % 32 != 0) return false;
-  return true;
+  return kAttnSlotOffset + (int64_t)sm_count() * (gk.cols + 2) * 8 <= VQB_WS_COUNTER_BYTES;
 }
 
 static int64_t a256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
-int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH) {
+static int64_t attn_generic_ws(const Geom& g, int64_t BH) {
+  const int64_t T = g.dims[2], C = g.cols;
+  return VQB_WS_COUNTER_BYTES + a256(2 * BH * T * C * 4) + BH * T * 4;
+}
+
+// Path-aware: the fast kernel needs only the self-resetting counter/slot head; the
+// generic path dense fp32 K + V + logits. Sized from K (V is expected in the same
+// format; a mismatching V that forces the generic path fails with ECAPACITY).
+int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH, const VqbLaunch* L) {
   Geom g;
   int s = make_geom(k, &g);
   if (s) return s;
-  const int64_t T = g.dims[2], C = g.cols;
-  const int64_t NT = ceil_div(T, kAttnChunk);
-  (void)NT;
-  const int64_t fast = VQB_WS_COUNTER_BYTES;
-  const int64_t generic = VQB_WS_COUNTER_BYTES + a256(2 * BH * T * C * 4) + BH * T * 4;
-  return std::max(fast, generic);
+  const bool fast = !(L && (L->flags & VQB_FLAG_FORCE_GENERIC)) && attn_fast_tensor_ok(g, k) &&
+                    kAttnSlotOffset + (int64_t)sm_count() * (g.cols + 2) * 8 <= VQB_WS_COUNTER_BYTES;
+  return fast ? (int64_t)VQB_WS_COUNTER_BYTES : attn_generic_ws(g, BH);
 }
 
 template <int V, int GPL>
@@ -655,11 +669,10 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
   if (q_dtype < VQB_F32 || q_dtype > VQB_BF16 || out_dtype < VQB_F32 || out_dtype > VQB_BF16)
     return set_error(VQB_ECONFIG, "unknown query/output dtype");
   const int64_t BH = (int64_t)B * H;
-  const int64_t need = attn_ws_bytes(k, BH);
+  const bool fast = attn_fast_ok(gk, gv, k, v, T_cap, L);
+  const int64_t need = fast ? (int64_t)VQB_WS_COUNTER_BYTES : attn_generic_ws(gk, BH);
   if ((int64_t)ws_bytes < need || !ws)
     return set_error(VQB_ECAPACITY, "attention workspace too small: %zu < %lld", ws_bytes, (long long)need);
-  const bool fast = attn_fast_ok(gk, gv, k, v, T_cap, L) &&
-                    kAttnSlotOffset + (int64_t)sm_count() * (C + 2) * 8 <= VQB_WS_COUNTER_BYTES;
   if (used_fast) *used_fast = fast;
   if (!fast && d_len)
     return set_error(VQB_ECONFIG, "a device-resident KV length needs the fast attention configuration");

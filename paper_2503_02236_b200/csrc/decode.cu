@@ -15,6 +15,18 @@
 
 namespace vqb {
 
+// Set (bit 0) when a KV append finds its write position outside [0, capacity):
+// the write is skipped instead of landing in the next head's token rows; the host
+// reads and clears it with vqb_take_device_error.
+__device__ unsigned int g_append_oob = 0;
+
+__device__ __forceinline__ bool append_pos_ok(int pos, int64_t cap) {
+  if (pos >= 0 && pos < cap) return true;
+  atomicOr(&g_append_oob, 1u);
+  return false;
+}
+
+
 // ---------------------------------------------------------------------------
 // RMSNorm (Llama): h = x + residual (residual updated in place), out = w * norm(h);
 // statistics in fp32 like the HF reference implementation.
@@ -277,6 +289,7 @@ __global__ void __launch_bounds__(256) cq_quantize_kernel(Geom g, void* __restri
   const int b = (int)(rest / H);
   const int p0 = d_len ? __ldg(d_len) - n_tok : tok0;  // decode: the rows end at the current length
   const int tok = p0 + t;
+  if (!append_pos_ok(tok, g.d_T)) return;
   const XT* xp = x + b * xs_b + h * xs_h + t * xs_t + gi * V;
   // sub-vector index in the reference's row-major order over (B, H, T_cap, C)
   const int64_t row = ((int64_t)b * H + h) * g.d_T + tok;
@@ -330,6 +343,7 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
   const bool is_k = role < G;
   const Geom& g = is_k ? gk : gv;
   const int gi = is_k ? role : role - G;
+  if (!append_pos_ok(pos, g.d_T)) return;
   const int64_t s = (((int64_t)b * H + h) * g.d_T + pos) * G + gi;
   with_v(g.v, [&](auto vc) {
     constexpr int VV = decltype(vc)::value;
@@ -389,6 +403,7 @@ __global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* _
   const int hg = (int)(is_k ? w : w - H * G);
   const int h = hg / G, gi = hg % G;
   const Geom& g = is_k ? gk : gv;
+  if (!append_pos_ok(pos, g.d_T)) return;
   const __half* book = (is_k ? kbooks : vbooks) + (int64_t)(h * G + gi) * 256 * 2;  // region = h*G + gi
   float4* bk = books_s[wl];
   float cmax2 = 0.f;
@@ -591,6 +606,14 @@ extern "C" int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, in
                             reinterpret_cast<const __half*>(d_gate_up), reinterpret_cast<__half*>(d_out), rows, ffn));
   VQB_LAUNCH_CHECK("silu_mul_kernel");
   set_kernel("silu_mul");
+  return VQB_OK;
+}
+
+extern "C" int vqb_take_device_error(int32_t* out) {
+  unsigned int v = 0, zero = 0;
+  VQB_CUDA_CHECK(cudaMemcpyFromSymbol(&v, vqb::g_append_oob, sizeof(v)));
+  VQB_CUDA_CHECK(cudaMemcpyToSymbol(vqb::g_append_oob, &zero, sizeof(zero)));
+  if (out) *out = (int32_t)v;
   return VQB_OK;
 }
 

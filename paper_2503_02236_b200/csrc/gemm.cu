@@ -461,10 +461,16 @@ template <int CBYTES, int R, bool BF16, typename OutT>
 static int launch_gemm_t(const CUtensorMap& map, const GemmArgs& a, int grid, cudaStream_t st) {
   auto kern = gemm_tc_kernel<CBYTES, R, BF16, OutT>;
   const size_t smem = gemm_smem(R);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-  if (attr_err != cudaSuccess) return cuda_error(attr_err, "cudaFuncSetAttribute(gemm_tc_kernel)");
+  // the attribute is per device: one guard per device ordinal
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64] = {};
+  int dev = 0;
+  VQB_CUDA_CHECK(cudaGetDevice(&dev));
+  dev &= 63;
+  std::call_once(once[dev], [&] {
+    attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr_err[dev] != cudaSuccess) return cuda_error(attr_err[dev], "cudaFuncSetAttribute(gemm_tc_kernel)");
   kern<<<grid, kGemmThreads, smem, st>>>(map, a);
   VQB_LAUNCH_CHECK("gemm_tc_kernel");
   if (a.splits > 1) {

@@ -20,8 +20,10 @@ from dataclasses import dataclass
 import torch
 
 from .codec import Sharing, VQConfig
-from .device import DeviceVQTensor
+from . import _native as N
 from . import ops
+from .device import DeviceVQTensor
+from .errors import CapacityError
 
 
 @dataclass(frozen=True)
@@ -67,6 +69,9 @@ class VQLlamaDecoder:
         self.res = torch.zeros((batch, shape.hidden), dtype=torch.float16, device=self.device)
         self.logits = None
         self._graph = None
+        self.length = 0  # host mirror of d_len (the step advances both)
+        self.ws = ops.Workspace(self.device)  # private arena the captured graph keeps alive
+        self.capacity = min(L.k_cache.shape[2] for L in self.layers) if self.layers else 0
 
     # -- construction -------------------------------------------------------------------------
 
@@ -116,6 +121,10 @@ class VQLlamaDecoder:
 
         VQB_DECODE_SKIP (comma list of norm, linear, front, attn, silu) drops stages
         for time attribution only — the output is then meaningless."""
+        with ops.use_workspace(self.ws):
+            return self._step()
+
+    def _step(self) -> torch.Tensor:
         skip = set(filter(None, os.environ.get("VQB_DECODE_SKIP", "").split(",")))
         if skip:
             return self._step_ablated(skip)
@@ -179,7 +188,7 @@ class VQLlamaDecoder:
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         saved_len, saved_tok = self.d_len.clone(), self.tokens.clone()
-        with torch.cuda.stream(s):
+        with torch.cuda.stream(s), ops.use_workspace(self.ws):
             self.step()
             self.d_len.copy_(saved_len)
             self.tokens.copy_(saved_tok)
@@ -191,11 +200,34 @@ class VQLlamaDecoder:
         torch.cuda.current_stream(self.device).wait_stream(s)
         self._graph = g
 
+    def _advance(self) -> None:
+        """A step writes the new token's K/V rows at position `length`: refuse
+        to step past the cache capacity (the kernels would skip the write and flag
+        the device error word)."""
+        if self.length + 1 > self.capacity:
+            raise CapacityError(f"KV cache full: {self.length} tokens cached, capacity {self.capacity}")
+        self.length += 1
+
     def replay(self) -> None:
         if self._graph is None:
             self.capture()
+        self._advance()
         self._graph.replay()
+
+    def run_step(self) -> torch.Tensor:
+        """One eager (uncaptured) step with the capacity check."""
+        self._advance()
+        return self.step()
 
     def set_length(self, n: int) -> None:
         """Pretend n tokens are already cached (benchmarks at a fixed context)."""
-        self.d_len.fill_(int(n))
+        n = int(n)
+        if n < 0 or n >= self.capacity:
+            raise CapacityError(f"length {n} outside [0, {self.capacity}) of the KV cache")
+        self.d_len.fill_(n)
+        self.length = n
+
+    def check_device_errors(self) -> None:
+        """Raise if any KV append since the last check fell outside the cache."""
+        if N.take_device_error() & 1:
+            raise CapacityError("a KV append position fell outside the cache capacity (write skipped)")

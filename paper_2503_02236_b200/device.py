@@ -54,6 +54,40 @@ def default_device(device=None) -> torch.device:
     return torch.device(device)
 
 
+def stack_codebooks(q) -> np.ndarray:
+    """All of ``q``'s books as one (R * n_regions, K, v) fp32 array, level-major
+    (book index ``level * n_regions + region``, codec.py:208-209).
+
+    Uses only the attributes vqforge's own ``QuantizedTensor`` has (``codebooks``,
+    a list of ``Codebook`` with ``.entries``; pkg/src/vqforge/codec.py:180-197), so
+    the reference's objects upload unchanged."""
+    books = getattr(q, "codebooks", None)
+    if not books:
+        raise ConfigError("quantized tensor has no codebooks")
+    return np.ascontiguousarray(np.stack([np.asarray(cb.entries, dtype=np.float32) for cb in books]))
+
+
+def host_codes(q) -> tuple:
+    """(codes narrowed to u8/u16 as a byte array, largest code) of a host quantized
+    tensor, range-checked with the reference's CodeRangeError message
+    (codec.py:401-405). Accepts vqforge's QuantizedTensor (int32 ``codes`` (R, S))."""
+    cfg = q.config
+    k = cfg.n_entries
+    codes = np.asarray(q.codes)
+    hi = -1
+    if codes.size:
+        lo, hi = int(codes.min()), int(codes.max())
+        if lo < 0 or hi >= k:
+            for r in range(codes.shape[0]):
+                row = codes[r]
+                bad = row[(row < 0) | (row >= k)]
+                if bad.size:
+                    raise CodeRangeError(
+                        f"code out of range: {int(bad[0])} not in [0, {k}) at residual level {r}")
+    narrow = np.uint8 if cfg.log2_entries <= 8 else np.uint16
+    return np.ascontiguousarray(codes.astype(narrow)).view(np.uint8), hi
+
+
 def auto_layout(shape, config: VQConfig) -> str:
     """Pick the interleaved layout the fast kernels read, else ``plain``."""
     b = config.log2_entries
@@ -83,22 +117,9 @@ class DeviceVQTensor:
                        layout: str = "auto") -> "DeviceVQTensor":
         dev = default_device(device)
         cfg = q.config
-        k = cfg.n_entries
-        codes = q.codes
-        hi = -1
-        if codes.size:
-            lo, hi = int(codes.min()), int(codes.max())
-            if lo < 0 or hi >= k:
-                for r in range(cfg.residuals):
-                    row = codes[r]
-                    bad = row[(row < 0) | (row >= k)]
-                    if bad.size:
-                        raise CodeRangeError(
-                            f"code out of range: {int(bad[0])} not in [0, {k}) at residual level {r}")
-        narrow = np.uint8 if cfg.log2_entries <= 8 else np.uint16
-        host = np.ascontiguousarray(codes.astype(narrow))
-        t = torch.from_numpy(host.view(np.uint8)).to(dev)
-        books = torch.from_numpy(q.stacked_entries()).to(dev).to(torch_dtype(codebook_dtype)).contiguous()
+        host, hi = host_codes(q)
+        t = torch.from_numpy(host).to(dev)
+        books = torch.from_numpy(stack_codebooks(q)).to(dev).to(torch_dtype(codebook_dtype)).contiguous()
         plain = cls(cfg, tuple(q.shape), q.n_regions, t, "plain", books, hi)
         if layout == "auto":
             layout = auto_layout(q.shape, cfg)

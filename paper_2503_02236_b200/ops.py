@@ -6,24 +6,59 @@ reference: weights W (M, N) with y = x @ W (pkg/src/vqforge/sim.py:136-144);
 attention q (B, H, C) with K, V (B, H, T, C) (sim.py:145-155).
 """
 
+import contextlib
 import threading
 
 import torch
 
 from . import _native as N
 from .device import DeviceVQTensor, dtype_enum, torch_dtype
-from .errors import ConfigError, ShapeError
+from .errors import CapacityError, ConfigError, ShapeError
 
 # -- workspace arena ----------------------------------------------------------------------------
 # One zero-initialised byte buffer per (device, stream). The kernels keep split
-# arrival counters in its head and reset them themselves, so it is zeroed only
-# when (re)allocated.
+# arrival counters / tagged slots in its head and reset them themselves, so it is
+# zeroed only when (re)allocated. Objects that capture CUDA graphs must not use
+# the shared arena (a later, larger request would free the buffer a graph baked in,
+# and two graphs sharing one slot head must never replay concurrently): they own a
+# ``Workspace`` and route their ops to it with ``use_workspace``.
 
 _ws = {}
 _ws_lock = threading.Lock()
+_tls = threading.local()
+
+
+class Workspace:
+    """A private, growable zeroed arena for one graph-owning object (decoder, stack)."""
+
+    def __init__(self, device, nbytes: int = 1 << 20):
+        self.device = torch.device(device)
+        self.buf = torch.zeros(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=self.device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf.numel() < nbytes:
+            if torch.cuda.is_current_stream_capturing():
+                raise CapacityError(f"private workspace of {self.buf.numel()} B cannot grow to {nbytes} B "
+                                    "during graph capture (run the step once eagerly first)")
+            self.buf = torch.zeros(max(int(nbytes), 2 * self.buf.numel()), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+@contextlib.contextmanager
+def use_workspace(ws: Workspace):
+    """Every op on this thread takes its workspace from ``ws`` inside the block."""
+    prev = getattr(_tls, "ws", None)
+    _tls.ws = ws
+    try:
+        yield ws
+    finally:
+        _tls.ws = prev
 
 
 def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    own = getattr(_tls, "ws", None)
+    if own is not None and own.device == torch.device(device):
+        return own.get(nbytes)
     stream = torch.cuda.current_stream(device).cuda_stream
     key = (device.index, stream)
     with _ws_lock:

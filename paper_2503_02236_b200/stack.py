@@ -10,7 +10,7 @@ import torch
 
 from . import _native as N
 from .device import DeviceVQTensor, dtype_enum
-from .ops import launch_struct, workspace
+from .ops import Workspace, launch_struct
 
 
 class VQLinearStack:
@@ -37,7 +37,8 @@ class VQLinearStack:
         lib = N.lib()
         need = max(N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMV, s, rows, L))
                    for s, L in zip(self._structs, self.launches))
-        self._ws = workspace(need, self.device)
+        # private arena: the graph bakes its pointer in (never the shared per-stream one)
+        self._ws = Workspace(self.device, need).buf
         self._graph = None
 
     @property
@@ -67,9 +68,6 @@ class VQLinearStack:
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
-            self.launch_all()
-            # the side stream needs its own workspace: rebind to the graph stream's arena
-            self._ws = workspace(self._ws.numel(), self.device)
             self.launch_all()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):

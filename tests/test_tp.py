@@ -13,6 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 from conftest import Case, O
+from paper_2503_02236_b200.device import stack_codebooks
 
 
 def _free_port():
@@ -26,7 +27,7 @@ def _free_port():
 def _dense(q):
     regs = O.region_ids(q.shape, q.config.vector_size, q.config.sharing.kind,
                         (q.config.sharing.tile_rows, q.config.sharing.tile_cols), q.config.sharing.group_width)
-    return O.dequantize(q.codes, q.stacked_entries(), q.shape, q.config.vector_size, q.n_regions, regs)
+    return O.dequantize(q.codes, stack_codebooks(q), q.shape, q.config.vector_size, q.n_regions, regs)
 
 
 def _oracle_linear(w, x):
