@@ -105,12 +105,13 @@ def ncu_traffic():
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        return json.load(f).get("gemv_fast")
+        return json.load(f).get("gemv_group")
 
 
 def roofline(achieved_gbs, peak, src, kern, kernel_us, per_linear):
-    """The step is 128 gemv_fast launches and nothing else, so the per-launch average
-    is algorithmic step bytes / step time; the per-linear graphs break it down."""
+    """At N=1 the step is ONE gemv_group launch and nothing else, so the kernel's
+    achieved bandwidth is algorithmic step bytes / its CUDA-event time; traffic is
+    that launch's DRAM bytes from the committed ncu --set full capture."""
     t = ncu_traffic()
     return {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s", "frac": achieved_gbs / peak,
             "traffic": t["dram_bytes"] if t else None,
@@ -132,11 +133,12 @@ def dist_env():
 _CPU_CASE = {}
 
 
-def cpu_sample(seconds_budget=12.0):
+def cpu_sample(seconds_budget=12.0, threads=None):
     """The reference algorithm (dequantize, V/codec.py:391-408, then the fp32 matmul of
-    reference_compute, V/sim.py:136-144) restated in C with OpenMP on all host cores, on one
-    4096x4096 q_proj of the workload config, repeated for ~seconds_budget.
-    Returns (GB/s over the same algorithmic bytes, sample description, threads)."""
+    reference_compute, V/sim.py:136-144) restated in C with OpenMP on the host cores
+    (all of them, or `threads`), on one 4096x4096 q_proj of the workload config,
+    repeated for ~seconds_budget. Returns (GB/s over the same algorithmic bytes,
+    sample description, threads)."""
     from oracle import c_oracle as C
     from oracle import vq_oracle as O
 
@@ -144,18 +146,23 @@ def cpu_sample(seconds_budget=12.0):
     if not _CPU_CASE:
         codes, books = O.synthetic_codes_books((m, n), v, 16, 1, 1, 0, working_entries=WORK)
         _CPU_CASE.update(codes=codes, books=books, regions=np.zeros(m * n // v, dtype=np.int32),
-                         x=O.synthetic_tensor((m,), 2))
+                         x=O.synthetic_tensor((m,), 2), all=C.threads())
     c = _CPU_CASE
+    C.set_threads(threads or c["all"])
     reps, t0 = 0, time.perf_counter()
-    while True:
-        C.gemv(c["codes"], c["books"], (m, n), v, 1, c["regions"], c["x"])
-        reps += 1
-        if time.perf_counter() - t0 > seconds_budget or reps >= 2000:
-            break
+    try:
+        while True:
+            C.gemv(c["codes"], c["books"], (m, n), v, 1, c["regions"], c["x"])
+            reps += 1
+            if time.perf_counter() - t0 > seconds_budget or reps >= 2000:
+                break
+        used = C.threads()
+    finally:
+        C.set_threads(c["all"])
     dt = (time.perf_counter() - t0) / reps
     gbs = algorithmic_bytes(m, n) / dt / 1e9
-    return gbs, (f"C/OpenMP oracle (dequantize + fp32 matmul) of one 4096x4096 quip2 q_proj, {reps} reps, "
-                 f"{dt*1e3:.2f} ms each"), C.threads()
+    return gbs, (f"C/OpenMP oracle (dequantize + fp32 matmul) of one 4096x4096 quip2 q_proj, {used} thread(s), "
+                 f"{reps} reps, {dt*1e3:.2f} ms each"), used
 
 
 def run_reference(args):
@@ -185,7 +192,19 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------------------------------
 
-def build_stack(torch, dev, rank=0, world=1):
+# Megatron-style tensor parallelism of the decode linears: qkv and
+# gate_up column-parallel (N / tp, outputs stay local for attention / SiLU), o and
+# down row-parallel (M / tp, partial outputs all-reduced)
+TP_KIND = {"qkv": "col", "o": "row", "gate_up": "col", "down": "row"}
+
+
+def shard_shape(name, m, n, world):
+    return (m, n // world) if TP_KIND[name] == "col" else (m // world, n)
+
+
+def build_stack(torch, dev, rank=0, world=1, grouped=True):
+    """The step's 32 x 4 linears (this rank's TP shards) as a VQLinearStack;
+    grouped=True runs them as one persistent grouped GEMV launch."""
     from paper_2503_02236_b200.codec import VQConfig
     from paper_2503_02236_b200.device import DeviceVQTensor
     from paper_2503_02236_b200.stack import VQLinearStack
@@ -193,21 +212,19 @@ def build_stack(torch, dev, rank=0, world=1):
     cfg = VQConfig(8, 16, 1)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
-    weights, bytes_per = [], []
+    weights, bytes_per, names = [], [], []
     for _layer in range(N_LAYERS):
-        for _name, m, n in LLAMA7B:
-            # a rank's column shard, padded up to whole 256-column blocks of the fast
-            # GEMV (gate_up / 4 and / 8 are not); only the real n / world columns'
-            # bytes are credited to the metric
-            n_loc = -(-(n // world) // 256) * 256
-            s = m * n_loc // 8
-            codes = torch.randint(0, WORK, (1, s), generator=g, device=dev, dtype=torch.int32)
+        for name, m, n in LLAMA7B:
+            ms, ns = shard_shape(name, m, n, world)
+            codes = torch.randint(0, WORK, (1, ms * ns // 8), generator=g, device=dev, dtype=torch.int32)
             books = (torch.randn((1, 1 << 16, 8), generator=g, device=dev) * 0.1).half()
-            w = DeviceVQTensor.from_device_codes(codes, (m, n_loc), cfg, books, layout="plain").relayout("gemv")
+            w = DeviceVQTensor.from_device_codes(codes, (ms, ns), cfg, books, layout="plain").relayout("gemv")
             weights.append(w)
-            bytes_per.append(algorithmic_bytes(m, n // world))
-    stack = VQLinearStack(weights, rows=1)
+            names.append(name)
+            bytes_per.append(algorithmic_bytes(ms, ns))
+    stack = VQLinearStack(weights, rows=1, grouped=grouped)
     stack.x.copy_((torch.randn(stack.x.shape, generator=g, device=dev)).half())
+    stack.names = names
     return stack, bytes_per
 
 
@@ -357,6 +374,135 @@ def time_decode(torch, dev, batch=1, ctx=4096, reps=10):
             "ms_per_step": ms, "tokens_per_s": batch * 1e3 / ms, "data": "synthetic weights/KV (random init)"}
 
 
+def tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 2250.0, 2250.0, "fallback (nominal dense bf16)"
+
+
+def _weights(torch, dev, cfg, shape, copies, work, seed):
+    from paper_2503_02236_b200.codec import region_count
+    from paper_2503_02236_b200.device import DeviceVQTensor
+    m, n = shape
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    nreg = region_count(shape, cfg)
+    out = []
+    for _ in range(copies):
+        codes = torch.randint(0, work or cfg.n_entries, (cfg.residuals, m * n // cfg.vector_size), generator=g,
+                              device=dev, dtype=torch.int32)
+        books = (torch.randn((cfg.residuals * nreg, cfg.n_entries, cfg.vector_size), generator=g, device=dev)
+                 * 0.1).half()
+        out.append(DeviceVQTensor.from_device_codes(codes, shape, cfg, books).relayout("gemv"))
+    return out
+
+
+def time_gemm(torch, dev, N, label, cfg, shapes, rows=1024, work=None, copies=4):
+    """Prefill GEMM y = X @ dequant(W) (rows x M x N, tcgen05) per shape and in total,
+    CUDA-graph replays over `copies` distinct weights, against dense fp16 cuBLAS at
+    the same shape; tensor-pipe roofline = flops / time vs MEASURED_PEAKS bf16 (burst,
+    the kernel is timed alone)."""
+    from paper_2503_02236_b200.ops import launch_struct, workspace
+    peak, _, src = tensor_peak()
+    lib = N.lib()
+    res, tot_flops, tot_us, tot_dense = {}, 0.0, 0.0, 0.0
+    for name, m, n in shapes:
+        ws = _weights(torch, dev, cfg, (m, n), copies, work, 21)
+        x = torch.randn((rows, m), device=dev).half()
+        ys = [torch.empty((rows, n), device=dev, dtype=torch.float16) for _ in ws]
+        L = launch_struct()
+        structs = [w.struct() for w in ws]
+        need = max(N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMM, st, rows, L)) for st in structs)
+        buf = workspace(need, dev)
+
+        def run():
+            st_ = torch.cuda.current_stream(dev).cuda_stream
+            for st, y in zip(structs, ys):
+                N.check(lib.vqb_gemm(st, x.data_ptr(), N.F16, rows, y.data_ptr(), N.F16, L, buf.data_ptr(),
+                                     buf.numel(), st_))
+
+        us = graph_time(torch, run, 10) / len(ws)
+        kern = N.last_kernel()
+        dense = [torch.randn((m, n), device=dev, dtype=torch.float16) for _ in range(copies)]
+        outs = [torch.empty((rows, n), device=dev, dtype=torch.float16) for _ in dense]
+
+        def run_dense():
+            for d, o in zip(dense, outs):
+                torch.matmul(x, d, out=o)
+
+        dus = graph_time(torch, run_dense, 10) / len(dense)
+        flops = 2.0 * rows * m * n
+        res[name] = {"shape": [rows, m, n], "kernel": kern, "us_per_call": round(us, 2),
+                     "TFLOP_s": round(flops / us / 1e6, 1), "frac": round(flops / us / 1e6 / peak, 3),
+                     "fp16_cublas_us": round(dus, 2), "fp16_cublas_TFLOP_s": round(flops / dus / 1e6, 1),
+                     "speedup_vs_fp16": round(dus / us, 3)}
+        tot_flops += flops
+        tot_us += us
+        tot_dense += dus
+        del ws, dense, outs, ys
+        torch.cuda.empty_cache()
+    return {"config": label, "rows": rows, "per_linear": res,
+            "roofline": {"bound": "tensor", "achieved": round(tot_flops / tot_us / 1e6, 1), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(tot_flops / tot_us / 1e6 / peak, 3),
+                         "peak_source": f"{src} bf16 burst (kernel timed alone)"},
+            "fp16_cublas_TFLOP_s": round(tot_flops / tot_dense / 1e6, 1),
+            "speedup_vs_fp16": round(tot_dense / tot_us, 3)}
+
+
+def time_gemv_shapes(torch, dev, N, cfg, shapes, work=None, rows=1):
+    """Per-call fused GEMV (batch `rows`) per shape: graph replays over > L2 of distinct
+    weights, HBM roofline on the algorithmic bytes, dense fp16 cuBLAS at equal shape."""
+    from paper_2503_02236_b200.stack import VQLinearStack
+    hbm, _ = peaks()
+    out = {}
+    for name, m, n in shapes:
+        code_bytes = cfg.residuals * (m * n // cfg.vector_size) * cfg.log2_entries // 8
+        copies = max(2, min(48, (256 << 20) // code_bytes + 1))
+        ws = _weights(torch, dev, cfg, (m, n), copies, work, 31)
+        sub = VQLinearStack(ws, rows=rows)
+        sub.x.copy_(torch.randn(sub.x.shape, device=dev).half())
+        us = graph_time(torch, sub.launch_all, 10) / len(ws)
+        kern = N.last_kernel()
+        alg = ws[0].algorithmic_bytes(work) + rows * (m + n) * 2
+        dense = [torch.randn((m, n), device=dev, dtype=torch.float16)
+                 for _ in range(max(2, (512 << 20) // (m * n * 2) + 1))]
+        xd = torch.randn((rows, m), device=dev).half()
+        outs = [torch.empty((rows, n), device=dev, dtype=torch.float16) for _ in dense]
+
+        def run_dense():
+            for d, o in zip(dense, outs):
+                torch.matmul(xd, d, out=o)
+
+        dus = graph_time(torch, run_dense, 10) / len(dense)
+        out[name] = {"shape": [m, n], "rows": rows, "kernel": kern, "us_per_call": round(us, 2),
+                     "alg_bytes": alg, "GB_s": round(alg / us / 1e3, 1), "frac": round(alg / us / 1e3 / hbm, 3),
+                     "fp16_cublas_us": round(dus, 2), "speedup_vs_fp16": round(dus / us, 2)}
+        del ws, sub, dense, outs
+        torch.cuda.empty_cache()
+    return out
+
+
+LLAMA65B = [("q", 8192, 8192), ("up", 8192, 22016), ("down", 22016, 8192)]
+
+
+def time_c3(torch, dev, N):
+    """C3: AQLM 2x8 (VQConfig(8, 8, 2)) at Llama-65B shapes — GEMV batch 1 at the
+    per-GPU shard of tensor parallelism 1/2/4/8 (column-parallel q/up: N/tp,
+    row-parallel down: M/tp), and the prefill GEMM (rows 1024) at TP1."""
+    from paper_2503_02236_b200.codec import VQConfig
+    cfg = VQConfig(8, 8, 2)
+    gemv = {}
+    for tp in (1, 2, 4, 8):
+        shapes = [("q", 8192, 8192 // tp), ("up", 8192, 22016 // tp), ("down", 22016 // tp, 8192)]
+        gemv[f"tp{tp}"] = time_gemv_shapes(torch, dev, N, cfg, shapes)
+    gemm = time_gemm(torch, dev, N, "C3 aqlm2x8 VQ<8,8,2> llama65b prefill rows 1024", cfg, LLAMA65B, copies=2)
+    return {"config": "C3 aqlm2x8 VQ<8,8,2> whole, llama65b q/up/down", "gemv_b1_per_gpu_shard": gemv,
+            "gemm_rows1024_tp1": gemm}
+
+
 def run_impl(args):
     import torch
     import torch.distributed as dist
@@ -371,15 +517,16 @@ def run_impl(args):
     from paper_2503_02236_b200 import _native as N
     from paper_2503_02236_b200 import ops
 
-    stack, bytes_per = build_stack(torch, dev, rank, world)
+    stack, bytes_per = build_stack(torch, dev, rank, world, grouped=True)
     step_bytes = sum(bytes_per)
-    stream = torch.cuda.current_stream(dev)
+    from paper_2503_02236_b200.stack import VQLinearStack
+    single = VQLinearStack(stack.weights, rows=1)  # one gemv_fast launch per linear
+    single.x.copy_(stack.x)
 
     # per-linear kernel times: CUDA-graph replays of one linear's GEMV over 32 layers'
     # distinct weights (> L2), CUDA events on the replaying stream
     per_linear = {}
     if not args.no_extra and world == 1:
-        from paper_2503_02236_b200.stack import VQLinearStack
         for li, (name, m, n) in enumerate(LLAMA7B):
             ws_ = [stack.weights[layer * len(LLAMA7B) + li] for layer in range(N_LAYERS)]
             sub = VQLinearStack(ws_, rows=1)
@@ -394,28 +541,29 @@ def run_impl(args):
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / (10 * N_LAYERS)
-            alg = algorithmic_bytes(m, n // world)
-            per_linear[name] = {"shape": [m, n // world], "us_per_call": round(us, 2), "alg_bytes": alg,
+            alg = algorithmic_bytes(m, n)
+            per_linear[name] = {"shape": [m, n], "us_per_call": round(us, 2), "alg_bytes": alg,
                                 "GB_s": round(alg / us / 1e3, 1)}
             del sub
-    kern = "gemv_fast"
 
-    stack.capture()
-    for _ in range(max(args.warmup, 3)):
-        stack.replay()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    # tensor parallelism: every rank holds N/world columns of every linear; the step
-    # ends with the column all-gather of all outputs (NCCL over NVLink)
-    gathered = torch.empty(world * stack.y.numel(), dtype=stack.y.dtype, device=dev) if world > 1 else None
+    # tensor parallelism: the row-parallel linears' partial outputs are all-reduced,
+    # one NCCL collective per row-parallel linear (64 per step), as a TP decode step does
+    row_views = [stack.output_view(i) for i, nm in enumerate(stack.names) if TP_KIND[nm] == "row"]
+
+    def collectives():
+        if world > 1:
+            for v in row_views:
+                dist.all_reduce(v)
 
     def step():
         stack.replay()
-        if gathered is not None:
-            dist.all_gather_into_tensor(gathered, stack.y)
+        collectives()
 
-    for _ in range(max(args.warmup, 1)):
+    stack.launch_all()
+    kern = N.last_kernel()  # the headline kernel (gemv_group)
+    stack.capture()
+    single.capture()
+    for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -429,25 +577,40 @@ def run_impl(args):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    # the same step as a chain of 128 single-linear launches (the per-call kernel a
+    # decode loop with dependencies between linears uses)
+    for _ in range(3):
+        single.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        single.replay()
+        collectives()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_single = e0.elapsed_time(e1) / args.steps
+    diff = float((single.y.float() - stack.y.float()).abs().max()) if world == 1 else None
     # e2e through the public API with pinned host buffers
     hx = torch.empty(stack.x.shape, dtype=stack.x.dtype, pin_memory=True)
     hx.copy_(stack.x)
     hy = torch.empty(stack.y.shape, dtype=stack.y.dtype, pin_memory=True)
     for _ in range(max(args.warmup, 1)):
         stack.run(hx, hy)
+        collectives()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0.record()
     for _ in range(args.steps):
         stack.run(hx, hy)
+        collectives()
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
     clk = clocks.stop()
     if world > 1:
-        t = torch.tensor([ms, e2e_ms], device=dev)
+        t = torch.tensor([ms, e2e_ms, ms_single], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, e2e_ms = float(t[0]), float(t[1])
+        ms, e2e_ms, ms_single = float(t[0]), float(t[1]), float(t[2])
 
     if rank == 0:
         hbm, src = peaks()
@@ -456,27 +619,48 @@ def run_impl(args):
         extra = {}
         if per_linear:
             extra["per_linear"] = per_linear
+        extra["step_per_launch"] = {
+            "what": "the same step as 128 single-linear gemv_fast launches (the per-call kernel of a decode loop)",
+            "ms_per_step": ms_single, "GB_s": total_bytes / (ms_single * 1e-3) / 1e9,
+            "frac": total_bytes / (ms_single * 1e-3) / 1e9 / world / hbm, "launches_per_step": single.n_launches,
+            "max_abs_diff_vs_grouped": diff}
+        want = (lambda k: True) if not args.only else (lambda k: k in args.only.split(","))
         if not args.no_extra and world == 1:
-            from paper_2503_02236_b200.codec import Sharing
-            extra["attention_c4"] = time_attention(torch, dev, ops, N)
-            extra["gemv_c1_gptvq2_q_proj"] = time_gemv_single(
-                torch, dev, ops, N, "C1 gptvq2 VQ<4,8,1> tile256 4096x4096 b1", (4, 8, 1, Sharing.per_tile(256, 256)),
-                (4096, 4096))
-            extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 8, 16, 64)]  # BASELINE C5 sweep
-            extra["gemv_c2_quip2_q_proj"] = time_gemv_single(
-                torch, dev, ops, N, "C2 quip2 VQ<8,16,1> ws256 4096x4096 b1", (8, 16, 1, Sharing.whole_tensor()),
-                (4096, 4096), work=WORK)
+            from paper_2503_02236_b200.codec import Sharing, VQConfig
+            if want("attention_c4"):
+                extra["attention_c4"] = time_attention(torch, dev, ops, N)
+            if want("gemv_c1"):
+                extra["gemv_c1_gptvq2_q_proj"] = time_gemv_single(
+                    torch, dev, ops, N, "C1 gptvq2 VQ<4,8,1> tile256 4096x4096 b1",
+                    (4, 8, 1, Sharing.per_tile(256, 256)), (4096, 4096))
+            if want("decode_c5"):
+                extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 8, 16, 64)]  # BASELINE C5 sweep
+            if want("gemm_c2"):
+                extra["gemm_c2_prefill"] = time_gemm(
+                    torch, dev, N, "C2 quip2 VQ<8,16,1> ws256 llama7b prefill rows 1024", VQConfig(8, 16, 1),
+                    LLAMA7B, work=WORK)
+            if want("c3"):
+                extra["c3_aqlm65b"] = time_c3(torch, dev, N)
+            if want("gemv_c2"):
+                extra["gemv_c2_quip2_q_proj"] = time_gemv_single(
+                    torch, dev, ops, N, "C2 quip2 VQ<8,16,1> ws256 4096x4096 b1", (8, 16, 1, Sharing.whole_tensor()),
+                    (4096, 4096), work=WORK)
         cpu = None
         if world == 1 and not args.no_cpu:
             gbs, sample, cores = cpu_sample()
-            cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample}
+            gbs1, sample1, _ = cpu_sample(seconds_budget=6.0, threads=1)
+            cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+                   "value_1thread": gbs1, "sample_1thread": sample1, "host_cpus": os.cpu_count()}
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": "llama7b-decode-linears quip2 VQ<8,16,1> ws256 batch1",
                        "layers": N_LAYERS, "launches_per_step": stack.n_launches,
-                       "parallelism": f"tp{world}" if world > 1 else "single",
+                       "grouping": "the step's 128 independent GEMVs as one persistent stream-K launch "
+                                   "(vqb_gemv_grouped); the 128-launch chain is step_per_launch",
+                       "parallelism": (f"tp{world}: qkv/gate_up column-parallel, o/down row-parallel + one "
+                                       f"NCCL all-reduce per row-parallel linear") if world > 1 else "single",
                        "l2": "inputs 1.6 GB/GPU > L2, no flush", "graph": True},
             "us_per_call": ms * 1e3 / stack.n_launches,
             "e2e": {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
@@ -484,6 +668,7 @@ def run_impl(args):
                     "d2h_bytes_per_step": int(stack.y.numel() * stack.y.element_size()),
                     "ms_per_step": e2e_ms},
             "roofline": roofline(value / world, hbm, src, kern, ms * 1e3 / stack.n_launches, per_linear),
+            "kernel": kern,
             "cpu_baseline": cpu,
             "gpu_launches": stack.n_launches * args.steps,
             "clocks": clk,
@@ -503,6 +688,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of extra keys to time (default: all)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -172,6 +172,18 @@ int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows,
              void* d_y, int32_t y_dtype, const VqbLaunch* launch, void* d_ws,
              size_t ws_bytes, void* stream);
 
+/* Grouped decode GEMV: n independent problems y_i(rows, N_i) = x_i(rows, M_i) @
+ * dequant(W_i), all of one VQ configuration (v = 8, one level, whole-tensor
+ * books with every code < 256 resident in shared memory, GEMV_IL codes, fp16),
+ * as ONE persistent stream-K launch over the units of every problem: a step's
+ * independent linears pay one prologue / tail instead of one per linear. w points
+ * to n consecutive VqbTensor; n <= 192. No vqforge counterpart (the reference runs
+ * one fused kernel per call, sim.py:297-316); per problem the result equals
+ * vqb_gemv's. */
+int vqb_gemv_grouped(const VqbTensor* w, int32_t n, const void* const* d_xs, int32_t x_dtype, int32_t rows,
+                     void* const* d_ys, int32_t y_dtype, const VqbLaunch* launch, void* d_ws,
+                     size_t ws_bytes, void* stream);
+
 /* Prefill GEMM: y(rows, N) = x(rows, M) @ dequant(W). Dequantised W tiles are
  * written to shared memory in the UMMA canonical layout and consumed by
  * tcgen05.mma with the accumulator in TMEM. x must be fp16 or bf16 matching the

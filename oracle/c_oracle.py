@@ -28,6 +28,7 @@ def lib():
         L = ctypes.CDLL(LIB)
         P = ctypes.c_void_p
         L.vqo_threads.restype = ctypes.c_int
+        L.vqo_set_threads.argtypes = [ctypes.c_int]
         L.vqo_dequant.argtypes = [P, ctypes.c_int, ctypes.c_int64, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
         L.vqo_gemv.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int,
                                ctypes.c_int, P, P, ctypes.c_int, P]
@@ -42,6 +43,10 @@ def _p(a):
 
 def threads() -> int:
     return int(lib().vqo_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().vqo_set_threads(int(n))
 
 
 def dequantize(codes, books, shape, v, n_regions, regions):

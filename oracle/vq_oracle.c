@@ -27,6 +27,16 @@ int vqo_threads(void) {
 #endif
 }
 
+/* thread count of the following calls (the CPU baseline reports 1 thread and all cores) */
+void vqo_set_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 /* out[s*v + j] = sum over levels of books[((r*n_regions + regions[s])*K + codes[r*S + s])*v + j] */
 int vqo_dequant(const int32_t* codes, int R, int64_t S, const float* books, int K, int v, int n_regions,
                 const int32_t* regions, float* out) {

@@ -38,7 +38,7 @@ EXPORTS = (
     "vqb_abi_version", "vqb_last_error", "vqb_last_kernel", "vqb_dequant", "vqb_workspace_bytes", "vqb_gemv",
     "vqb_gemm", "vqb_attn_decode", "vqb_layout_bytes", "vqb_repack", "vqb_query_usage",
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
-    "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error",
+    "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error", "vqb_gemv_grouped",
 )
 
 
@@ -113,6 +113,7 @@ def lib():
             L.vqb_workspace_bytes.restype = i64
             L.vqb_gemv.argtypes = [T, vp, i32, i32, vp, i32, La, vp, sz, vp]
             L.vqb_gemm.argtypes = [T, vp, i32, i32, vp, i32, La, vp, sz, vp]
+            L.vqb_gemv_grouped.argtypes = [vp, i32, vp, i32, i32, vp, i32, La, vp, sz, vp]
             L.vqb_attn_decode.argtypes = [T, T, vp, i32, i32, i32, i32, i32, vp, i32, La, vp, sz, vp]
             L.vqb_attn_decode_len.argtypes = [T, T, vp, i32, i32, i32, i32, i32, vp, vp, i32, La, vp, sz, vp]
             f32 = ctypes.c_float
@@ -132,7 +133,7 @@ def lib():
             for name in ("vqb_dequant", "vqb_gemv", "vqb_gemm", "vqb_attn_decode", "vqb_repack",
                          "vqb_query_usage", "vqb_attn_decode_len", "vqb_rmsnorm", "vqb_qkv_rope",
                          "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append",
-                         "vqb_take_device_error"):
+                         "vqb_take_device_error", "vqb_gemv_grouped"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib

@@ -88,6 +88,37 @@ struct GemvFastArgs {
   unsigned long long* part;  // (grid, B, COLS) tagged partials {fp32 value, tag 1}, one slot per CTA,
                              // in the self-resetting workspace head (zeroed by the consumer)
   unsigned long long* trace;  // optional per-CTA phase timestamps (debug flag 32), 8 per CTA
+  int total_units;            // grouped launch: units over every problem of the table
+  int n_probs;                // grouped launch: problems in the table (0: the single problem above)
+};
+
+// One linear of a grouped launch (vqb_gemv_grouped): same VQ config and batch as
+// every other problem of the launch, its own codes, codebook, x and y. Units of all
+// problems form one stream-K range, so a step's independent GEMVs run as one
+// persistent kernel with no per-launch prologue / tail.
+struct GemvProblem {
+  const uint8_t* codes;
+  int64_t level_bytes;
+  const __half* books;
+  const __half* x;
+  void* y;
+  int M, N, n_cblk, n_chunks, unit_base, pad;
+};
+constexpr int kMaxGroup = 192;  // problems per grouped launch (kernel parameter table, 12 KB)
+struct GemvTable {
+  GemvProblem p[kMaxGroup];
+};
+
+// The problem a unit belongs to, seen through a forward-only cursor (CTAs walk
+// their units in order). For a single-problem launch it never moves.
+struct ProbCursor {
+  const uint8_t* codes;
+  int64_t level_bytes;
+  const __half* books;
+  const __half* x;
+  void* y;
+  int M, N, n_cblk, n_chunks, base, end, idx;
+  int last_wb;  // sub-vector groups of the (possibly narrower) last column block
 };
 
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
@@ -107,11 +138,12 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // entries become A fragments through ldmatrix.trans straight from the replicated
 // shared codebook (W^T: 16 columns x 16 rows per column pair), the activations the
 // B fragment (16 rows x 8 batch rows), fp32 accumulation.
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC>
-__global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool GROUP>
+__device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const GemvProblem* __restrict__ probs) {
   constexpr bool H2 = ACC == 1;
   constexpr bool MMA = ACC == 2;
   static_assert(!MMA || (V == 8 && WG == 1 && !GTIER && !TILE), "tensor-core GEMV: v = 8, codes in shared memory");
+  static_assert(!GROUP || (!TILE && !GTIER && R == 1), "grouped GEMV: whole-tensor books resident in shared memory");
   constexpr int kGemvWarps = gemv_warps(B, MMA);
   constexpr int kGemvThreads = kGemvWarps * 32;
   constexpr int EB = V * 2;              // fp16 entry bytes
@@ -126,7 +158,8 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   constexpr int NQ = V / 4;              // float4 per lane in the cross-warp reduction
   constexpr int RGB = GC * 16;           // bytes of one row group of a column block, per level
   constexpr int LEVB = (CR / RPL) * RGB; // bytes per level per full chunk (contiguous in GEMV_IL)
-  constexpr int NBUF = TILE ? 2 : 1;     // codebook buffers
+  constexpr bool SWITCH = TILE || GROUP; // the codebook changes inside a CTA's range
+  constexpr int NBUF = SWITCH ? 2 : 1;   // codebook buffers
   // WIDE book layout (every code < 256 is in shared memory): entry e owns a 256-byte
   // row, half h = level (R == 2) or buffer (tile double buffering) holds its
   // replicas, so a lookup address is ONE PRMT of the code byte and the lane's
@@ -151,11 +184,45 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + RED_ROWS * WM * COLS);  // full[kStages], empty[kStages]
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
 
-  const int U = a.n_cblk * a.n_chunks;
+  const int U = GROUP ? a.total_units : a.n_cblk * a.n_chunks;
   const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
   const int n = u1 - u0;
-  const int last_rows = a.M - (a.n_chunks - 1) * CR;  // rows of the (possibly partial) last chunk
+
+  // problem cursors: `fc` for the TMA feed (thread 0, runs kStages units ahead),
+  // `cc` for the compute and epilogue
+  auto load_prob = [&](ProbCursor& c, int i) {
+    if constexpr (GROUP) {
+      const GemvProblem& q = probs[i];
+      c.codes = q.codes; c.level_bytes = q.level_bytes; c.books = q.books; c.x = q.x; c.y = q.y;
+      c.M = q.M; c.N = q.N; c.n_cblk = q.n_cblk; c.n_chunks = q.n_chunks; c.base = q.unit_base;
+    } else {
+      c.codes = a.codes; c.level_bytes = a.level_bytes; c.books = a.books; c.x = a.x; c.y = a.y;
+      c.M = a.M; c.N = a.N; c.n_cblk = a.n_cblk; c.n_chunks = a.n_chunks; c.base = 0;
+    }
+    c.end = c.base + c.n_cblk * c.n_chunks;
+    c.idx = i;
+    c.last_wb = (c.N / V) - (c.n_cblk - 1) * GC;
+  };
+  auto seek = [&](ProbCursor& c, int u) {
+    if constexpr (GROUP) {
+      while (u >= c.end) load_prob(c, c.idx + 1);
+    }
+  };
+  auto first_prob = [&](int u) {
+    int lo = 0;
+    if constexpr (GROUP) {
+      int hi = a.n_probs - 1;
+      while (lo < hi) {  // last problem whose base <= u
+        const int mid = (lo + hi + 1) >> 1;
+        if (probs[mid].unit_base <= u) lo = mid; else hi = mid - 1;
+      }
+    }
+    return lo;
+  };
+  ProbCursor cc, fc;
+  load_prob(cc, first_prob(u0));
+  fc = cc;
 
   if (tid == 0) {
     trace_at(a.trace, 0);
@@ -177,28 +244,41 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   // column-blocked GEMV_IL layout, so each unit is one bulk copy per level plus one
   // per activation row. Codes do not depend on the previous kernel and are
   // requested before griddepcontrol.wait; activations only after it.
-  auto unit_rows = [&](int u) { return (u % a.n_chunks == a.n_chunks - 1) ? last_rows : CR; };
+  // rows of a unit (the last chunk of a column block may be partial) and the byte
+  // width of one row group (the last column block may be narrower than 256 columns)
+  auto unit_rows = [&](const ProbCursor& c, int u) {
+    const int chunk = (u - c.base) % c.n_chunks;
+    return chunk == c.n_chunks - 1 ? c.M - (c.n_chunks - 1) * CR : CR;
+  };
+  auto unit_rgb = [&](const ProbCursor& c, int u) {
+    return ((u - c.base) / c.n_chunks == c.n_cblk - 1) ? c.last_wb * 16 : RGB;
+  };
   auto expect = [&](int idx) {
-    const int rows = unit_rows(u0 + idx);
-    mbar_arrive_expect_tx(full0 + 8 * (idx % kStages), (uint32_t)(R * (rows / RPL) * RGB + B * rows * 2));
+    const int u = u0 + idx;
+    seek(fc, u);
+    const int rows = unit_rows(fc, u);
+    mbar_arrive_expect_tx(full0 + 8 * (idx % kStages),
+                          (uint32_t)(R * (rows / RPL) * unit_rgb(fc, u) + B * rows * 2));
   };
   auto issue_codes = [&](int idx) {
     const int s = idx % kStages, u = u0 + idx;
-    const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
-    const int rows = unit_rows(u);
-    const int64_t off = (int64_t)cb * GC * (a.M / RPL) * 16 + (int64_t)chunk * (CR / RPL) * RGB;
+    seek(fc, u);
+    const int cb = (u - fc.base) / fc.n_chunks, chunk = (u - fc.base) - cb * fc.n_chunks;
+    const int rows = unit_rows(fc, u), rgb = unit_rgb(fc, u);
+    const int64_t off = (int64_t)cb * GC * (fc.M / RPL) * 16 + (int64_t)chunk * (CR / RPL) * rgb;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      tma_load_1d(smem_u32(stages + s * STG + r * LEVB), a.codes + r * a.level_bytes + off,
-                  (uint32_t)((rows / RPL) * RGB), full0 + 8 * s);
+      tma_load_1d(smem_u32(stages + s * STG + r * LEVB), fc.codes + r * fc.level_bytes + off,
+                  (uint32_t)((rows / RPL) * rgb), full0 + 8 * s);
   };
-  auto issue_x = [&](int idx) {
+  auto issue_x = [&](ProbCursor& c, int idx) {
     const int s = idx % kStages, u = u0 + idx;
-    const int chunk = u % a.n_chunks;
-    const int rows = unit_rows(u);
+    seek(c, u);
+    const int chunk = (u - c.base) % c.n_chunks;
+    const int rows = unit_rows(c, u);
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      tma_load_1d(smem_u32(stages + s * STG + STAGEB + b * XROWB), a.x + (int64_t)b * a.M + (int64_t)chunk * CR,
+      tma_load_1d(smem_u32(stages + s * STG + STAGEB + b * XROWB), c.x + (int64_t)b * c.M + (int64_t)chunk * CR,
                   (uint32_t)(rows * 2), full0 + 8 * s);
   };
   const int pre = min(n, kStages);
@@ -214,13 +294,13 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   const int g_local = wg * 32 + lane;
 
   constexpr int MAX_PER_THREAD = (1024 + kGemvThreads - 1) / kGemvThreads;  // n_sh * R <= 1024 entries
-  auto book_issue = [&](int region, uint4 (&buf)[MAX_PER_THREAD]) {
+  auto book_issue = [&](const __half* books, int region, uint4 (&buf)[MAX_PER_THREAD]) {
 #pragma unroll
     for (int k = 0; k < MAX_PER_THREAD; ++k) {
       const int idx = tid + k * kGemvThreads;
       if (idx < R * a.n_sh) {
         const int r = idx / a.n_sh, e = idx - r * a.n_sh;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.books) +
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(books) +
                              (((int64_t)(r * a.n_regions + region) * a.K) + e) * EB;
         if constexpr (EB == 16) buf[k] = __ldg(reinterpret_cast<const uint4*>(src));
         else {
@@ -251,18 +331,19 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
   // row tile and per column tile; whole-tensor sharing has one book
   auto region_of = [&](int u) {
     if constexpr (!TILE) return 0;
-    const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;
+    const int cb = u / a.n_chunks, chunk = u - cb * a.n_chunks;  // TILE: single-problem launches only
     return (chunk * CR / a.tile_rows) * a.n_tc + (cb * COLS) / a.tile_cols;
   };
 
   {
     uint4 bb[MAX_PER_THREAD];
-    book_issue(region_of(u0), bb);
+    book_issue(cc.books, region_of(u0), bb);
     book_commit(0, bb);
   }
   pdl_wait();  // x / y / the partial workspace may belong to the previous kernel
+  ProbCursor xc = cc;  // x cursor of the prologue (thread 0)
   if (tid == 0)
-    for (int idx = 0; idx < pre; ++idx) issue_x(idx);
+    for (int idx = 0; idx < pre; ++idx) issue_x(xc, idx);
   __syncthreads();
   if (tid == 0) trace_at(a.trace, 1);
 
@@ -280,8 +361,8 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
 
   int cur_buf = 0;
   int span_first = u0;  // first unit of the current span
-  int cb = u0 / a.n_chunks;
-  int span_end = min(u1, (cb + 1) * a.n_chunks);
+  int cb = (u0 - cc.base) / cc.n_chunks;
+  int span_end = min(u1, cc.base + (cb + 1) * cc.n_chunks);
   for (int u = u0, idx = 0; u < u1; ++u, ++idx) {
     const int s = idx % kStages;
     // refill the stage unit idx-2 used with unit idx-2+kStages (thread 0 only). Lagging
@@ -293,7 +374,7 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
         mbar_wait(empty0 + 8 * (j % kStages), ((idx - 2) / kStages) & 1);
         expect(j);
         issue_codes(j);
-        issue_x(j);
+        issue_x(fc, j);
       }
       __syncwarp();
     }
@@ -301,7 +382,10 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
     bool sw = false;
     if constexpr (TILE) {
       sw = (u + 1 < u1) && region_of(u + 1) != region_of(u);
-      if (sw) book_issue(region_of(u + 1), nb);
+      if (sw) book_issue(cc.books, region_of(u + 1), nb);
+    } else if constexpr (GROUP) {
+      sw = (u + 1 < u1) && (u + 1 >= cc.end);  // the next unit is the next linear's
+      if (sw) book_issue(probs[cc.idx + 1].books, 0, nb);
     }
     mbar_wait(full0 + 8 * s, (idx / kStages) & 1);
     if (tid == 0 && idx == 0) trace_at(a.trace, 2);
@@ -309,7 +393,9 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
     const uint8_t* xs = st + STAGEB + (wm * kSlabRows) * 2;  // this warp's rows of the chunk's activations
     const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
     const int region = region_of(u);
-    const bool active = wm * kSlabRows < unit_rows(u);  // the last chunk may be partial
+    const bool active = wm * kSlabRows < unit_rows(cc, u);  // the last chunk may be partial
+    const int rgb = unit_rgb(cc, u);                        // row-group bytes (narrow last column block)
+    const int wb = rgb >> 4;                                // sub-vector groups present
     if (MMA && active) {
       // per 16-row k-block: the activations' B fragment (lane: batch row lane/4, rows
       // 2(lane%4)+{0,1}, +8), then per column pair one ldmatrix.x4.trans whose 32 row
@@ -325,13 +411,16 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
           xb1 = *reinterpret_cast<const uint32_t*>(xr + 16);
         }
         const int row = kb * 16 + (j4 >> 1) * 8 + rr;  // this lane's row of the slab
-        const uint8_t* cbase = st + (wm * LOADS + row / RPL) * RGB + (row % RPL) * CBYTES + (j4 & 1) * 16;
+        const uint8_t* cbase = st + (wm * LOADS + row / RPL) * rgb + (row % RPL) * CBYTES + (j4 & 1) * 16;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const uint8_t* cp = cbase + r * LEVB + q * 32;
-            const uint32_t code = CBYTES == 2 ? (uint32_t)*reinterpret_cast<const uint16_t*>(cp) : (uint32_t)*cp;
+            // groups past a narrow last column block hold no codes: entry 0 (never stored)
+            const uint32_t code = (2 * q + (j4 & 1) >= wb) ? 0u
+                                  : CBYTES == 2 ? (uint32_t)*reinterpret_cast<const uint16_t*>(cp) & 0xffu
+                                                : (uint32_t)*cp;
             const uint32_t addr = WIDE ? smem_u32(books_s) + (code << 8) + (R == 2 ? r : cur_buf) * 128 + rep_off
                                        : smem_u32(bsm) + (uint32_t)(r * a.n_sh * 128) + (code << 7);
             uint32_t a0, a1, a2, a3;
@@ -351,7 +440,8 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
       for (int i = 0; i < LOADS; ++i)
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          cw[i][r] = *reinterpret_cast<const uint4*>(st + r * LEVB + (wm * LOADS + i) * RGB + g_local * 16);
+          cw[i][r] = g_local < wb ? *reinterpret_cast<const uint4*>(st + r * LEVB + (wm * LOADS + i) * rgb + g_local * 16)
+                                  : make_uint4(0u, 0u, 0u, 0u);
       auto lookup = [&](int k, int r) -> const uint8_t* {
         const int i = k / RPL, kr = k % RPL;
         if constexpr (WIDE) {
@@ -372,7 +462,7 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
         bool in_smem = true;
         if constexpr (GTIER) in_smem = code < (uint32_t)a.n_sh;
         return in_smem ? bsm + (size_t)r * a.n_sh * 128 + ((size_t)code << 7)
-                       : reinterpret_cast<const uint8_t*>(a.books) +
+                       : reinterpret_cast<const uint8_t*>(cc.books) +
                              (((int64_t)(r * a.n_regions + region) * a.K) + code) * EB;
       };
       if constexpr (B >= 4 && H2) {
@@ -486,7 +576,7 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
-    if constexpr (TILE) {
+    if constexpr (SWITCH) {
       if (sw) {
         book_commit(cur_buf ^ 1, nb);  // the other buffer was released at the previous swap
         __syncthreads();
@@ -498,9 +588,9 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
     // publish a partial, or finish a split column block
     if (u + 1 == span_end) {
       if (tid == 0 && u + 1 == u1) trace_at(a.trace, 3);
-      const int cf = span_first - cb * a.n_chunks;  // first chunk of the span
-      const int cl = u - cb * a.n_chunks;           // last chunk
-      const bool whole = (cf == 0 && cl == a.n_chunks - 1);
+      const int cf = span_first - cc.base - cb * cc.n_chunks;  // first chunk of the span
+      const int cl = u - cc.base - cb * cc.n_chunks;           // last chunk
+      const bool whole = (cf == 0 && cl == cc.n_chunks - 1);
       const bool finisher = (cf == 0 && !whole);
       // with 512 threads each pass reduces two batch rows (thread half t / COLS takes
       // row b + half; a D fragment of the MMA path holds two rows anyway); keep[b] then
@@ -546,7 +636,9 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
           for (int w = 0; w < WM; ++w) sum += red[(size_t)(half * WM + w) * COLS + o];
           const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
           const int col = MMA ? o : g * V + q * 4 + c;
-          if (whole) store_from_f32(a.y, a.y_dtype, (int64_t)bb * a.N + (int64_t)cb * COLS + col, sum);
+          if (whole) {
+            if (cb * COLS + col < cc.N) store_from_f32(cc.y, a.y_dtype, (int64_t)bb * cc.N + (int64_t)cb * COLS + col, sum);
+          }
           else if (finisher) keep[b] = sum;
           else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + bb) * COLS + col, tag_partial(sum));
         }
@@ -557,7 +649,8 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
         // k in (blockIdx.x, k_end); their tagged partials are polled in parallel,
         // summed in chunk order, and the slots zeroed for the next launch
         int k_end = blockIdx.x + 1;
-        while (k_end < (int)gridDim.x && (int)((int64_t)k_end * U / gridDim.x) < (cb + 1) * a.n_chunks) ++k_end;
+        while (k_end < (int)gridDim.x && (int)((int64_t)k_end * U / gridDim.x) < cc.base + (cb + 1) * cc.n_chunks)
+          ++k_end;
         const int n_later = k_end - blockIdx.x - 1;
         if (tid < BP * COLS) {
           const int o = tid % COLS;
@@ -585,7 +678,7 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
                 }
               }
             }
-            store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * COLS + col, sum);
+            if (cb * COLS + col < cc.N) store_from_f32(cc.y, a.y_dtype, (int64_t)b * cc.N + (int64_t)cb * COLS + col, sum);
           }
         }
         if (tid == 0) trace_at(a.trace, 5);
@@ -599,11 +692,26 @@ __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_ker
 #pragma unroll
         for (int j = 0; j < 4; ++j) cacc[q][j] = 0.f;
       span_first = u + 1;
-      cb += 1;
-      span_end = min(u1, (cb + 1) * a.n_chunks);
+      if (u + 1 < u1) {
+        seek(cc, u + 1);
+        cb = (u + 1 - cc.base) / cc.n_chunks;
+        span_end = min(u1, cc.base + (cb + 1) * cc.n_chunks);
+      }
     }
   }
   if (tid == 0) trace_at(a.trace, 6);
+}
+
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC>
+__global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
+  gemv_fast_body<V, CBYTES, R, B, WG, TILE, GTIER, ACC, false>(a, nullptr);
+}
+
+// grouped launch: the problem table travels as a __grid_constant__ kernel parameter
+template <int V, int CBYTES, int R, int B, int WG, int ACC>
+__global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1)
+    gemv_group_kernel(GemvFastArgs a, const __grid_constant__ GemvTable t) {
+  gemv_fast_body<V, CBYTES, R, B, WG, false, false, ACC, true>(a, t.p);
 }
 
 // generic path
@@ -690,7 +798,9 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   p.WG = (g.v == 4) ? 2 : 1;
   const int cols_per_cta = 32 * p.WG * g.v;
   const int CR = gemv_chunk_rows(p.WG, rows, p.cbytes);
-  if (g.rows % gemv_slab_rows(p.cbytes) != 0 || g.cols % cols_per_cta != 0) return p;
+  // the last column block may be narrower than 256 columns (TP shards such as
+  // 22016 / 4 = 5504 columns): GEMV_IL stores it with its own row-group width
+  if (g.rows % gemv_slab_rows(p.cbytes) != 0) return p;
   if (g.sharing == VQB_SHARE_TILE) {
     if (g.tile_rows % CR != 0 || g.tile_cols % cols_per_cta != 0) return p;
     p.tile = true;
@@ -714,7 +824,7 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   // 2-way bank conflict per 16-row k-block of the GEMV_IL words).
   p.mma = p.h2 && !p.gtier && !p.tile && g.v == 8 && rows >= 4 && !(L && (L->flags & VQB_FLAG_NO_MMA));
   const int CRm = gemv_chunk_rows(p.WG, rows, p.cbytes, p.mma);
-  p.n_cblk = (int)(g.cols / cols_per_cta);
+  p.n_cblk = (int)ceil_div(g.cols, cols_per_cta);
   p.n_chunks = (int)((g.rows + CRm - 1) / CRm);
   p.threads = gemv_warps(rows, p.mma) * 32;
   const int nst = gemv_stages(p.R, p.cbytes, p.WG, rows, p.mma);
@@ -895,6 +1005,119 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
   return VQB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// grouped launch: every problem one GEMV of the same configuration
+
+typedef void (*GemvGroupKernel)(GemvFastArgs, const GemvTable);
+
+template <int CBYTES, int B>
+static GemvGroupKernel group_kernel_acc(bool h2, bool mma) {
+  if constexpr (B >= 4)
+    if (mma) return gemv_group_kernel<8, CBYTES, 1, B, 1, 2>;
+  return h2 ? gemv_group_kernel<8, CBYTES, 1, B, 1, 1> : gemv_group_kernel<8, CBYTES, 1, B, 1, 0>;
+}
+
+template <int CBYTES>
+static GemvGroupKernel group_kernel_rows(int rows, bool h2, bool mma) {
+  switch (rows) {
+    case 1: return group_kernel_acc<CBYTES, 1>(h2, mma);
+    case 2: return group_kernel_acc<CBYTES, 2>(h2, mma);
+    case 4: return group_kernel_acc<CBYTES, 4>(h2, mma);
+    default: return group_kernel_acc<CBYTES, 8>(h2, mma);
+  }
+}
+
+int gemv_grouped_dispatch(const VqbTensor* ws_t, int n, const void* const* xs, int x_dtype, int rows,
+                          void* const* ys, int y_dtype, const VqbLaunch* L, void* ws, size_t ws_bytes,
+                          cudaStream_t st) {
+  if (n < 1 || n > kMaxGroup) return set_error(VQB_ESHAPE, "grouped GEMV takes 1..%d problems, got %d", kMaxGroup, n);
+  if (x_dtype != VQB_F16 || y_dtype < VQB_F32 || y_dtype > VQB_BF16)
+    return set_error(VQB_ECONFIG, "grouped GEMV: fp16 activations, f32/f16/bf16 outputs");
+  GemvTable table;
+  FastPlan p0;
+  int units = 0;
+  for (int i = 0; i < n; ++i) {
+    Geom g;
+    int s = make_geom(&ws_t[i], &g);
+    if (s) return s;
+    if (g.ndim != 2) return set_error(VQB_ESHAPE, "grouped GEMV problem %d is not 2-D", i);
+    FastPlan p = plan_fast(g, &ws_t[i], rows, x_dtype, L);
+    if (!p.ok || p.tile || p.gtier || p.R != 1 || p.V != 8 || (reinterpret_cast<uintptr_t>(xs[i]) & 15) != 0)
+      return set_error(VQB_ECONFIG,
+                       "grouped GEMV problem %d: needs whole-tensor books with every code < 256, v = 8, R = 1, "
+                       "GEMV_IL codes, fp16 books and 16-byte aligned activations", i);
+    if (i == 0) {
+      p0 = p;
+    } else if (p.cbytes != p0.cbytes || p.mma != p0.mma || p.h2 != p0.h2 || p.n_sh != p0.n_sh ||
+               ws_t[i].log2_entries != ws_t[0].log2_entries) {
+      return set_error(VQB_ECONFIG, "grouped GEMV problem %d differs in configuration from problem 0", i);
+    }
+    GemvProblem& q = table.p[i];
+    q.codes = reinterpret_cast<const uint8_t*>(ws_t[i].d_codes);
+    q.level_bytes = g.S * g.code_bytes;
+    q.books = reinterpret_cast<const __half*>(ws_t[i].d_codebooks);
+    q.x = reinterpret_cast<const __half*>(xs[i]);
+    q.y = ys[i];
+    q.M = (int)g.rows;
+    q.N = (int)g.cols;
+    q.n_cblk = p.n_cblk;
+    q.n_chunks = p.n_chunks;
+    q.unit_base = units;
+    q.pad = 0;
+    if ((int64_t)units + (int64_t)p.n_cblk * p.n_chunks > (1LL << 30))
+      return set_error(VQB_ESHAPE, "grouped GEMV: too many work units");
+    units += p.n_cblk * p.n_chunks;
+  }
+  if ((int64_t)ws_bytes < (int64_t)VQB_WS_COUNTER_BYTES + 65536 || !ws)
+    return set_error(VQB_ECAPACITY, "GEMV workspace too small: %zu", ws_bytes);
+  GemvGroupKernel kernel = p0.cbytes == 2 ? group_kernel_rows<2>(rows, p0.h2, p0.mma)
+                                          : group_kernel_rows<1>(rows, p0.h2, p0.mma);
+  Geom g0;
+  make_geom(&ws_t[0], &g0);
+  GemvFastArgs a = {};
+  a.y_dtype = y_dtype;
+  a.K = g0.K;
+  a.n_regions = 1;
+  a.n_sh = p0.n_sh;
+  a.total_units = units;
+  a.n_probs = n;
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  int grid = std::min(units, sm_count());
+  if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
+  if ((int64_t)grid * rows * 256 * 8 > VQB_WS_COUNTER_BYTES - 65536)
+    return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
+  a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
+  a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
+  {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kernel) ^ ((uintptr_t)dev << 56));
+    if (!done.count(key)) {
+      VQB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+      int occ = 0;
+      VQB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, p0.threads, p0.smem));
+      done[key] = occ;
+    }
+    if (done[key] < 1) return set_error(VQB_ECAPACITY, "grouped GEMV plan does not fit one CTA per SM");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(p0.threads);
+  cfg.dynamicSmemBytes = p0.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (L && (L->flags & VQB_FLAG_NO_PDL)) ? 0 : 1;
+  VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, a, table));
+  set_kernel("gemv_group");
+  return VQB_OK;
+}
+
 int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
   Geom g;
   int s = make_geom(w, &g);
@@ -922,6 +1145,13 @@ int gemv_usage(VqbUsage* u) {
 }
 
 }  // namespace vqb
+
+extern "C" int vqb_gemv_grouped(const VqbTensor* w, int32_t n, const void* const* d_xs, int32_t x_dtype,
+                                int32_t rows, void* const* d_ys, int32_t y_dtype, const VqbLaunch* launch, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+  return vqb::gemv_grouped_dispatch(w, n, d_xs, x_dtype, rows, d_ys, y_dtype, launch, d_ws, ws_bytes,
+                                    reinterpret_cast<cudaStream_t>(stream));
+}
 
 extern "C" int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows, void* d_y,
                         int32_t y_dtype, const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {

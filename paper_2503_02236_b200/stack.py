@@ -15,7 +15,7 @@ from .ops import Workspace, launch_struct
 
 class VQLinearStack:
     def __init__(self, weights, rows: int = 1, act_dtype=torch.float16, out_dtype=torch.float16,
-                 launches=None):
+                 launches=None, grouped: bool = False):
         self.weights = list(weights)
         if not self.weights:
             raise ValueError("empty stack")
@@ -40,10 +40,25 @@ class VQLinearStack:
         # private arena: the graph bakes its pointer in (never the shared per-stream one)
         self._ws = Workspace(self.device, need).buf
         self._graph = None
+        # grouped: the stack's (independent) GEMVs run as persistent launches of up to
+        # GROUP_MAX problems each (vqb_gemv_grouped) instead of one launch per linear
+        self.grouped = bool(grouped)
+        self._groups = []
+        if self.grouped:
+            import ctypes
+            esz_x, esz_y = self.x.element_size(), self.y.element_size()
+            for g0 in range(0, len(self.weights), self.GROUP_MAX):
+                idx = list(range(g0, min(g0 + self.GROUP_MAX, len(self.weights))))
+                structs = (N.VqbTensor * len(idx))(*[self._structs[i] for i in idx])
+                xs = (ctypes.c_void_p * len(idx))(*[self.x.data_ptr() + self.in_off[i] * esz_x for i in idx])
+                ys = (ctypes.c_void_p * len(idx))(*[self.y.data_ptr() + self.out_off[i] * esz_y for i in idx])
+                self._groups.append((structs, xs, ys, len(idx), self.launches[g0]))
+
+    GROUP_MAX = 192
 
     @property
     def n_launches(self) -> int:
-        return len(self.weights)
+        return len(self._groups) if self.grouped else len(self.weights)
 
     def input_view(self, i: int) -> torch.Tensor:
         return self.x[self.in_off[i]:self.in_off[i + 1]].view(self.rows, -1)
@@ -59,6 +74,12 @@ class VQLinearStack:
         esz_x, esz_y = self.x.element_size(), self.y.element_size()
         xb, yb = self.x.data_ptr(), self.y.data_ptr()
         ws, wsn = self._ws.data_ptr(), self._ws.numel()
+        if self.grouped:
+            import ctypes
+            for structs, xs, ys, n, L in self._groups:
+                N.check(lib.vqb_gemv_grouped(ctypes.cast(structs, ctypes.c_void_p), n, ctypes.cast(xs, ctypes.c_void_p),
+                                             xd, self.rows, ctypes.cast(ys, ctypes.c_void_p), yd, L, ws, wsn, stream))
+            return
         for i, (s, L) in enumerate(zip(self._structs, self.launches)):
             N.check(lib.vqb_gemv(s, xb + self.in_off[i] * esz_x, xd, self.rows,
                                  yb + self.out_off[i] * esz_y, yd, L, ws, wsn, stream))
