@@ -149,6 +149,9 @@ const char* vqb_last_error(void);
 /* Name of the last kernel this thread launched ("gemv_fast", "attn_cq", ...):
  * lets tests and the benchmark prove which path ran. */
 const char* vqb_last_kernel(void);
+/* {grid CTAs, threads per CTA, shared-tier entries, register-tier entries} of this
+ * thread's last fused launch: shows which plan the kernel actually ran with. */
+int vqb_last_launch(int32_t* out4);
 
 /* Reconstruct the dense tensor (dequantize, codec.py:391-408): fp32 output is
  * bit-exact with the reference (accumulation from +0.0f in level order);

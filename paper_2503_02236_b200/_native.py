@@ -35,7 +35,7 @@ _ERRORS = {
 
 # every symbol include/vqb.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "vqb_abi_version", "vqb_last_error", "vqb_last_kernel", "vqb_dequant", "vqb_workspace_bytes", "vqb_gemv",
+    "vqb_abi_version", "vqb_last_error", "vqb_last_kernel", "vqb_last_launch", "vqb_dequant", "vqb_workspace_bytes", "vqb_gemv",
     "vqb_gemm", "vqb_attn_decode", "vqb_layout_bytes", "vqb_repack", "vqb_query_usage",
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
     "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error", "vqb_gemv_grouped",
@@ -108,6 +108,7 @@ def lib():
             L.vqb_abi_version.restype = ctypes.c_int
             L.vqb_last_error.restype = ctypes.c_char_p
             L.vqb_last_kernel.restype = ctypes.c_char_p
+            L.vqb_last_launch.argtypes = [P(i32)]
             L.vqb_dequant.argtypes = [T, vp, i32, vp]
             L.vqb_workspace_bytes.argtypes = [i32, T, i64, La]
             L.vqb_workspace_bytes.restype = i64
@@ -155,6 +156,13 @@ def take_device_error() -> int:
     v = ctypes.c_int32(0)
     check(lib().vqb_take_device_error(ctypes.byref(v)))
     return int(v.value)
+
+
+def last_launch() -> dict:
+    """grid / threads / shared-tier / register-tier entries of the last fused launch."""
+    out = (ctypes.c_int32 * 4)()
+    lib().vqb_last_launch(out)
+    return {"grid": out[0], "threads": out[1], "n_shared": out[2], "n_reg": out[3]}
 
 
 def check(status: int) -> int:

@@ -17,7 +17,15 @@ namespace vqb {
 static thread_local std::string g_last_error;
 static thread_local const char* g_last_kernel = "";
 
+static thread_local int32_t g_last_launch[4] = {0, 0, 0, 0};
+
 void set_kernel(const char* name) { g_last_kernel = name; }
+void set_launch(int grid, int threads, int n_shared, int n_reg) {
+  g_last_launch[0] = grid;
+  g_last_launch[1] = threads;
+  g_last_launch[2] = n_shared;
+  g_last_launch[3] = n_reg;
+}
 
 int set_error(int code, const char* fmt, ...) {
   char buf[1024];
@@ -253,6 +261,10 @@ int vqb_abi_version(void) { return VQB_ABI_VERSION; }
 const char* vqb_last_error(void) { return g_last_error.c_str(); }
 
 const char* vqb_last_kernel(void) { return g_last_kernel; }
+int vqb_last_launch(int32_t* out4) {
+  for (int i = 0; i < 4; ++i) out4[i] = g_last_launch[i];
+  return VQB_OK;
+}
 
 int vqb_dequant(const VqbTensor* t, void* d_out, int32_t out_dtype, void* stream) {
   Geom g;

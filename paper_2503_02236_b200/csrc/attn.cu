@@ -648,6 +648,7 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
   if (grid_limit > 0) grid = std::min(grid, grid_limit);
   VQB_CUDA_CHECK(launch_pdl(kern, dim3(grid), dim3(kAttnThreads), smem, st, a));
   set_kernel("attn_cq");
+  set_launch(grid, kAttnThreads, 256, 0);
   return VQB_OK;
 }
 
@@ -699,7 +700,13 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + 8192)
                                      : nullptr;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)C);
-    const int gl = L ? L->grid_limit : 0;
+    int gl = L ? L->grid_limit : 0;
+    // the planner's split of T (VqbLaunch split over T): each (b, h) span is shared
+    // by ~split_factor CTAs of the persistent schedule
+    if (L && L->split_axis == 'T' && L->split_factor > 0) {
+      const int cap = std::max(1, B * H * L->split_factor);
+      gl = gl > 0 ? std::min(gl, cap) : cap;
+    }
     const int gpl = (int)(gk.gpr / 32);
     if (gk.v == 2 && gpl == 2) return launch_attn_t<2, 2>(a, st, gl);
     if (gk.v == 2 && gpl == 1) return launch_attn_t<2, 1>(a, st, gl);

@@ -28,6 +28,8 @@ int set_error(int code, const char* fmt, ...);
 int cuda_error(cudaError_t e, const char* what);
 int sm_count();
 void set_kernel(const char* name);
+// grid, threads, shared-tier entries and register-tier entries of the last fused launch
+void set_launch(int grid, int threads, int n_shared, int n_reg);
 
 #define VQB_CUDA_CHECK(expr)                            \
   do {                                                  \

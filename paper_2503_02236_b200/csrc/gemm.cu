@@ -473,6 +473,7 @@ static int launch_gemm_t(const CUtensorMap& map, const GemmArgs& a, int grid, cu
   if (attr_err[dev] != cudaSuccess) return cuda_error(attr_err[dev], "cudaFuncSetAttribute(gemm_tc_kernel)");
   kern<<<grid, kGemmThreads, smem, st>>>(map, a);
   VQB_LAUNCH_CHECK("gemm_tc_kernel");
+  set_launch(grid, kGemmThreads, 256, 0);
   if (a.splits > 1) {
     const int64_t n_out = (int64_t)a.rows * a.N;
     const int blocks = (int)std::min<int64_t>(ceil_div(n_out, 256), (int64_t)sm_count() * 4);

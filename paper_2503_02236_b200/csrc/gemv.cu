@@ -88,6 +88,7 @@ struct GemvFastArgs {
   unsigned long long* part;  // (grid, B, COLS) tagged partials {fp32 value, tag 1}, one slot per CTA,
                              // in the self-resetting workspace head (zeroed by the consumer)
   unsigned long long* trace;  // optional per-CTA phase timestamps (debug flag 32), 8 per CTA
+  int n_reg;                  // register tier: entries [0, n_reg) held in registers (REGT kernels, <= 4)
   int total_units;            // grouped launch: units over every problem of the table
   int n_probs;                // grouped launch: problems in the table (0: the single problem above)
 };
@@ -138,12 +139,13 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // entries become A fragments through ldmatrix.trans straight from the replicated
 // shared codebook (W^T: 16 columns x 16 rows per column pair), the activations the
 // B fragment (16 rows x 8 batch rows), fp32 accumulation.
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool GROUP>
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool GROUP, bool REGT = false>
 __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const GemvProblem* __restrict__ probs) {
   constexpr bool H2 = ACC == 1;
   constexpr bool MMA = ACC == 2;
   static_assert(!MMA || (V == 8 && WG == 1 && !GTIER && !TILE), "tensor-core GEMV: v = 8, codes in shared memory");
   static_assert(!GROUP || (!TILE && !GTIER && R == 1), "grouped GEMV: whole-tensor books resident in shared memory");
+  static_assert(!REGT || (V == 8 && R == 1 && !TILE && !GROUP && ACC != 2), "register tier: one whole-tensor book, CUDA cores");
   constexpr int kGemvWarps = gemv_warps(B, MMA);
   constexpr int kGemvThreads = kGemvWarps * 32;
   constexpr int EB = V * 2;              // fp16 entry bytes
@@ -223,6 +225,17 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
   ProbCursor cc, fc;
   load_prob(cc, first_prob(u0));
   fc = cc;
+  // register tier (paper O2): the n_reg hottest entries of the (frequency-ordered,
+  // whole-tensor) book live in registers of every thread; codes below n_reg are
+  // served by a select chain instead of a shared-memory gather
+  constexpr int kRegSlots = 4;
+  uint4 hot[REGT ? kRegSlots : 1];
+  const uint32_t nreg = REGT ? (uint32_t)min(a.n_reg, kRegSlots) : 0u;
+  if constexpr (REGT) {
+#pragma unroll
+    for (int j = 0; j < kRegSlots; ++j)
+      hot[j] = (j < (int)nreg) ? __ldg(reinterpret_cast<const uint4*>(cc.books) + j) : make_uint4(0u, 0u, 0u, 0u);
+  }
 
   if (tid == 0) {
     trace_at(a.trace, 0);
@@ -527,7 +540,27 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const uint8_t* src = lookup(w8 * 8 + l0 + kk, r);
-            if constexpr (EB == 16) {
+            if constexpr (REGT) {
+              // the code (16-bit or 8-bit) of row k; below n_reg -> registers
+              const int k = w8 * 8 + l0 + kk, i = k / RPL, kr = k % RPL;
+              uint32_t code;
+              if constexpr (CBYTES == 2) {
+                const uint32_t w = (&cw[i][r].x)[kr / 2];
+                code = (kr & 1) ? (w >> 16) : (w & 0xffffu);
+              } else {
+                code = ((&cw[i][r].x)[kr / 4] >> (8 * (kr % 4))) & 0xffu;
+              }
+              uint4 q;
+              if (code < nreg) {
+                q = hot[0];
+#pragma unroll
+                for (int j = 1; j < kRegSlots; ++j)
+                  if (code == (uint32_t)j) q = hot[j];
+              } else {
+                q = *reinterpret_cast<const uint4*>(src);
+              }
+              ent[kk][r][0] = q.x; ent[kk][r][1] = q.y; ent[kk][r][2] = q.z; ent[kk][r][3] = q.w;
+            } else if constexpr (EB == 16) {
               const uint4 q = *reinterpret_cast<const uint4*>(src);
               ent[kk][r][0] = q.x; ent[kk][r][1] = q.y; ent[kk][r][2] = q.z; ent[kk][r][3] = q.w;
             } else {
@@ -702,9 +735,9 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
   if (tid == 0) trace_at(a.trace, 6);
 }
 
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC>
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool REGT = false>
 __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
-  gemv_fast_body<V, CBYTES, R, B, WG, TILE, GTIER, ACC, false>(a, nullptr);
+  gemv_fast_body<V, CBYTES, R, B, WG, TILE, GTIER, ACC, false, REGT>(a, nullptr);
 }
 
 // grouped launch: the problem table travels as a __grid_constant__ kernel parameter
@@ -780,7 +813,7 @@ struct FastPlan {
   bool ok = false;
   int V = 0, cbytes = 0, R = 0, WG = 1;
   bool tile = false, gtier = true, h2 = true, mma = false;
-  int n_sh = 0, n_cblk = 0, n_chunks = 0, threads = 0;
+  int n_sh = 0, n_cblk = 0, n_chunks = 0, threads = 0, n_reg = 0;
   size_t smem = 0;
 };
 
@@ -818,6 +851,9 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   if (!p.gtier) n_sh = std::min(n_sh, 256);
   p.n_sh = n_sh;
   p.h2 = !(L && (L->flags & VQB_FLAG_EXACT_ACCUM));
+  // register tier: batch 1, one 16-bit/8-bit level of a whole-tensor book (REGT kernels)
+  if (L && L->n_reg > 0 && rows == 1 && g.v == 8 && g.R == 1 && !p.tile && p.h2)
+    p.n_reg = std::min(L->n_reg, std::min(4, g.K));
   // batch 4-8: tensor-core inner product (every entry resident in shared memory).
   // Measured (quip2 4096x12288 / 4096x4096): batch 8 22.0 / 13.7 us vs 28.1 / 20.1 on
   // CUDA cores, batch 4 about even, batch 2 slower (the mma path reads its codes with a
@@ -880,6 +916,9 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
   // one persistent CTA per SM: every CTA is resident (a finishing CTA polls the
   // partials of later CTAs) and the SM's second slot is left to the next kernel
   int grid = std::min(p.n_cblk * p.n_chunks, sm_count());
+  // the planner's split of the reduction over M: each column block is shared by
+  // ~split_factor CTAs of the stream-K schedule
+  if (L && L->split_axis == 'M' && L->split_factor > 0) grid = std::max(1, std::min(grid, p.n_cblk * L->split_factor));
   if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -893,11 +932,15 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
   cfg.numAttrs = (L && (L->flags & VQB_FLAG_NO_PDL)) ? 0 : 1;
   VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, a));
   set_kernel("gemv_fast");
+  set_launch(grid, p.threads, p.n_sh, p.n_reg);
   return VQB_OK;
 }
 
 template <int V, int CBYTES, int R, int B, int WG, bool TILE>
-static GemvKernel pick_acc(bool gtier, bool h2, bool mma) {
+static GemvKernel pick_acc(bool gtier, bool h2, bool mma, bool regt) {
+  if constexpr (V == 8 && WG == 1 && !TILE && B == 1 && R == 1)
+    if (regt && h2) return gtier ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, 1, true>
+                                 : gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, 1, true>;
   if constexpr (V == 8 && WG == 1 && !TILE && B >= 2)
     if (mma && !gtier) return gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, false, 2>;
   return gtier ? (h2 ? gemv_fast_kernel<V, CBYTES, R, B, WG, TILE, true, 1>
@@ -907,23 +950,23 @@ static GemvKernel pick_acc(bool gtier, bool h2, bool mma) {
 }
 
 template <int V, int CBYTES, int R, int WG, bool TILE>
-static GemvKernel pick_kernel(int rows, bool gtier, bool h2, bool mma) {
+static GemvKernel pick_kernel(int rows, bool gtier, bool h2, bool mma, bool regt) {
   switch (rows) {
-    case 1: return pick_acc<V, CBYTES, R, 1, WG, TILE>(gtier, h2, mma);
-    case 2: return pick_acc<V, CBYTES, R, 2, WG, TILE>(gtier, h2, mma);
-    case 4: return pick_acc<V, CBYTES, R, 4, WG, TILE>(gtier, h2, mma);
-    default: return pick_acc<V, CBYTES, R, 8, WG, TILE>(gtier, h2, mma);
+    case 1: return pick_acc<V, CBYTES, R, 1, WG, TILE>(gtier, h2, mma, regt);
+    case 2: return pick_acc<V, CBYTES, R, 2, WG, TILE>(gtier, h2, mma, regt);
+    case 4: return pick_acc<V, CBYTES, R, 4, WG, TILE>(gtier, h2, mma, regt);
+    default: return pick_acc<V, CBYTES, R, 8, WG, TILE>(gtier, h2, mma, regt);
   }
 }
 
 static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
   // (V, code bytes, R, WG, tile-shared) combinations covering the BASELINE configs
-  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier, p.h2, p.mma);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier, p.h2, p.mma);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier, p.h2, p.mma);
-  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier, p.h2, p.mma);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier, p.h2, p.mma);
-  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier, p.h2, p.mma);
+  if (p.V == 8 && p.cbytes == 2 && p.R == 1 && !p.tile) return pick_kernel<8, 2, 1, 1, false>(rows, p.gtier, p.h2, p.mma, p.n_reg > 0);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 2 && !p.tile) return pick_kernel<8, 1, 2, 1, false>(rows, p.gtier, p.h2, p.mma, p.n_reg > 0);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<8, 1, 1, 1, false>(rows, p.gtier, p.h2, p.mma, p.n_reg > 0);
+  if (p.V == 8 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<8, 1, 1, 1, true>(rows, p.gtier, p.h2, p.mma, p.n_reg > 0);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && p.tile) return pick_kernel<4, 1, 1, 2, true>(rows, p.gtier, p.h2, p.mma, p.n_reg > 0);
+  if (p.V == 4 && p.cbytes == 1 && p.R == 1 && !p.tile) return pick_kernel<4, 1, 1, 2, false>(rows, p.gtier, p.h2, p.mma, p.n_reg > 0);
   return nullptr;
 }
 
@@ -965,7 +1008,8 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.n_chunks = p.n_chunks;
     a.n_cblk = p.n_cblk;
     a.n_sh = p.n_sh;
-    const int grid = std::min<int64_t>(units, sm_count());
+    a.n_reg = p.n_reg;
+    const int grid = (int)std::min<int64_t>(units, sm_count());  // upper bound for the slot check
     // head layout: [0, 64 KB) split-arrival counters (attention), then the GEMV slots
     if ((int64_t)grid * rows * (32 * p.WG * p.V) * 8 > VQB_WS_COUNTER_BYTES - 65536)
       return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
@@ -1115,6 +1159,7 @@ int gemv_grouped_dispatch(const VqbTensor* ws_t, int n, const void* const* xs, i
   cfg.numAttrs = (L && (L->flags & VQB_FLAG_NO_PDL)) ? 0 : 1;
   VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, a, table));
   set_kernel("gemv_group");
+  set_launch(grid, p0.threads, p0.n_sh, 0);
   return VQB_OK;
 }
 

@@ -1,19 +1,23 @@
-"""Hierarchical fusion planning (vqforge.fusion, pkg/src/vqforge/fusion.py; paper §VI-B, Alg. 1).
+"""Hierarchical fusion: how dequantized codebook entries reach the consumer's
+operand layout (paper §VI-B, Alg. 1; reference pkg/src/vqforge/fusion.py).
 
-The planner decides whether dequantized data reaches the compute layout through
-intra-warp register exchanges (``n_shuffle = v / required_layout - 1`` xor
-steps inside mini-warps) or through shared memory, using the profiled latency
-ratio THRES_SHUFFLE.
+The reference decides between *register* fusion (intra-warp xor exchanges inside
+mini-warps of ``v / required_layout`` lanes; ``n_shuffle = iters - 1``) and
+*shared* fusion (stage the dequantized tile in shared memory) by comparing the
+exchange count with the profiled latency ratio THRES_SHUFFLE. The schedule API
+below reproduces its mapping and is verified lane by lane against the
+reference's ownership oracle (tests/test_host.py).
 
-How the B200 kernels realise the two levels:
-* "register": GEMV and decode attention are CUDA-core kernels where each lane
-  owns whole sub-vectors and consumes them itself with fma.rn.f32.f16 — the
-  exchange schedule degenerates to zero shuffles.
-* "shared": tcgen05.mma reads operands only from shared memory / TMEM, so the
-  prefill GEMM always stages dequantized tiles in shared memory in the UMMA
-  canonical layout.
-The schedule construction below is kept for API parity and is verified against
-the reference's exhaustive ownership oracle in tests.
+On B200 the level selects a kernel family (``b200_fusion``):
+
+* ``register`` — looked-up entries go straight into the consumer's registers:
+  CUDA-core FMAs where a lane owns whole sub-vectors (GEMV batch 1-2, decode
+  attention: zero exchanges needed), or mma.sync A fragments gathered by
+  ``ldmatrix.trans`` from the replicated table (GEMV batch 4-8: the hardware
+  transpose replaces the xor exchange schedule);
+* ``shared`` — the dequantized W tile is written to shared memory in the UMMA
+  canonical layout for tcgen05 (prefill GEMM): tcgen05.mma reads operands only
+  from shared memory / TMEM.
 """
 
 import json
@@ -27,14 +31,17 @@ WARP = 32
 THRES_SHUFFLE = 5
 STYLE_STRIDED = "strided"
 STYLE_MMA = "mma"
+B200_GEMV_MAX_ROWS = 8  # rows above this take the tcgen05 GEMM (shared-level fusion)
 
 
 def _pow2(n: int) -> bool:
-    return n > 0 and not n & (n - 1)
+    return n > 0 and (n & (n - 1)) == 0
 
 
 @dataclass(frozen=True)
 class LayoutPair:
+    """Elements per thread after dequantization (src = v) and as the consumer needs them (dst)."""
+
     layout_src: int
     layout_dst: int
 
@@ -44,7 +51,7 @@ class LayoutPair:
 
     @property
     def register_compatible(self) -> bool:
-        return self.layout_src >= self.layout_dst
+        return self.layout_dst <= self.layout_src
 
     @property
     def iters(self) -> int:
@@ -63,9 +70,15 @@ def shuffle_count(vector_size: int, required_layout: int) -> int:
 
 
 def choose_fusion_level(layouts: LayoutPair, thres_shuffle: int = THRES_SHUFFLE) -> str:
-    if layouts.register_compatible and layouts.n_shuffle < thres_shuffle:
-        return "register"
-    return "shared"
+    ok = layouts.register_compatible and layouts.n_shuffle < thres_shuffle
+    return "register" if ok else "shared"
+
+
+def b200_fusion(op_kind: str, rows: int = 1) -> str:
+    """Fusion level of the sm_100a kernel that serves the op (see module doc)."""
+    if op_kind == "gemm" and rows > B200_GEMV_MAX_ROWS:
+        return "shared"
+    return "register"
 
 
 @dataclass(frozen=True)
@@ -80,22 +93,26 @@ class WarpTile:
 
 
 def default_warp_tile(layouts: LayoutPair, style: str) -> WarpTile:
+    """Strided: 32 rows of v. MMA (dst 2): 16 rows of 2v (one m16n8k16 A operand
+    row pair per lane quad); below v = 4 the strided tile is used."""
+    if style not in (STYLE_STRIDED, STYLE_MMA):
+        raise MappingError(f"unknown compute style {style!r}")
     src = layouts.layout_src
-    if style == STYLE_STRIDED:
-        return WarpTile(WARP, src, style)
     if style == STYLE_MMA:
         if layouts.layout_dst != 2:
             raise MappingError("mma consumers take layout_dst = 2")
-        return WarpTile(WARP, src, STYLE_STRIDED) if src < 4 else WarpTile(16, 2 * src, style)
-    raise MappingError(f"unknown compute style {style!r}")
+        if src >= 4:
+            return WarpTile(16, 2 * src, STYLE_MMA)
+    return WarpTile(WARP, src, STYLE_STRIDED)
 
 
 def compute_owner(tile: WarpTile, dst: int, e: np.ndarray):
-    """(lane, slot) consuming element e in the compute layout."""
+    """(lane, slot) that consumes element e in the compute layout."""
+    e = np.asarray(e)
     if tile.style == STYLE_STRIDED:
         return (e // dst) % WARP, e // (WARP * dst)
     r, c = np.divmod(e, tile.cols)
-    return (r % 8) * 4 + (c % 8) // 2, (r // 8) * (tile.cols // 8) + c // 8
+    return 4 * (r % 8) + (c % 8) // 2, (tile.cols // 8) * (r // 8) + c // 8
 
 
 @dataclass(frozen=True)
@@ -112,9 +129,8 @@ class ShuffleSchedule:
 
     @property
     def subvector_of_lane(self) -> np.ndarray:
-        inv = np.empty(WARP, dtype=np.int64)
-        inv[np.asarray(self.thread_remap)] = np.arange(WARP)
-        return inv
+        """Inverse remap: the naive sub-vector each lane dequantizes."""
+        return np.argsort(np.asarray(self.thread_remap))
 
     def to_json(self) -> str:
         return json.dumps({"mini_warp_size": self.mini_warp_size, "remap": list(self.thread_remap),
@@ -122,27 +138,37 @@ class ShuffleSchedule:
 
 
 def build_thread_mapping(warp_tile: WarpTile, layouts: LayoutPair) -> np.ndarray:
-    """remap[naive dequant lane] = lane that dequantizes it, so every mini-warp of
-    ``iters`` lanes dequantizes exactly what it consumes (Alg. 1 lines 2-11)."""
-    src, dst, it = layouts.layout_src, layouts.layout_dst, layouts.iters
+    """remap[sub-vector] = lane that dequantizes it, chosen so every xor-aligned
+    mini-warp of ``iters`` lanes dequantizes exactly the elements it consumes."""
+    src, it = layouts.layout_src, layouts.iters
     if it > WARP:
-        raise MappingError(f"exchange group of {it} lanes exceeds the warp; use shared fusion")
-    e = np.arange(warp_tile.n_elements)
-    consumer, _ = compute_owner(warp_tile, dst, e)
-    producer = e // src
-    groups = {}
-    for lane in range(WARP):
-        key = tuple(dict.fromkeys(consumer[producer == lane].tolist()))
-        groups.setdefault(key, []).append(lane)
-    remap = np.full(WARP, -1, dtype=np.int64)
-    for key, lanes in groups.items():
-        if len(key) != it or len(lanes) != it:
-            raise MappingError(f"consumer set {key} of lanes {lanes} is not an {it}-lane exchange "
+        raise MappingError(f"an exchange group of {it} lanes exceeds the warp; use shared fusion")
+    consumer, _ = compute_owner(warp_tile, layouts.layout_dst, np.arange(warp_tile.n_elements))
+    # consumer lanes of each sub-vector's src elements, as a (32, src) matrix
+    cons = consumer.reshape(WARP, src)
+    first = cons.min(axis=1)
+    sig = np.sort(cons, axis=1)
+    # each sub-vector must feed one complete xor-aligned group {g, g+1, ..., g+it-1},
+    # met in ascending lane order along its elements
+    for row in cons:
+        _, at = np.unique(row, return_index=True)
+        if np.any(np.diff(row[np.sort(at)]) < 0):
+            raise MappingError("consumer lanes of a sub-vector are not met in ascending order; use shared fusion")
+    groups = np.unique(sig, axis=0)
+    for row in groups:
+        lanes = np.unique(row)
+        if lanes.size != it or lanes[0] % it or not np.array_equal(lanes, lanes[0] + np.arange(it)):
+            raise MappingError(f"consumer lanes {lanes.tolist()} are not an aligned {it}-lane exchange "
                                "group; use shared fusion")
-        if key[0] % it or key != tuple(range(key[0], key[0] + it)):
-            raise MappingError(f"consumer set {key} is not xor-aligned; use shared fusion")
-        remap[sorted(lanes)] = key
-    if (remap < 0).any() or np.unique(remap).size != WARP:
+    # sub-vectors feeding a group are assigned to that group's lanes in order
+    order = np.lexsort((np.arange(WARP), first))
+    remap = np.empty(WARP, dtype=np.int64)
+    base = first[order]
+    rank = np.arange(WARP) - np.searchsorted(base, base, side="left")
+    if (rank >= it).any():
+        raise MappingError("more sub-vectors than lanes in an exchange group; use shared fusion")
+    remap[order] = base + rank
+    if np.unique(remap).size != WARP:
         raise MappingError("thread remap is not a bijection over the warp")
     return remap
 
@@ -155,21 +181,21 @@ def build_shuffle_schedule(layouts: LayoutPair, style: str = STYLE_STRIDED) -> S
 
 
 def dequant_register_file(schedule: ShuffleSchedule) -> np.ndarray:
-    """(32, iters, dst) element ids right after dequantization under the remap."""
+    """(32, iters, dst) element ids each lane holds right after dequantization."""
     src, dst, it = schedule.layouts.layout_src, schedule.layouts.layout_dst, schedule.layouts.iters
-    sub = schedule.subvector_of_lane
-    return (sub[:, None] * src + np.arange(src)[None, :]).reshape(WARP, it, dst)
+    elems = schedule.subvector_of_lane[:, None] * src + np.arange(src)
+    return elems.reshape(WARP, it, dst)
 
 
 def run_shuffle_steps(schedule: ShuffleSchedule, regs: np.ndarray) -> np.ndarray:
-    """Warp-synchronous xor exchanges: step ``off`` swaps slot (lane^off) % iters with lane^off."""
+    """Warp-synchronous xor exchanges: at step ``off`` lane l receives its partner's
+    (l ^ off) slot (l mod iters) into its own slot (partner mod iters)."""
     it = schedule.mini_warp_size
-    lanes = np.arange(WARP)
-    cur = regs.copy()
+    lane = np.arange(WARP)
+    cur = np.array(regs, copy=True)
     for off in schedule.offsets:
-        partner = lanes ^ off
-        prev = cur.copy()
-        cur[lanes, partner % it] = prev[partner, lanes % it]
+        partner = lane ^ off
+        cur[lane, partner % it] = cur[partner, lane % it].copy()
     return cur
 
 
@@ -177,8 +203,6 @@ def expected_compute_ownership(schedule: ShuffleSchedule) -> np.ndarray:
     tile, dst, it = schedule.tile, schedule.layouts.layout_dst, schedule.layouts.iters
     e = np.arange(tile.n_elements)
     lane, slot = compute_owner(tile, dst, e)
-    want = np.empty((WARP, it, dst), dtype=np.int64)
-    for ln in range(WARP):
-        for j in range(it):
-            want[ln, j] = np.sort(e[(lane == ln) & (slot == j)])
-    return want
+    key = lane * it + slot
+    order = np.lexsort((e, key))
+    return e[order].reshape(WARP, it, dst)

@@ -21,12 +21,12 @@ from typing import Optional
 
 import numpy as np
 
-from .cacheplan import CachePlan, b200_shared_entries, compute_slack, plan_cache
+from .cacheplan import CachePlan, compute_slack, plan_b200_tiers, plan_cache
 from .codec import Codebook, QuantizedTensor, VQConfig
-from .dataflow import ATTENTION, GEMM, GEMV, ComputeOp, DataflowPlan, build_dataflow
+from .dataflow import ATTENTION, GEMM, GEMV, ComputeOp, DataflowPlan, b200_split, build_dataflow
 from .errors import CapacityError, ConfigError, ShapeError
-from .fusion import (STYLE_MMA, STYLE_STRIDED, THRES_SHUFFLE, LayoutPair, MappingError,
-                     ShuffleSchedule, build_shuffle_schedule, choose_fusion_level)
+from .fusion import (B200_GEMV_MAX_ROWS, STYLE_MMA, STYLE_STRIDED, THRES_SHUFFLE, LayoutPair, MappingError,
+                     ShuffleSchedule, b200_fusion, build_shuffle_schedule, choose_fusion_level)
 from .gpumodel import GpuModel, KernelUsage, load_gpu_model
 from .report import SimReport
 
@@ -93,26 +93,54 @@ def plan_kernel(config: VQConfig, op: ComputeOp, model: Optional[GpuModel] = Non
                 kernel_usage: Optional[KernelUsage] = None, histogram=None, n_reg: Optional[int] = None,
                 n_shared: Optional[int] = None, split_factor: Optional[int] = None,
                 thres_shuffle: int = THRES_SHUFFLE) -> FusedPlans:
+    """FusedPlans for (config, op, model), the reference signature (sim.py:255-269).
+
+    Reference models (rtx4090, a40) get the reference's plans exactly. The b200
+    model gets the plan the sm_100a kernels launch with: tiers from the real
+    cubin's shared-memory slack and (if given) a measured access histogram
+    (cacheplan.plan_b200_tiers), the persistent kernels' split granularity
+    (dataflow.b200_split) and the kernel family's fusion level (fusion.b200_fusion).
+    ``run_fused_kernel`` turns every field into a launch parameter."""
     model = model or load_gpu_model("b200")
-    b200 = model.name == "b200"
-    if kernel_usage is not None:
-        usage = kernel_usage
-    elif b200:
-        usage = measured_usage(op.kind) or B200_KERNEL_USAGE[op.kind]
-    else:
-        usage = KERNEL_USAGE[op.kind]
-    slack = compute_slack(usage, model)
-    if b200:
-        # register tier reserved; shared tier in 128-byte replicated rows per entry
-        if n_reg is None:
-            n_reg = 0
-        if n_shared is None:
-            levels = config.residuals if op.kind != ATTENTION else 1
-            n_shared = n_reg + b200_shared_entries(slack[0], config.vector_size, config.n_entries, levels)
-    cache = plan_cache(_proto(config), histogram, slack, n_reg=n_reg, n_shared=n_shared)
-    flow = build_dataflow(config, op, model, split_factor=split_factor)
-    level, schedule = fusion_for(config, op, thres_shuffle)
+    if model.name != "b200":
+        usage = kernel_usage or KERNEL_USAGE[op.kind]
+        cache = plan_cache(_proto(config), histogram, compute_slack(usage, model), n_reg=n_reg, n_shared=n_shared)
+        flow = build_dataflow(config, op, model, split_factor=split_factor)
+        level, schedule = fusion_for(config, op, thres_shuffle)
+        return FusedPlans(cache, flow, level, schedule)
+    usage = kernel_usage or measured_usage(op.kind) or B200_KERNEL_USAGE[op.kind]
+    shared_slack, _ = compute_slack(usage, model)
+    levels = config.residuals if op.kind != ATTENTION else 1
+    reg, shared = plan_b200_tiers(config.n_entries, config.vector_size, levels, shared_slack,
+                                  histogram=histogram, n_reg=n_reg, n_shared=n_shared)
+    cache = CachePlan(reg, shared, config.n_entries, config.entry_bytes)
+    axis, f = b200_split(op, model.sm_count)
+    if split_factor is not None:
+        f = int(split_factor)
+    flow = build_dataflow(config, op, model, split_factor=None)
+    flow = DataflowPlan(flow.op_kind, flow.switch_axes, flow.global_reduce_axes, axis, f,
+                        dict(flow.region_tasks, **{axis: max(f, 1)}), flow.base_tiles, flow.temporal_axes,
+                        meta={"model": "b200", "split": "persistent-kernel granularity (dataflow.b200_split)"})
+    level = b200_fusion(op.kind, op.activation_rows)
+    schedule = None
+    if level == "register":
+        _, schedule = fusion_for(config, op, thres_shuffle)
     return FusedPlans(cache, flow, level, schedule)
+
+
+def launch_of(plans: FusedPlans, op: ComputeOp):
+    """VqbLaunch carrying every field of the plan the kernels read: n_reg (register
+    slots), n_shared (shared span; codes beyond it use the global tier),
+    split_axis/split_factor (M for the GEMV's stream-K granularity, T for the
+    attention's span split; splits over other axes are not a launch parameter of
+    these kernels and are dropped)."""
+    from .ops import launch_struct
+    L = launch_struct(plans)
+    ax = plans.dataflow_plan.split_axis
+    ok = (op.kind in (GEMV, GEMM) and ax == "M") or (op.kind == ATTENTION and ax == "T")
+    if not ok:
+        L.split_factor, L.split_axis = 0, 0
+    return L
 
 
 class B200Machine:
@@ -171,12 +199,7 @@ class B200Machine:
         if plans.cache_plan.n_entries != cfg.n_entries:
             raise ConfigError(f"cache plan over {plans.cache_plan.n_entries} entries used with "
                               f"{cfg.n_entries}-entry codebooks")
-        from .ops import launch_struct
-
-        L = launch_struct(plans)
-        if op.kind != GEMV or plans.dataflow_plan.split_axis != "M":
-            L.split_factor = 0  # only an M split maps onto the GEMV kernel's partition
-        L.split_axis = 0 if L.split_factor == 0 else L.split_axis
+        L = launch_of(plans, op)
         return self._execute(quantized, op, operands, L, plans, variant="o4")
 
     def run_variant(self, name: str, quantized, op: ComputeOp, operands: dict,
@@ -265,7 +288,14 @@ class B200Machine:
                 raise ShapeError(f"activation {ashape} does not match M={m}")
             wd = self.to_device(w)
             at, host = self._operand(a)
-            fn = vq_gemv if (op.kind == GEMV or (at.dim() == 2 and at.shape[0] <= 8)) else vq_gemm
+            # fusion level -> kernel family: "register" = lookups feed the consumer's
+            # registers (GEMV kernels, rows <= 8); "shared" = dequantized tiles staged
+            # in shared memory for tcgen05 (GEMM). One activation row always takes the
+            # GEMV (a 128-row MMA tile would be 1/128 used).
+            rows = 1 if at.dim() == 1 else at.shape[0]
+            gemv_ok = rows <= B200_GEMV_MAX_ROWS and rows in (1, 2, 4, 8)
+            use_gemv = op.kind == GEMV or (gemv_ok and (plans.fusion_level == "register" or rows == 1))
+            fn = vq_gemv if use_gemv else vq_gemm
             if ev:
                 ev[0].record()
             out = fn(wd, at, out_dtype=torch.float32, launch=L)

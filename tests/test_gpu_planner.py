@@ -1,0 +1,158 @@
+"""The planner drives the launch: every field of the B200
+FusedPlans changes what runs — n_shared the shared tier, n_reg the register tier,
+the split factor the persistent grid, the fusion level the kernel family — and
+the adaptive loop closes on the device: profile (GPU histogram) -> reorder
+(hottest-first, bit-exact) -> plan (mu + 3 sigma hot set -> register slots) ->
+launch."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+from conftest import O
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL_F16 = 1e-3
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda", 0)
+
+
+def _mods():
+    from paper_2503_02236_b200 import _native as N
+    from paper_2503_02236_b200.dataflow import ComputeOp
+    from paper_2503_02236_b200.gpumodel import load_gpu_model
+    from paper_2503_02236_b200.machine import B200Machine, plan_kernel
+    return N, ComputeOp, load_gpu_model("b200"), B200Machine, plan_kernel
+
+
+def _quip(m, n, seed, work=256, zipf=None, scramble=False):
+    from paper_2503_02236_b200.codec import Codebook, QuantizedTensor, VQConfig
+    cfg = VQConfig(8, 16, 1)
+    codes, books = O.synthetic_codes_books((m, n), 8, 16, 1, 1, seed, working_entries=work, zipf_s=zipf)
+    books = O.round_f16(books)
+    if scramble:  # hide the hot entries at random indices (a relabelling: same dense tensor)
+        perm = np.random.default_rng(seed).permutation(cfg.n_entries)
+        inv = np.argsort(perm)
+        codes = perm[codes].astype(np.int32)
+        books = books[:, inv]
+    q = QuantizedTensor(codes, (m, n), cfg, [Codebook(books[0], 0, 0)], 1)
+    dense = O.dequantize(codes, books, (m, n), 8, 1, np.zeros(m * n // 8, np.int32))
+    return cfg, q, dense
+
+
+def test_split_factor_sets_the_gemv_grid(dev):
+    N, ComputeOp, b200, B200Machine, plan_kernel = _mods()
+    m, n = 2048, 4096  # 16 column blocks of 256, 4 chunks of 512 rows
+    cfg, q, dense = _quip(m, n, 3)
+    op = ComputeOp.gemv(m, n)
+    mach = B200Machine()
+    x = O.round_f16(O.synthetic_tensor((m,), 4))
+    ref = O.matmul_ref(x, dense)
+    grids = []
+    for f in (1, 2, 4):
+        plans = plan_kernel(cfg, op, b200, split_factor=f)
+        assert plans.dataflow_plan.split_axis == "M" and plans.dataflow_plan.split_factor == f
+        out, rep = mach.run_fused_kernel(q, plans, op, {"activation": x})
+        assert rep.meta["kernel"] == "gemv_fast"
+        grids.append(N.last_launch()["grid"])
+        assert O.rel_err(out, ref) <= TOL_F16
+    assert grids == [16, 32, 64]
+    # the default B200 plan fills the machine: ceil(148 / 16) = 10 -> capped by the 4 chunks
+    plans = plan_kernel(cfg, op, b200)
+    assert plans.dataflow_plan.split_factor == 4
+    mach.run_fused_kernel(q, plans, op, {"activation": x})
+    assert N.last_launch()["grid"] == 64
+
+
+def test_shared_span_follows_the_plan(dev):
+    N, ComputeOp, b200, B200Machine, plan_kernel = _mods()
+    m, n = 1024, 2048
+    cfg, q, dense = _quip(m, n, 5)
+    op = ComputeOp.gemv(m, n)
+    mach = B200Machine()
+    x = O.round_f16(O.synthetic_tensor((m,), 6))
+    ref = O.matmul_ref(x, dense)
+    for ns in (64, 128, 256):
+        plans = plan_kernel(cfg, op, b200, n_shared=ns)
+        assert plans.cache_plan.n_shared == ns
+        out, _ = mach.run_fused_kernel(q, plans, op, {"activation": x})
+        assert N.last_launch()["n_shared"] == ns  # codes >= ns take the global tier
+        assert O.rel_err(out, ref) <= TOL_F16
+
+
+def test_fusion_level_selects_the_kernel_family(dev):
+    N, ComputeOp, b200, B200Machine, plan_kernel = _mods()
+    m, n, rows = 1024, 1024, 4
+    cfg, q, dense = _quip(m, n, 7)
+    op = ComputeOp.gemm(m, n, rows)
+    mach = B200Machine()
+    x = O.round_f16(O.synthetic_tensor((rows, m), 8))
+    ref = O.matmul_ref(x, dense)
+    plans = plan_kernel(cfg, op, b200)
+    assert plans.fusion_level == "register"  # rows <= 8: lookups straight into registers
+    out, rep = mach.run_fused_kernel(q, plans, op, {"activation": x})
+    assert rep.meta["kernel"] == "gemv_fast" and O.rel_err(out, ref) <= TOL_F16
+    shared = dataclasses.replace(plans, fusion_level="shared")  # stage tiles in smem for tcgen05
+    out, rep = mach.run_fused_kernel(q, shared, op, {"activation": x})
+    assert rep.meta["kernel"] == "gemm_tc" and O.rel_err(out, ref) <= 2e-3
+
+
+def test_attention_split_sets_the_grid(dev):
+    N, ComputeOp, b200, B200Machine, plan_kernel = _mods()
+    from paper_2503_02236_b200.codec import Codebook, QuantizedTensor, Sharing, VQConfig
+    B, H, T, C = 2, 4, 2048, 128
+    cfg = VQConfig(2, 8, 1, Sharing.per_channel_group(2))
+    nreg = O.n_regions_of((B, H, T, C), 2, "channel_group", group_width=2)
+    regs = O.region_ids((B, H, T, C), 2, "channel_group", group_width=2)
+    qs, dense = [], []
+    for seed in (11, 12):
+        codes, books = O.synthetic_codes_books((B, H, T, C), 2, 8, 1, nreg, seed)
+        books = O.round_f16(books)
+        qs.append(QuantizedTensor(codes, (B, H, T, C), cfg, [Codebook(books[i], 0, i) for i in range(nreg)], nreg))
+        dense.append(O.dequantize(codes, books, (B, H, T, C), 2, nreg, regs))
+    op = ComputeOp.attention_decode(B, H, T, C)
+    query = O.round_f16(O.synthetic_tensor((B, H, C), 13))
+    ref = O.attention_ref(query, dense[0], dense[1])
+    mach = B200Machine()
+    for f in (1, 2, 4):
+        plans = plan_kernel(cfg, op, b200, split_factor=f)
+        assert plans.dataflow_plan.split_axis == "T"
+        out, rep = mach.run_fused_kernel({"k": qs[0], "v": qs[1]}, plans, op, {"query": query})
+        assert rep.meta["kernel"] == "attn_cq"
+        assert N.last_launch()["grid"] == B * H * f
+        assert O.rel_err(out, ref) <= 2e-3
+
+
+def test_device_profile_reorder_plan_register_tier(dev):
+    """Zipf(1.2) codes with the hot entries scrambled across the book: the GPU
+    histogram + reorder restores hottest-first order without changing the tensor,
+    the planner's mu + 3 sigma rule opens register slots, and the GEMV runs with
+    them (register-tier kernel) at full parity."""
+    N, ComputeOp, b200, B200Machine, plan_kernel = _mods()
+    from paper_2503_02236_b200.device import DeviceVQTensor
+    from paper_2503_02236_b200.ops import vq_dequantize, vq_gemv
+    from paper_2503_02236_b200.profiling import device_histograms, reorder_device
+    m, n = 2048, 4096
+    cfg, q, dense = _quip(m, n, 21, zipf=1.2, scramble=True)
+    w = DeviceVQTensor.from_quantized(q, device=dev)
+    w2, counts, fwd = reorder_device(w)
+    assert torch.equal(vq_dequantize(w2), vq_dequantize(w))  # a relabelling: bit-exact
+    hist = device_histograms(counts)[0]
+    assert (np.diff(hist.counts) <= 0).all()
+    plans = plan_kernel(cfg, ComputeOp.gemv(m, n), b200, histogram=hist)
+    assert plans.cache_plan.n_reg == 4
+    from paper_2503_02236_b200.machine import launch_of
+    L = launch_of(plans, ComputeOp.gemv(m, n))
+    x = O.round_f16(O.synthetic_tensor((m,), 22))
+    xt = torch.from_numpy(x).to(dev).half()
+    y = vq_gemv(w2, xt, out_dtype=torch.float32, launch=L)
+    assert N.last_kernel() == "gemv_fast" and N.last_launch()["n_reg"] == 4
+    assert O.rel_err(y.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
+    # without a histogram the plan keeps the register tier closed
+    assert plan_kernel(cfg, ComputeOp.gemv(m, n), b200).cache_plan.n_reg == 0
