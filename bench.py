@@ -485,6 +485,95 @@ def time_gemv_shapes(torch, dev, N, cfg, shapes, work=None, rows=1):
     return out
 
 
+def time_zipf(torch, dev, N, m=4096, n=12288, copies=12):
+    """Adaptive codebook placement on skewed codes (SURVEY §8d variant: Zipf(1.2)
+    + reorder_all, V/cli.py:204-223): quip VQ<8,16,1> qkv-shaped GEMVs, batch 1,
+    graph replays over > L2 of distinct weights.
+
+    full_book:   Zipf over all 2^16 entries with the hot entries scattered (the
+                 trained order), shared tier = the planned span; vs the same
+                 weights after the device profile + reorder (hot entries first,
+                 so the shared span catches most lookups; the rest use L2)
+    working_set: Zipf over a 256-entry working set, reordered: register tier off
+                 vs the planner's mu + 3 sigma register slots."""
+    from paper_2503_02236_b200.codec import VQConfig
+    from paper_2503_02236_b200.dataflow import ComputeOp
+    from paper_2503_02236_b200.device import DeviceVQTensor
+    from paper_2503_02236_b200.gpumodel import load_gpu_model
+    from paper_2503_02236_b200.machine import launch_of, plan_kernel
+    from paper_2503_02236_b200.ops import workspace
+    from paper_2503_02236_b200.profiling import device_histograms, reorder_device
+
+    cfg = VQConfig(8, 16, 1)
+    b200 = load_gpu_model("b200")
+    op = ComputeOp.gemv(m, n)
+    hbm, _ = peaks()
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    lib = N.lib()
+
+    def zipf_codes(hi, count):
+        p = 1.0 / torch.arange(1, hi + 1, device=dev, dtype=torch.float64) ** 1.2
+        return torch.multinomial((p / p.sum()).float(), count, replacement=True, generator=g).to(torch.int32)
+
+    def make(hi, scramble):
+        ws = []
+        for _ in range(copies):
+            codes = zipf_codes(hi, m * n // 8)
+            if scramble:
+                codes = torch.randperm(1 << 16, device=dev, generator=g).to(torch.int32)[codes]
+            books = (torch.randn((1, 1 << 16, 8), generator=g, device=dev) * 0.1).half()
+            ws.append(DeviceVQTensor.from_device_codes(codes.view(1, -1), (m, n), cfg, books).relayout("gemv"))
+        return ws
+
+    def timed(ws, L):
+        x = torch.randn((m,), device=dev).half()
+        ys = [torch.empty((n,), device=dev, dtype=torch.float16) for _ in ws]
+        structs = [w.struct() for w in ws]
+        need = max(N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMV, st, 1, L)) for st in structs)
+        buf = workspace(need, dev)
+
+        def run():
+            st_ = torch.cuda.current_stream(dev).cuda_stream
+            for st, y in zip(structs, ys):
+                N.check(lib.vqb_gemv(st, x.data_ptr(), N.F16, 1, y.data_ptr(), N.F16, L, buf.data_ptr(),
+                                     buf.numel(), st_))
+
+        us = graph_time(torch, run, 10) / len(ws)
+        info = N.last_launch()
+        alg = ws[0].algorithmic_bytes(256) + (m + n) * 2
+        return {"us_per_call": round(us, 2), "GB_s": round(alg / us / 1e3, 1), "frac": round(alg / us / 1e3 / hbm, 3),
+                "n_shared": info["n_shared"], "n_reg": info["n_reg"]}
+
+    out = {"config": f"quip VQ<8,16,1> {m}x{n} b1, Zipf(1.2) codes"}
+    ws = make(1 << 16, scramble=True)
+    plans = plan_kernel(cfg, op, b200)
+    res = {"trained_order": timed(ws, launch_of(plans, op))}
+    ro = [reorder_device(w) for w in ws]
+    ws2 = [r[0] for r in ro]
+    hist = device_histograms(ro[0][1])[0]
+    ns = plans.cache_plan.n_shared
+    res["reordered"] = timed(ws2, launch_of(plans, op))
+    # lookups served by the shared span [0, ns) before (old index < ns) and after reordering
+    sorted_counts, fwd = ro[0][1][0, 0], ro[0][2][0, 0]
+    res["shared_hit_fraction_trained"] = round(float(sorted_counts[fwd[:ns]].sum()) / hist.total, 4)
+    res["shared_hit_fraction_reordered"] = round(float(hist.counts[:ns].sum()) / hist.total, 4)
+    out["full_book"] = res
+    del ws, ws2, ro
+    ws = [reorder_device(w)[0] for w in make(256, scramble=True)]
+    _, counts, _ = reorder_device(ws[0])
+    hist = device_histograms(counts)[0]
+    hot = plan_kernel(cfg, op, b200, histogram=hist).dataflow_plan.meta["hot_register_slots"]
+    planned = plan_kernel(cfg, op, b200, histogram=hist, n_reg=hot)  # the paper's mu + 3 sigma slots
+    off = plan_kernel(cfg, op, b200, histogram=hist, n_reg=0)
+    out["working_set"] = {"hot_register_slots": hot,
+                          "register_tier_off": timed(ws, launch_of(off, op)),
+                          "register_tier_planned": timed(ws, launch_of(planned, op))}
+    del ws
+    torch.cuda.empty_cache()
+    return out
+
+
 LLAMA65B = [("q", 8192, 8192), ("up", 8192, 22016), ("down", 22016, 8192)]
 
 
@@ -639,6 +728,8 @@ def run_impl(args):
                 extra["gemm_c2_prefill"] = time_gemm(
                     torch, dev, N, "C2 quip2 VQ<8,16,1> ws256 llama7b prefill rows 1024", VQConfig(8, 16, 1),
                     LLAMA7B, work=WORK)
+            if want("zipf"):
+                extra["zipf_adaptive_cache"] = time_zipf(torch, dev, N)
             if want("c3"):
                 extra["c3_aqlm65b"] = time_c3(torch, dev, N)
             if want("gemv_c2"):

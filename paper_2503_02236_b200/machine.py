@@ -118,9 +118,12 @@ def plan_kernel(config: VQConfig, op: ComputeOp, model: Optional[GpuModel] = Non
     if split_factor is not None:
         f = int(split_factor)
     flow = build_dataflow(config, op, model, split_factor=None)
+    from .cacheplan import hot_register_slots
     flow = DataflowPlan(flow.op_kind, flow.switch_axes, flow.global_reduce_axes, axis, f,
                         dict(flow.region_tasks, **{axis: max(f, 1)}), flow.base_tiles, flow.temporal_axes,
-                        meta={"model": "b200", "split": "persistent-kernel granularity (dataflow.b200_split)"})
+                        meta={"model": "b200", "split": "persistent-kernel granularity (dataflow.b200_split)",
+                              "hot_entries": (int(histogram.hot_set().size) if histogram is not None else None),
+                              "hot_register_slots": hot_register_slots(histogram)})
     level = b200_fusion(op.kind, op.activation_rows)
     schedule = None
     if level == "register":

@@ -146,6 +146,12 @@ def test_device_profile_reorder_plan_register_tier(dev):
     hist = device_histograms(counts)[0]
     assert (np.diff(hist.counts) <= 0).all()
     plans = plan_kernel(cfg, ComputeOp.gemv(m, n), b200, histogram=hist)
+    # the paper's rule finds the hot prefix; on B200 the register tier was measured not
+    # to pay (cacheplan.REGISTER_TIER_PAYS), so the default plan keeps it closed ...
+    assert plans.dataflow_plan.meta["hot_register_slots"] == 4 and plans.cache_plan.n_reg == 0
+    # ... and the register-tier kernel runs when a plan asks for it
+    plans = plan_kernel(cfg, ComputeOp.gemv(m, n), b200, histogram=hist,
+                        n_reg=plans.dataflow_plan.meta["hot_register_slots"])
     assert plans.cache_plan.n_reg == 4
     from paper_2503_02236_b200.machine import launch_of
     L = launch_of(plans, ComputeOp.gemv(m, n))
@@ -154,5 +160,4 @@ def test_device_profile_reorder_plan_register_tier(dev):
     y = vq_gemv(w2, xt, out_dtype=torch.float32, launch=L)
     assert N.last_kernel() == "gemv_fast" and N.last_launch()["n_reg"] == 4
     assert O.rel_err(y.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
-    # without a histogram the plan keeps the register tier closed
-    assert plan_kernel(cfg, ComputeOp.gemv(m, n), b200).cache_plan.n_reg == 0
+    assert plan_kernel(cfg, ComputeOp.gemv(m, n), b200).dataflow_plan.meta["hot_register_slots"] == 0
