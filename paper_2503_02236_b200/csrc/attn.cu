@@ -219,30 +219,48 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     for (int j = 0; j < GPL; ++j)
 #pragma unroll
       for (int c = 0; c < V; ++c) acc[j][c] *= corr;
-    return (uint32_t)__half_as_ushort(__float2half_rn(p));
+    const uint32_t ph = (uint32_t)__half_as_ushort(__float2half_rn(p));
+    return ph | (ph << 16);  // (p, p) for the fp16x2 V accumulation
   };
-  // V phase: slot i holds token i ^ lane, whose probability lives on that lane
+  // V phase: slot i holds token i ^ lane, whose probability lives on that lane.
+  // p * V accumulates in packed fp16x2 windows of 8 tokens (HFMA2, full rate; the
+  // mixed-precision fp32 FMA is quarter rate), flushed into the fp32 accumulators
+  // with an exact widening FMA — the GEMV's windowing, at attention's 2e-3 bound.
   auto vphase = [&](const uint4 (&vc)[Q], uint32_t ph) {
+    constexpr int HW = V / 2;  // fp16x2 words per entry
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const uint16_t pk = (uint16_t)__shfl_sync(0xffffffffu, ph, i ^ lane);
+    for (int w8 = 0; w8 < 4; ++w8) {
+      uint32_t hw[GPL][HW];
 #pragma unroll
-      for (int j = 0; j < GPL; ++j) {
-        const int byte = i * GPL + j;
-        const uint32_t w = (&vc[byte / 16].x)[(byte % 16) / 4];
-        const uint32_t addr = row_addr<G * EPB, PRMT>(w, byte % 4, cbV[j], colV[j], vbook_base);
-        if constexpr (V == 2) {
-          const uint32_t e = lds32(addr);
-          acc[j][0] = fma_h((uint16_t)(e & 0xffff), pk, acc[j][0]);
-          acc[j][1] = fma_h((uint16_t)(e >> 16), pk, acc[j][1]);
-        } else {
-          const uint2 e = lds64(addr);
-          acc[j][0] = fma_h((uint16_t)(e.x & 0xffff), pk, acc[j][0]);
-          acc[j][1] = fma_h((uint16_t)(e.x >> 16), pk, acc[j][1]);
-          acc[j][2] = fma_h((uint16_t)(e.y & 0xffff), pk, acc[j][2]);
-          acc[j][3] = fma_h((uint16_t)(e.y >> 16), pk, acc[j][3]);
+      for (int j = 0; j < GPL; ++j)
+#pragma unroll
+        for (int c = 0; c < HW; ++c) hw[j][c] = 0u;
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii) {
+        const int i = w8 * 8 + ii;
+        const uint32_t pp = (uint32_t)__shfl_sync(0xffffffffu, ph, i ^ lane);
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+          const int byte = i * GPL + j;
+          const uint32_t w = (&vc[byte / 16].x)[(byte % 16) / 4];
+          const uint32_t addr = row_addr<G * EPB, PRMT>(w, byte % 4, cbV[j], colV[j], vbook_base);
+          if constexpr (V == 2) {
+            const uint32_t e = lds32(addr);
+            asm("fma.rn.f16x2 %0, %1, %2, %0;" : "+r"(hw[j][0]) : "r"(e), "r"(pp));
+          } else {
+            const uint2 e = lds64(addr);
+            asm("fma.rn.f16x2 %0, %1, %2, %0;" : "+r"(hw[j][0]) : "r"(e.x), "r"(pp));
+            asm("fma.rn.f16x2 %0, %1, %2, %0;" : "+r"(hw[j][1]) : "r"(e.y), "r"(pp));
+          }
         }
       }
+#pragma unroll
+      for (int j = 0; j < GPL; ++j)
+#pragma unroll
+        for (int c = 0; c < HW; ++c) {
+          acc[j][2 * c] = fma_h((uint16_t)(hw[j][c] & 0xffff), (uint16_t)0x3C00, acc[j][2 * c]);
+          acc[j][2 * c + 1] = fma_h((uint16_t)(hw[j][c] >> 16), (uint16_t)0x3C00, acc[j][2 * c + 1]);
+        }
     }
   };
   auto load_k = [&](uint4 (&kc)[Q], int t0) {
@@ -644,7 +662,7 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
     configured[dev & 63] = true;
   }
   const int U = a.B * a.H * (a.len_ptr ? a.NT_cap : a.NT);  // a device length is bounded by the capacity
-  int grid = std::min(U, sm_count());
+  int grid = balanced_grid(U, sm_count());
   if (grid_limit > 0) grid = std::min(grid, grid_limit);
   VQB_CUDA_CHECK(launch_pdl(kern, dim3(grid), dim3(kAttnThreads), smem, st, a));
   set_kernel("attn_cq");

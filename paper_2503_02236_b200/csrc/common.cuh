@@ -28,6 +28,15 @@ int set_error(int code, const char* fmt, ...);
 int cuda_error(cudaError_t e, const char* what);
 int sm_count();
 void set_kernel(const char* name);
+// Persistent grid for `units` equal work units: the fewest CTAs that still give the
+// minimal per-CTA load ceil(units / SMs). Same makespan as one CTA per SM, but
+// every CTA gets the same whole number of units (no CTA waits on a longer
+// neighbour, fewer split outputs / codebook switches).
+inline int balanced_grid(int64_t units, int sms) {
+  if (units <= 0) return 1;
+  const int64_t per = (units + sms - 1) / sms;
+  return (int)((units + per - 1) / per);
+}
 // grid, threads, shared-tier entries and register-tier entries of the last fused launch
 void set_launch(int grid, int threads, int n_shared, int n_reg);
 

@@ -915,7 +915,7 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
   if (occ < 1) return set_error(VQB_ECAPACITY, "GEMV plan (n_shared=%d) does not fit one CTA per SM", p.n_sh);
   // one persistent CTA per SM: every CTA is resident (a finishing CTA polls the
   // partials of later CTAs) and the SM's second slot is left to the next kernel
-  int grid = std::min(p.n_cblk * p.n_chunks, sm_count());
+  int grid = balanced_grid((int64_t)p.n_cblk * p.n_chunks, sm_count());
   // the planner's split of the reduction over M: each column block is shared by
   // ~split_factor CTAs of the stream-K schedule
   if (L && L->split_axis == 'M' && L->split_factor > 0) grid = std::max(1, std::min(grid, p.n_cblk * L->split_factor));
@@ -1126,7 +1126,7 @@ int gemv_grouped_dispatch(const VqbTensor* ws_t, int n, const void* const* xs, i
   a.total_units = units;
   a.n_probs = n;
   uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
-  int grid = std::min(units, sm_count());
+  int grid = balanced_grid(units, sm_count());
   if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
   if ((int64_t)grid * rows * 256 * 8 > VQB_WS_COUNTER_BYTES - 65536)
     return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
