@@ -351,11 +351,16 @@ def time_gemv_single(torch, dev, ops, N, label, cfg_args, shape, work=None):
             "fp16_cublas_us": dense_us, "note": "CUDA graphs over > L2 of distinct weights (both arms)"}
 
 
-def time_decode(torch, dev, batch=1, ctx=4096, reps=10):
+def time_decode(torch, dev, batch=1, ctx=4096, reps=10, tp=False):
     """C5: end-to-end Llama-7B-shaped decode step (VQ weights + CQ-4 KV cache), one
-    CUDA graph per step at a context of `ctx` cached tokens."""
+    CUDA graph per step at a context of `ctx` cached tokens. tp=True: this rank's
+    Megatron shard (heads / ffn slice, NCCL all-reduce after o and down, captured
+    in the graph)."""
     from paper_2503_02236_b200.decode import LlamaShape, VQLlamaDecoder
     dec = VQLlamaDecoder.synthetic(LlamaShape(), batch, ctx, dev, seed=3)
+    if tp:
+        dec = VQLlamaDecoder.tensor_parallel(dec, None)
+        torch.cuda.empty_cache()
     dec.set_length(ctx - 1 - reps - 3)
     dec.capture()
     for _ in range(3):
@@ -370,7 +375,12 @@ def time_decode(torch, dev, batch=1, ctx=4096, reps=10):
     ms = e0.elapsed_time(e1) / reps
     del dec
     torch.cuda.empty_cache()
-    return {"config": f"C5 llama7b decode quip2 weights + cq4 KV, batch {batch}, ctx {ctx}", "batch": batch,
+    if tp:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t[0])
+    return {"config": f"C5 llama7b decode quip2 weights + cq4 KV, batch {batch}, ctx {ctx}"
+                      + (f", tp{dec.world}" if tp else ""), "batch": batch,
             "ms_per_step": ms, "tokens_per_s": batch * 1e3 / ms, "data": "synthetic weights/KV (random init)"}
 
 
@@ -701,6 +711,9 @@ def run_impl(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_ms, ms_single = float(t[0]), float(t[1]), float(t[2])
 
+    decode_tp = None
+    if world > 1 and not args.no_extra:
+        decode_tp = [time_decode(torch, dev, b, tp=True) for b in (1, 16, 64)]  # C5 at N GPUs
     if rank == 0:
         hbm, src = peaks()
         total_bytes = step_bytes * world
@@ -708,6 +721,8 @@ def run_impl(args):
         extra = {}
         if per_linear:
             extra["per_linear"] = per_linear
+        if decode_tp:
+            extra["decode_c5"] = decode_tp
         extra["step_per_launch"] = {
             "what": "the same step as 128 single-linear gemv_fast launches (the per-call kernel of a decode loop)",
             "ms_per_step": ms_single, "GB_s": total_bytes / (ms_single * 1e-3) / 1e9,

@@ -23,7 +23,7 @@ from .codec import Sharing, VQConfig
 from . import _native as N
 from . import ops
 from .device import DeviceVQTensor
-from .errors import CapacityError
+from .errors import CapacityError, ConfigError
 
 
 @dataclass(frozen=True)
@@ -56,7 +56,7 @@ class DecoderLayer:
 
 class VQLlamaDecoder:
     def __init__(self, shape: LlamaShape, layers, embed: torch.Tensor, final_norm: torch.Tensor,
-                 lm_head: torch.Tensor, batch: int):
+                 lm_head: torch.Tensor, batch: int, group=None, tp_world: int = 1):
         self.shape = shape
         self.layers = list(layers)
         self.embed = embed          # (vocab, hidden) fp16
@@ -64,6 +64,11 @@ class VQLlamaDecoder:
         self.lm_head = lm_head      # (hidden, vocab) fp16: logits = x @ lm_head
         self.batch = batch
         self.device = embed.device
+        # tensor parallelism (Megatron): this rank holds heads [h0, h1) of qkv / the KV
+        # caches and its slice of ffn; o and down are row-parallel and all-reduced
+        self.group = group           # None = the default process group when tp_world > 1
+        self.world = int(tp_world)
+        self.local_heads = self.layers[0].k_cache.shape[1] if self.layers else shape.heads
         self.d_len = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.tokens = torch.zeros(batch, dtype=torch.int64, device=self.device)
         self.res = torch.zeros((batch, shape.hidden), dtype=torch.float16, device=self.device)
@@ -114,6 +119,46 @@ class VQLlamaDecoder:
             return ops.vq_gemv(w, x, out_dtype=torch.float16)
         return ops.vq_gemm(w, x, out_dtype=torch.float16)
 
+    def _reduce(self, y: torch.Tensor) -> torch.Tensor:
+        """Sum a row-parallel linear's partial output over the TP group."""
+        if self.world > 1:
+            torch.distributed.all_reduce(y, group=self.group)
+        return y
+
+    @classmethod
+    def tensor_parallel(cls, full: "VQLlamaDecoder", group, rank: int = None, world: int = None) -> "VQLlamaDecoder":
+        """This rank's shard of a decoder (same weights): qkv columns of heads
+        [h0, h1) for q, k and v, o rows of those heads, gate/up columns of ffn slice
+        [f0, f1), down rows of it, KV caches (and their per-head CQ books) of the
+        local heads. Embedding, norms and LM head are replicated."""
+        from .tp import device_shard
+        if world is None:
+            world, rank = torch.distributed.get_world_size(group), torch.distributed.get_rank(group)
+        sh = full.shape
+        if sh.heads % world or sh.ffn % world:
+            raise ConfigError(f"heads {sh.heads} / ffn {sh.ffn} not divisible by tensor-parallel size {world}")
+        hl, fl, c, d = sh.heads // world, sh.ffn // world, sh.head_dim, sh.hidden
+        h0, f0 = rank * hl, rank * fl
+        hcols = [(part * d + h0 * c, part * d + (h0 + hl) * c) for part in range(3)]
+        layers = []
+        for L in full.layers:
+            groups = c // KV_CFG.vector_size
+
+            def cache(src):
+                books = src.codebooks[h0 * groups:(h0 + hl) * groups].contiguous()
+                return DeviceVQTensor.empty_cache((full.batch, hl, src.shape[2], c), KV_CFG, books)
+
+            layers.append(DecoderLayer(
+                device_shard(L.qkv, col_ranges=hcols), device_shard(L.o, rows=(h0 * c, (h0 + hl) * c)),
+                device_shard(L.gate_up, col_ranges=[(f0, f0 + fl), (sh.ffn + f0, sh.ffn + f0 + fl)]),
+                device_shard(L.down, rows=(f0, f0 + fl)), L.attn_norm, L.ffn_norm, cache(L.k_cache),
+                cache(L.v_cache)))
+        # the collectives run only in a real process group (rank / world given without
+        # one emulate a shard, e.g. to check it in a single process)
+        live = torch.distributed.is_initialized()
+        return cls(sh, layers, full.embed, full.final_norm, full.lm_head, full.batch, group=group,
+                   tp_world=world if live else 1)
+
     def step(self) -> torch.Tensor:
         """One decode step for the current tokens; returns (and stores) the next ones.
         Device-side only (capturable): the length counter advances first, so every
@@ -132,16 +177,16 @@ class VQLlamaDecoder:
         ops.add_len(self.d_len, 1)
         self.res.copy_(torch.index_select(self.embed, 0, self.tokens))
         x = None
-        hc = sh.heads * sh.head_dim
+        hc = self.local_heads * sh.head_dim
         for L in self.layers:
             xn = ops.rmsnorm(x, self.res, L.attn_norm, sh.eps)
             qkv = self._linear(L.qkv, xn)
             q = ops.qkv_rope_append(qkv, L.k_cache, L.v_cache, self.d_len, sh.rope_theta)
             a = ops.vq_attention(L.k_cache, L.v_cache, q, out_dtype=torch.float16, d_len=self.d_len)
-            o = self._linear(L.o, a.view(b, hc))
+            o = self._reduce(self._linear(L.o, a.view(b, hc)))
             xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)
             gu = self._linear(L.gate_up, xn)
-            x = self._linear(L.down, ops.silu_mul(gu))
+            x = self._reduce(self._linear(L.down, ops.silu_mul(gu)))
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
         self.tokens.copy_(torch.argmax(self.logits, dim=-1))

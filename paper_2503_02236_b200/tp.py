@@ -121,6 +121,55 @@ def shard_heads(q: QuantizedTensor, rank: int, world: int) -> QuantizedTensor:
     return QuantizedTensor(codes, shape, q.config, books, nreg)
 
 
+def _backend(group) -> str:
+    try:
+        return dist.get_backend(group)
+    except Exception:  # pragma: no cover
+        return "nccl"
+
+
+def all_gather_into(out: torch.Tensor, y: torch.Tensor, group=None) -> None:
+    """all_gather_into_tensor (NCCL); gloo (the CPU / single-GPU multi-process tests)
+    gathers into a list and concatenates."""
+    if _backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, y, group=group)
+        return
+    parts = list(out.view((dist.get_world_size(group),) + tuple(y.shape)).unbind(0))
+    dist.all_gather(parts, y, group=group)
+
+
+def device_shard(w, rows=None, col_ranges=None):
+    """Shard of a device-resident 2-D weight with a whole-tensor codebook (replicated):
+    input rows [r0, r1) and/or the concatenation of output column ranges
+    [(c0, c1), ...] — e.g. one rank's q | k | v head columns of a fused qkv weight.
+    Done on the GPU from the plain codes; returns a DeviceVQTensor in the input's layout."""
+    from .device import DeviceVQTensor
+    cfg = w.config
+    if cfg.sharing.kind != "whole" or len(w.shape) != 2:
+        raise ConfigError("device_shard handles 2-D weights with whole-tensor codebooks")
+    m, n = w.shape
+    v = cfg.vector_size
+    plain = w.relayout("plain")
+    s = m * n // v
+    if cfg.log2_entries <= 8:
+        codes = plain.codes[: cfg.residuals * s].view(cfg.residuals, m, n // v).to(torch.int32)
+    else:
+        codes = (plain.codes[: 2 * cfg.residuals * s].view(torch.int16).to(torch.int32) & 0xFFFF).view(
+            cfg.residuals, m, n // v)
+    r0, r1 = rows if rows is not None else (0, m)
+    codes = codes[:, r0:r1]
+    if col_ranges is not None:
+        for c0, c1 in col_ranges:
+            if c0 % v or c1 % v:
+                raise ConfigError(f"column range ({c0}, {c1}) is not on a sub-vector boundary")
+        codes = torch.cat([codes[:, :, c0 // v:c1 // v] for c0, c1 in col_ranges], dim=2)
+    shape = (r1 - r0, codes.shape[2] * v)
+    out = DeviceVQTensor.from_device_codes(codes.reshape(cfg.residuals, -1).contiguous(), shape, cfg,
+                                           w.codebooks, layout="plain")
+    out.max_code = w.max_code
+    return out if w.layout == "plain" else out.relayout(w.layout)
+
+
 def _default_linear(w, x):
     from .device import DeviceVQTensor
     from .ops import vq_gemm, vq_gemv
@@ -167,7 +216,7 @@ class TPLinear:
         if self.mode == "column":
             y = self.compute(self.weight, x).contiguous()
             out = torch.empty((world * y.shape[0],) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
-            dist.all_gather_into_tensor(out, y, group=self.group)
+            all_gather_into(out, y, group=self.group)
             out = out.view((world,) + tuple(y.shape))
             # (world, ..., N/world) -> (..., N)
             return torch.movedim(out, 0, -2).reshape(tuple(y.shape[:-1]) + (world * y.shape[-1],))
@@ -206,7 +255,7 @@ class TPAttention:
         qs = q[:, rank * h_local:(rank + 1) * h_local].contiguous()
         o = self.compute(self.k, self.v, qs).contiguous()
         out = torch.empty((world * o.shape[0],) + tuple(o.shape[1:]), dtype=o.dtype, device=o.device)
-        dist.all_gather_into_tensor(out, o, group=self.group)
+        all_gather_into(out, o, group=self.group)
         out = out.view((world,) + tuple(o.shape))
         return torch.movedim(out, 0, 1).reshape(o.shape[0], world * h_local, o.shape[2])
 
