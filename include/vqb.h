@@ -128,6 +128,13 @@ typedef struct VqbLaunch {
                                     FMA, quarter rate) instead of 8-row fp16x2 windows */
 #define VQB_FLAG_NO_MMA 16       /* GEMV batch 4-8: CUDA-core FMAs instead of the tensor-core
                                     (mma.sync) inner product */
+#define VQB_FLAG_COOPERATIVE 64  /* GEMV / attention: cooperative launch. The split reduction's
+                                    finisher CTAs wait for partials of later CTAs, which needs
+                                    the whole (<= 1 CTA per SM) grid resident; the default launch
+                                    relies on that (grid <= SMs, occupancy checked) and on any
+                                    concurrent kernel finishing. With this flag the driver
+                                    guarantees co-residency (or the launch fails loudly) — for
+                                    streams that overlap with kernels waiting on this one. */
 
 /* Kernel resource usage (KernelUsage, gpumodel.py:30-36) measured with
  * cudaFuncGetAttributes on the loaded cubin. */

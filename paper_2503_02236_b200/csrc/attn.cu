@@ -651,7 +651,7 @@ int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH, const VqbLaunch* L) {
 }
 
 template <int V, int GPL>
-static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
+static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit, int flags) {
   auto kern = attn_cq_kernel<V, GPL>;
   constexpr size_t smem = AttnSmem<V, GPL>::total;
   static bool configured[64] = {false};
@@ -664,7 +664,15 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit) {
   const int U = a.B * a.H * (a.len_ptr ? a.NT_cap : a.NT);  // a device length is bounded by the capacity
   int grid = balanced_grid(U, sm_count());
   if (grid_limit > 0) grid = std::min(grid, grid_limit);
-  VQB_CUDA_CHECK(launch_pdl(kern, dim3(grid), dim3(kAttnThreads), smem, st, a));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  cfg.attrs = attr;
+  cfg.numAttrs = persistent_attrs(attr, flags);
+  VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
   set_kernel("attn_cq");
   set_launch(grid, kAttnThreads, 256, 0);
   return VQB_OK;
@@ -726,9 +734,9 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
       gl = gl > 0 ? std::min(gl, cap) : cap;
     }
     const int gpl = (int)(gk.gpr / 32);
-    if (gk.v == 2 && gpl == 2) return launch_attn_t<2, 2>(a, st, gl);
-    if (gk.v == 2 && gpl == 1) return launch_attn_t<2, 1>(a, st, gl);
-    if (gk.v == 4 && gpl == 1) return launch_attn_t<4, 1>(a, st, gl);
+    if (gk.v == 2 && gpl == 2) return launch_attn_t<2, 2>(a, st, gl, L ? L->flags : 0);
+    if (gk.v == 2 && gpl == 1) return launch_attn_t<2, 1>(a, st, gl, L ? L->flags : 0);
+    if (gk.v == 4 && gpl == 1) return launch_attn_t<4, 1>(a, st, gl, L ? L->flags : 0);
     return set_error(VQB_ECONFIG, "no fast attention instance for this configuration");
   }
   float* kd = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);

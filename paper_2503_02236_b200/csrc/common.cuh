@@ -282,6 +282,23 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Launch attributes of the persistent split-reduction kernels: programmatic
+// dependent launch (unless VQB_FLAG_NO_PDL) and, with VQB_FLAG_COOPERATIVE, a
+// cooperative launch (co-residency of the whole grid guaranteed by the driver).
+inline int persistent_attrs(cudaLaunchAttribute* attr, int flags) {
+  int n = 0;
+  if (flags & VQB_FLAG_COOPERATIVE) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  } else if (!(flags & VQB_FLAG_NO_PDL)) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  return n;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -925,11 +925,9 @@ static int launch_gemv_kernel(GemvKernel kernel, const FastPlan& p, const GemvFa
   cfg.blockDim = dim3(p.threads);
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
-  cfg.numAttrs = (L && (L->flags & VQB_FLAG_NO_PDL)) ? 0 : 1;
+  cfg.numAttrs = persistent_attrs(attr, L ? L->flags : 0);
   VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, a));
   set_kernel("gemv_fast");
   set_launch(grid, p.threads, p.n_sh, p.n_reg);
@@ -1152,11 +1150,9 @@ int gemv_grouped_dispatch(const VqbTensor* ws_t, int n, const void* const* xs, i
   cfg.blockDim = dim3(p0.threads);
   cfg.dynamicSmemBytes = p0.smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
-  cfg.numAttrs = (L && (L->flags & VQB_FLAG_NO_PDL)) ? 0 : 1;
+  cfg.numAttrs = persistent_attrs(attr, L ? L->flags : 0);
   VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, a, table));
   set_kernel("gemv_group");
   set_launch(grid, p0.threads, p0.n_sh, 0);

@@ -103,3 +103,52 @@ def test_decoder_refuses_to_step_past_capacity(dev):
         dec.replay()
     dec.check_device_errors()
     assert int(dec.d_len.item()) == 64
+
+
+def _quip_weight(dev, m=4096, n=12288, seed=3):
+    from paper_2503_02236_b200.codec import VQConfig
+    from paper_2503_02236_b200.device import DeviceVQTensor
+    g = torch.Generator(device=dev).manual_seed(seed)
+    codes = torch.randint(0, 256, (1, m * n // 8), generator=g, device=dev, dtype=torch.int32)
+    books = (torch.randn((1, 1 << 16, 8), generator=g, device=dev) * 0.1).half()
+    return DeviceVQTensor.from_device_codes(codes, (m, n), VQConfig(8, 16, 1), books).relayout("gemv")
+
+
+def test_cooperative_launch_matches_default(dev, long_cache):
+    """VQB_FLAG_COOPERATIVE (driver-guaranteed co-residency of the persistent grid)
+    gives the same results as the default PDL launch."""
+    from paper_2503_02236_b200 import _native as N
+    from paper_2503_02236_b200 import ops
+    w = _quip_weight(dev)
+    x = torch.randn((1, 4096), device=dev).half()
+    coop = ops.launch_struct()
+    coop.flags |= N.FLAG_COOPERATIVE
+    assert torch.equal(ops.vq_gemv(w, x), ops.vq_gemv(w, x, launch=coop))
+    kd, vd, _, _ = long_cache
+    q = torch.randn((1, 32, 128), device=dev).half()
+    assert torch.equal(ops.vq_attention(kd, vd, q), ops.vq_attention(kd, vd, q, launch=coop))
+
+
+def test_concurrent_stream_holding_sms(dev, long_cache):
+    """The persistent kernels' finishers wait on later CTAs: with another stream's
+    kernels holding SMs they must still complete (the other work is finite) and
+    give the same results."""
+    from paper_2503_02236_b200 import ops
+    w = _quip_weight(dev)
+    kd, vd, _, _ = long_cache
+    x = torch.randn((1, 4096), device=dev).half()
+    q = torch.randn((1, 32, 128), device=dev).half()
+    y0, a0 = ops.vq_gemv(w, x), ops.vq_attention(kd, vd, q)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream(dev)
+    big = torch.randn((8192, 8192), device=dev).half()
+    with torch.cuda.stream(side):
+        for _ in range(12):
+            big = (big @ big).clamp_(-1, 1)
+    ys, as_ = [], []
+    for _ in range(30):
+        ys.append(ops.vq_gemv(w, x))
+        as_.append(ops.vq_attention(kd, vd, q))
+    torch.cuda.synchronize()
+    assert all(torch.equal(y, y0) for y in ys)
+    assert all(torch.equal(a, a0) for a in as_)
