@@ -128,6 +128,9 @@ typedef struct VqbLaunch {
                                     FMA, quarter rate) instead of 8-row fp16x2 windows */
 #define VQB_FLAG_NO_MMA 16       /* GEMV batch 4-8: CUDA-core FMAs instead of the tensor-core
                                     (mma.sync) inner product */
+#define VQB_FLAG_NO_PAIR 128     /* GEMM: the one-CTA tcgen05 kernel instead of the CTA-pair
+                                    (cta_group::2) kernel at prefill sizes */
+#define VQB_FLAG_PAIR_N128 256   /* GEMM: CTA-pair kernel with 256 x 128 tiles (N % 128) */
 #define VQB_FLAG_COOPERATIVE 64  /* GEMV / attention: cooperative launch. The split reduction's
                                     finisher CTAs wait for partials of later CTAs, which needs
                                     the whole (<= 1 CTA per SM) grid resident; the default launch

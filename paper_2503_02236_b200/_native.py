@@ -23,7 +23,9 @@ LAYOUT_PACKED, LAYOUT_GEMV_IL, LAYOUT_KV_IL, LAYOUT_PLAIN = 0, 1, 2, 3
 KERNEL_DEQUANT, KERNEL_GEMV, KERNEL_GEMM, KERNEL_ATTN = 0, 1, 2, 3
 FLAG_FORCE_GENERIC = 1
 FLAG_NO_MMA = 16  # GEMV batch 4-8 on CUDA-core FMAs instead of mma.sync
-FLAG_COOPERATIVE = 64  # cooperative launch: the driver guarantees the persistent grid is co-resident
+FLAG_COOPERATIVE = 64
+FLAG_NO_PAIR = 128  # GEMM: one-CTA tcgen05 kernel instead of the CTA-pair kernel
+FLAG_PAIR_N128 = 256  # GEMM: CTA-pair kernel with 256 x 128 tiles  # cooperative launch: the driver guarantees the persistent grid is co-resident
 
 _ERRORS = {
     ESHAPE: ShapeError,

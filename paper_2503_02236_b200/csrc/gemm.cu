@@ -382,6 +382,294 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair GEMM (tcgen05.mma.cta_group::2): a cluster of two CTAs on one TPC
+// computes a 256 x NT output tile with UMMA M = 256. Each CTA holds its 128 rows of
+// the X tile (TMA) and dequantises HALF of the W tile (NT / 2 columns) into its own
+// shared memory; the leader CTA's single thread issues one MMA per K=16 step that
+// reads A and B from both CTAs and writes each CTA's 128 x NT accumulator into its
+// own TMEM. Per SM and K stage that is 16 KB of A + NT / 2 x 64 x 2 B of B read by
+// the tensor core plus the same B bytes of dequantisation stores/gathers — half the
+// B-side shared-memory traffic per flop of the one-CTA kernel, whose 256 x 128 tile
+// reads its B tile once per 128-row half. Barriers: the leader's "full" barriers
+// count both CTAs' X bytes (cta_group::2 TMA) and both CTAs' dequant-warp arrivals
+// (remote mbarrier arrive through mapa); tcgen05.commit multicasts "empty" and the
+// final "TMEM full" to both CTAs.
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(addr), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Remote arrive on the leader's barrier. Default (.release.cta) semantics like
+// CUTLASS's 2-SM transform pipeline: the data is consumed by the pair's tensor core
+// (async proxy), ordered by the preceding fence.proxy.async; a .release.cluster arrive
+// costs a cluster-scope memory barrier per stage (measured: the dominant stall).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(bar)
+      : "memory");
+}
+
+constexpr int kPairRowsCta = 128;                  // X rows per CTA (UMMA M = 256 per pair)
+constexpr int kPairABytes = kPairRowsCta * kTileK * 2;  // 16 KB
+__host__ __device__ constexpr int pair_stages(int R) { return R == 1 ? 5 : 4; }
+__host__ __device__ constexpr size_t pair_smem(int R, int NT) {
+  return (size_t)R * kBookBytes + (size_t)pair_stages(R) * (kPairABytes + kTileK * (NT / 2) * 2) +
+         (3 * pair_stages(R) + 1) * 8 + 16;
+}
+
+template <int CBYTES, int R, bool BF16, typename OutT, int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
+  constexpr int CN = NT / 2;                        // W columns this CTA dequantises
+  constexpr int BBYTES = kTileK * CN * 2;
+  constexpr int RPL = 16 / CBYTES;
+  constexpr int WORDS = (kTileK / RPL) * (CN / 8);  // code words per level per stage (this CTA)
+  constexpr int STG = pair_stages(R);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* book = smem;
+  uint8_t* sa = smem + R * kBookBytes;
+  uint8_t* sb = sa + STG * kPairABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + STG * BBYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STG + 1);
+  const uint32_t full_a0 = smem_u32(bars), full_b0 = smem_u32(bars + STG);
+  const uint32_t empty0 = smem_u32(bars + 2 * STG), tmem_full = smem_u32(bars + 3 * STG);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int n_tiles_n = a.N / NT;
+  const int tile_n = pair % n_tiles_n, tile_m = pair / n_tiles_n;
+  const int row0 = tile_m * 2 * kPairRowsCta + (int)rank * kPairRowsCta;  // this CTA's X rows
+  const int n0 = tile_n * NT + (int)rank * CN;                            // this CTA's W columns
+  const int k_iters = a.M / kTileK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STG; ++s) {
+      mbar_init(full_a0 + 8 * s, 1);               // the leader's expect_tx (both CTAs' bytes)
+      mbar_init(full_b0 + 8 * s, 2 * kProdWarps);  // every dequant warp of the pair
+      mbar_init(empty0 + 8 * s, 1);                // multicast tcgen05.commit
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  for (int idx = tid; idx < R * a.n_sh; idx += kGemmThreads) {
+    const int r = idx / a.n_sh, e = idx - r * a.n_sh;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.books + ((int64_t)r * a.K + e) * 8));
+    uint8_t* row = book + ((size_t)r * kBookEntries + e) * 128;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(row + ((q + e) & 7) * 16) = v;
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer: this CTA's 128 X rows; bytes counted on the leader's barrier
+    if (lane == 0) {
+      for (int it = 0; it < k_iters; ++it) {
+        const int s = it % STG;
+        mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(full_a0 + 8 * s, 2 * kPairABytes);
+        tma_load_2d_pair(smem_u32(sa + s * kPairABytes), &tmap_x, it * kTileK, row0,
+                         mapa_rank(full_a0 + 8 * s, 0));
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA, one thread): UMMA 256 x NT x 16 over both CTAs
+    const uint32_t fmt = BF16 ? 1u : 0u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
+                           ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    if (rank == 0 && lane == 0) {
+      for (int it = 0; it < k_iters; ++it) {
+        const int s = it % STG;
+        const uint32_t ph = (it / STG) & 1;
+        mbar_wait(full_a0 + 8 * s, ph);
+        mbar_wait(full_b0 + 8 * s, ph);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sa + s * kPairABytes), b_base = smem_u32(sb + s * BBYTES);
+#pragma unroll
+        for (int k = 0; k < kTileK / 16; ++k) {
+          // B: this CTA's CN columns, MN-major SW128 atoms (8 K-rows x 64 columns, 1 KB);
+          // LBO = column-atom stride (1 KB), SBO = 8-row-group stride (CN / 64 KB)
+          const uint64_t bdesc = umma_desc(b_base + k * 2 * (CN / 64) * 1024, 1024, (CN / 64) * 1024);
+          const uint64_t adesc = umma_desc(a_base + k * 32, 16, 1024);
+          umma_f16_pair(tmem_base, adesc, bdesc, idesc, (it | k) != 0);
+        }
+        umma_commit_pair(empty0 + 8 * s);  // frees the stage in both CTAs
+      }
+      umma_commit_pair(tmem_full);
+    }
+  } else {
+    // ===== dequantisation producers: this CTA's CN columns of the W tile
+    const int dw = warp - 2;
+    const int dtid = dw * 32 + lane;
+    constexpr int NPT = kProdWarps * 32;
+    static_assert(WORDS * RPL % NPT == 0 && NPT % WORDS == 0, "producer split");
+    constexpr int KROWS = WORDS * RPL / NPT;
+    const int my_item = dtid % WORDS;
+    const int k_off = (dtid / WORDS) * KROWS;
+    const uint32_t full_b_leader = mapa_rank(full_b0, 0);
+    constexpr int PF = 6;  // code words requested 6 stages ahead (3: latency-bound)
+    uint4 ring[PF][R];
+    const int grp = my_item % (CN / 8), blk = my_item / (CN / 8);
+    const int gg = n0 / 8 + grp, cb = gg / 32, gi = gg % 32, wb = min(32, a.G - cb * 32);
+    auto fetch = [&](int it, uint4 (&cw)[R]) {
+      if (it < k_iters) {
+        const int64_t word = ((int64_t)cb * 32 * (a.M / RPL) + (int64_t)(it * kTileK / RPL + blk) * wb + gi) * 16;
+#pragma unroll
+        for (int r = 0; r < R; ++r) cw[r] = ldg_stream(a.codes + r * a.level_bytes + word);
+      }
+    };
+#pragma unroll
+    for (int p = 0; p < PF; ++p) fetch(p, ring[p]);
+    const int c = grp & 7, nb = grp >> 3;  // 16-byte chunk and 64-column atom
+    for (int it0 = 0; it0 < k_iters; it0 += PF)
+#pragma unroll
+      for (int pp = 0; pp < PF; ++pp) {
+        const int it = it0 + pp;
+        if (it >= k_iters) break;
+        const int s = it % STG;
+        uint4 cw[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) cw[r] = ring[pp][r];
+        fetch(it + PF, ring[pp]);
+        mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
+        uint8_t* btile = sb + s * BBYTES;
+        auto rows = [&](auto ko) {
+          constexpr int KO = decltype(ko)::value;
+#pragma unroll
+          for (int kk = 0; kk < KROWS; ++kk) {
+            const int k = KO + kk;
+            uint4 e;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              uint32_t code;
+              if constexpr (CBYTES == 2) {
+                const uint32_t w = (&cw[r].x)[k / 2];
+                code = (k & 1) ? (w >> 16) : (w & 0xffff);
+              } else {
+                const uint32_t w = (&cw[r].x)[k / 4];
+                code = (w >> (8 * (k % 4))) & 0xff;
+              }
+              const uint4 q = code < (uint32_t)a.n_sh
+                                  ? *reinterpret_cast<const uint4*>(book + ((size_t)r * kBookEntries + code) * 128 +
+                                                                     (lane & 7) * 16)
+                                  : __ldg(reinterpret_cast<const uint4*>(a.books + ((int64_t)r * a.K + code) * 8));
+              if (r == 0) {
+                e = q;
+              } else {
+                uint32_t* ew = &e.x;
+                const uint32_t* qw = &q.x;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if constexpr (BF16) {
+                    const __nv_bfloat162 h = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&ew[j]),
+                                                     *reinterpret_cast<const __nv_bfloat162*>(&qw[j]));
+                    ew[j] = *reinterpret_cast<const uint32_t*>(&h);
+                  } else {
+                    const __half2 h = __hadd2(*reinterpret_cast<const __half2*>(&ew[j]),
+                                              *reinterpret_cast<const __half2*>(&qw[j]));
+                    ew[j] = *reinterpret_cast<const uint32_t*>(&h);
+                  }
+                }
+              }
+            }
+            const int kr = blk * RPL + k;  // K-row within the stage
+            uint8_t* dst = btile + ((kr >> 3) * (CN / 64) + nb) * 1024 + (kr & 7) * 128 + ((c ^ (kr & 7)) << 4);
+            *reinterpret_cast<uint4*>(dst) = e;
+          }
+        };
+        dispatch_rows<0, RPL / KROWS, KROWS>(k_off / KROWS, rows);
+        fence_proxy_async();  // generic stores -> async proxy (the pair's tensor core)
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(full_b_leader + 8 * s);
+      }
+
+    // ===== epilogue: this CTA's 128 rows x NT columns of TMEM
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int quarter = warp & 3;
+    constexpr int CPW = (NT / 32) / (kProdWarps / 4);
+    const int cc0 = ((warp - 2) / 4) * CPW;
+    const int row = row0 + quarter * 32 + lane;
+    const int ncol0 = tile_n * NT;
+#pragma unroll
+    for (int c2 = 0; c2 < CPW; ++c2) {
+      const int cc = cc0 + c2;
+      uint32_t v[32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + cc * 32;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+            "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+            "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < a.rows) store_row32<OutT>(a.y, a.y_dtype, (int64_t)row * a.N + ncol0 + cc * 32, v);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs are done with the pair's shared memory and TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NT));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -484,6 +772,40 @@ static int launch_gemm_t(const CUtensorMap& map, const GemmArgs& a, int grid, cu
   return VQB_OK;
 }
 
+template <int CBYTES, int R, bool BF16, typename OutT, int NT>
+static int launch_pair_t(const CUtensorMap& map, const GemmArgs& a, int grid, cudaStream_t st) {
+  auto kern = gemm_pair_kernel<CBYTES, R, BF16, OutT, NT>;
+  const size_t smem = pair_smem(R, NT);
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64] = {};
+  int dev = 0;
+  VQB_CUDA_CHECK(cudaGetDevice(&dev));
+  dev &= 63;
+  std::call_once(once[dev], [&] {
+    attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr_err[dev] != cudaSuccess) return cuda_error(attr_err[dev], "cudaFuncSetAttribute(gemm_pair_kernel)");
+  kern<<<grid, kGemmThreads, smem, st>>>(map, a);  // cluster dims (2, 1, 1) from __cluster_dims__
+  VQB_LAUNCH_CHECK("gemm_pair_kernel");
+  set_launch(grid, kGemmThreads, 256, 0);
+  set_kernel("gemm_tc2");
+  return VQB_OK;
+}
+
+template <int CBYTES, int R, bool BF16, int NT>
+static int launch_pair_out(const CUtensorMap& map, const GemmArgs& a, int grid, cudaStream_t st) {
+  if (a.y_dtype == VQB_F32) return launch_pair_t<CBYTES, R, BF16, float, NT>(map, a, grid, st);
+  if (a.y_dtype == VQB_F16) return launch_pair_t<CBYTES, R, BF16, __half, NT>(map, a, grid, st);
+  return launch_pair_t<CBYTES, R, BF16, __nv_bfloat16, NT>(map, a, grid, st);
+}
+
+template <int CBYTES, int R, bool BF16>
+static int launch_pair_nt(const CUtensorMap& map, const GemmArgs& a, int nt, cudaStream_t st) {
+  const int grid = 2 * (int)(ceil_div(a.rows, 2 * kPairRowsCta) * (a.N / nt));
+  return nt == 256 ? launch_pair_out<CBYTES, R, BF16, 256>(map, a, grid, st)
+                   : launch_pair_out<CBYTES, R, BF16, 128>(map, a, grid, st);
+}
+
 template <int CBYTES, int R, bool BF16>
 static int launch_gemm_out(const CUtensorMap& map, const GemmArgs& a, int grid, cudaStream_t st) {
   if (a.y_dtype == VQB_F32) return launch_gemm_t<CBYTES, R, BF16, float>(map, a, grid, st);
@@ -547,8 +869,28 @@ extern "C" int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, in
         a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(d_ws) + VQB_WS_COUNTER_BYTES);
       }
     }
-    const int grid = tiles * a.splits;
     const bool bf = w->codebook_dtype == VQB_BF16;
+    // prefill sizes (no split-K): the CTA-pair kernel with 256 x 256 tiles
+    // (VQB_FLAG_NO_PAIR keeps the one-CTA kernel)
+    // (measured: the pair kernel's 256 x 128 tiles run at ~500 TFLOP/s, latency-bound
+    // on the per-stage cross-CTA handshake with only 256 MMA cycles per stage, so
+    // they are used only where 256-wide tiles do not divide N; VQB_FLAG_PAIR_N128
+    // forces them)
+    const bool pair_ok = a.splits == 1 && g.cols % 128 == 0 && !(launch && (launch->flags & VQB_FLAG_NO_PAIR));
+    const bool force128 = launch && (launch->flags & VQB_FLAG_PAIR_N128);
+    if (pair_ok && (g.cols % 256 == 0 || force128)) {
+      const int nt = (g.cols % 256 == 0 && !force128) ? 256 : 128;
+      CUtensorMap map2;
+      const cuuint32_t box2[2] = {(cuuint32_t)kTileK, (cuuint32_t)kPairRowsCta};
+      cr = enc(&map2, x_dtype == VQB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+               const_cast<void*>(d_x), dims, strides, box2, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+      if (g.bits == 16) return bf ? launch_pair_nt<2, 1, true>(map2, a, nt, st) : launch_pair_nt<2, 1, false>(map2, a, nt, st);
+      if (g.R == 1) return bf ? launch_pair_nt<1, 1, true>(map2, a, nt, st) : launch_pair_nt<1, 1, false>(map2, a, nt, st);
+      return bf ? launch_pair_nt<1, 2, true>(map2, a, nt, st) : launch_pair_nt<1, 2, false>(map2, a, nt, st);
+    }
+    const int grid = tiles * a.splits;
     if (g.bits == 16) return bf ? launch_gemm_out<2, 1, true>(map, a, grid, st) : launch_gemm_out<2, 1, false>(map, a, grid, st);
     if (g.R == 1) return bf ? launch_gemm_out<1, 1, true>(map, a, grid, st) : launch_gemm_out<1, 1, false>(map, a, grid, st);
     return bf ? launch_gemm_out<1, 2, true>(map, a, grid, st) : launch_gemm_out<1, 2, false>(map, a, grid, st);

@@ -288,6 +288,7 @@ GEMM_CASES = [
     ("C2_quip2_full_table", (256, 256), 8, 16, 1, None, 64),   # codes beyond the shared tier
     ("C3_aqlm2x8", (1024, 256), 8, 8, 2, None, 300),
     ("aqlm1x8", (768, 640), 8, 8, 1, None, 512),
+    ("C2_quip2_prefill_pair", (1024, 768), 8, 16, 1, 256, 600),  # CTA-pair kernel, 256 x 128 tiles
 ]
 
 
@@ -306,8 +307,17 @@ def test_gemm_tcgen05(label, shape, v, bits, r, work, rows, dtype, dev):
     d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev, codebook_dtype=dtype)
     x = torch.from_numpy(O.synthetic_tensor((rows, shape[0]), 22)).to(tdt)
     ref = O.matmul_ref(x.float().numpy(), dense)
+    # prefill sizes (> 256 rows) run the CTA-pair (cta_group::2) kernel; VQB_FLAG_NO_PAIR
+    # pins the one-CTA kernel, which also serves the split-K decode sizes
+    no_pair = ops.launch_struct()
+    no_pair.flags |= N.FLAG_NO_PAIR
     for out_dtype in (torch.float32, tdt):
-        y = ops.vq_gemm(d, x.to(dev), out_dtype=out_dtype)
-        assert N.last_kernel() == "gemm_tc", N.last_kernel()
-        tol = 2e-3 if dtype == "float16" else 1.6e-2
-        assert O.rel_err(y.float().cpu().numpy(), ref) <= tol, (label, out_dtype)
+        n128 = ops.launch_struct()
+        n128.flags |= N.FLAG_PAIR_N128
+        pair_default = rows > 256 and shape[1] % 256 == 0
+        for L, kerns in ((None, ("gemm_tc2",) if pair_default else ("gemm_tc", "gemm_tc2")),
+                         (no_pair, ("gemm_tc",)), (n128, ("gemm_tc2",) if rows > 256 else ("gemm_tc", "gemm_tc2"))):
+            y = ops.vq_gemm(d, x.to(dev), out_dtype=out_dtype, launch=L)
+            assert N.last_kernel() in kerns, (N.last_kernel(), kerns)
+            tol = 2e-3 if dtype == "float16" else 1.6e-2
+            assert O.rel_err(y.float().cpu().numpy(), ref) <= tol, (label, out_dtype, kern)
