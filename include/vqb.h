@@ -251,6 +251,46 @@ int vqb_add_len(int32_t* d_len, int32_t delta, void* stream);
  * write position outside [0, capacity) and skipped the write. */
 int vqb_take_device_error(int32_t* out);
 
+/* ---- tensor-parallel collectives fused into the decode GEMV ----
+ * No vqforge counterpart (the reference is single-device; TP is the paper's future
+ * work). Replaces the NCCL all-reduce / all-gather that follows a
+ * row- / column-parallel linear (paper_2503_02236_b200/tp.py) with peer-memory
+ * stores issued by the GEMV's own epilogue: each output element travels to every
+ * rank as soon as its column block is reduced, overlapping the transfer with the
+ * remaining tiles. Every rank owns one symmetric buffer of vqb_tp_buffer_bytes,
+ * zeroed once and mapped on every peer with the IPC calls below (one process per
+ * GPU; on NVSwitch the peer stores travel over NVLink). Collectives run in epochs:
+ * the GEMV writes slot parity (epoch & 1) of every rank and the grid's last CTA
+ * signals each rank once; vqb_tp_finish waits for all `world` signals, reduces the
+ * slots in rank order (identical bits on every rank) or copies the gathered row,
+ * and advances the epoch. Stream-ordered and graph-capturable; a rank waits at
+ * most ~10 s for its peers, then sets bit 0 of the header's error word
+ * (vqb_tp_take_error) instead of hanging. */
+#define VQB_TP_HEADER_BYTES 4096
+#define VQB_TP_MAX_WORLD 8
+#define VQB_TP_ALLREDUCE 0 /* row-parallel: y = sum over ranks of the partial outputs */
+#define VQB_TP_ALLGATHER 1 /* column-parallel: y = [y_0 | y_1 | ... ] along N */
+typedef struct VqbPeerComm {
+  int32_t rank, world;                 /* 1 <= world <= VQB_TP_MAX_WORLD */
+  void* d_peer[VQB_TP_MAX_WORLD];      /* every rank's symmetric buffer as mapped here (d_peer[rank] is local) */
+  int64_t slot_elems;                  /* fp32 elements per slot: >= rows*N (all-reduce), >= rows*N*world (all-gather) */
+} VqbPeerComm;
+int64_t vqb_tp_buffer_bytes(int32_t world, int64_t slot_elems);
+/* CUDA IPC of a device pointer inside any allocation: 64-byte handle + offset. */
+int vqb_ipc_get_handle(const void* d_ptr, void* handle64, int64_t* offset);
+int vqb_ipc_open_handle(const void* handle64, int64_t offset, void** d_ptr);
+int vqb_ipc_close_handle(void* d_ptr);
+/* The decode GEMV (as vqb_gemv, fast configurations only) whose outputs go to the
+ * current slot of every rank instead of a local y. */
+int vqb_gemv_tp(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows, int32_t mode,
+                const VqbPeerComm* comm, const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream);
+/* Wait for every rank's signal, then y (rows, n_local) = sum of the slots
+ * (all-reduce) or y (rows, n_local * world) = the gathered slot (all-gather). */
+int vqb_tp_finish(const VqbPeerComm* comm, int32_t mode, int32_t rows, int32_t n_local, void* d_y,
+                  int32_t y_dtype, void* stream);
+/* Read and clear the symmetric buffer's error word (synchronises the device). */
+int vqb_tp_take_error(const VqbPeerComm* comm, int32_t* out);
+
 /* Convert a PACKED stream (src, layout must be VQB_LAYOUT_PACKED) into
  * `dst_layout`, writing into d_dst (dst_bytes available). Bytes needed are
  * returned by vqb_layout_bytes. */

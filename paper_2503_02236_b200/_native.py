@@ -42,6 +42,8 @@ EXPORTS = (
     "vqb_gemm", "vqb_attn_decode", "vqb_layout_bytes", "vqb_repack", "vqb_query_usage",
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
     "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error", "vqb_gemv_grouped",
+    "vqb_tp_buffer_bytes", "vqb_ipc_get_handle", "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp",
+    "vqb_tp_finish", "vqb_tp_take_error",
 )
 
 
@@ -77,6 +79,16 @@ class VqbLaunch(ctypes.Structure):
         ("grid_limit", ctypes.c_int32),
         ("flags", ctypes.c_int32),
     ]
+
+
+TP_MAX_WORLD = 8
+TP_ALLREDUCE, TP_ALLGATHER = 0, 1
+
+
+class VqbPeerComm(ctypes.Structure):
+    """include/vqb.h VqbPeerComm: every rank's symmetric buffer as mapped here."""
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("d_peer", ctypes.c_void_p * TP_MAX_WORLD), ("slot_elems", ctypes.c_int64)]
 
 
 class VqbUsage(ctypes.Structure):
@@ -132,12 +144,23 @@ def lib():
             L.vqb_layout_bytes.restype = i64
             L.vqb_repack.argtypes = [T, i32, vp, i64, vp]
             L.vqb_query_usage.argtypes = [i32, T, P(VqbUsage)]
+            C = P(VqbPeerComm)
+            L.vqb_tp_buffer_bytes.argtypes = [i32, i64]
+            L.vqb_tp_buffer_bytes.restype = i64
+            L.vqb_ipc_get_handle.argtypes = [vp, vp, P(i64)]
+            L.vqb_ipc_open_handle.argtypes = [vp, i64, P(vp)]
+            L.vqb_ipc_close_handle.argtypes = [vp]
+            L.vqb_gemv_tp.argtypes = [T, vp, i32, i32, i32, C, La, vp, sz, vp]
+            L.vqb_tp_finish.argtypes = [C, i32, i32, i32, vp, i32, vp]
+            L.vqb_tp_take_error.argtypes = [C, P(i32)]
             L.vqb_debug_smem_base.argtypes = [vp, vp]
             L.vqb_debug_smem_base.restype = ctypes.c_int
             for name in ("vqb_dequant", "vqb_gemv", "vqb_gemm", "vqb_attn_decode", "vqb_repack",
                          "vqb_query_usage", "vqb_attn_decode_len", "vqb_rmsnorm", "vqb_qkv_rope",
                          "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append",
-                         "vqb_take_device_error", "vqb_gemv_grouped"):
+                         "vqb_take_device_error", "vqb_gemv_grouped", "vqb_ipc_get_handle",
+                         "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp", "vqb_tp_finish",
+                         "vqb_tp_take_error"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib

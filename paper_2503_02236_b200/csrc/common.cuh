@@ -320,4 +320,51 @@ __device__ __forceinline__ unsigned long long tag_partial(float v) {
   return (1ull << 32) | (unsigned long long)__float_as_uint(v);
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-parallel collectives over peer memory (tp.cu, vqb_gemv_tp): every rank owns
+// one symmetric buffer, VQB_TP_HEADER_BYTES of header then two parities of fp32
+// slots. Header words: [0] arrive[2] (u64, incremented remotely by every rank's
+// producer, one per collective), [64] producer CTA counter, [128] epoch (collectives
+// finished on this rank), [192] finish-kernel CTA counter, [256] error word.
+constexpr int kTpMaxWorld = 8;
+constexpr int kTpOffDone = 64, kTpOffEpoch = 128, kTpOffFinish = 192, kTpOffErr = 256;
+
+__device__ __forceinline__ int tp_epoch_of(const char* me) {
+  return *reinterpret_cast<const volatile int*>(me + kTpOffEpoch);
+}
+// slot element of output (b, n): all-reduce [par][rank][b][N]; all-gather
+// [par][b][world * N] with this rank's N columns at rank * N
+__device__ __forceinline__ int64_t tp_slot_offset(int mode, int par, int world, int rank, int64_t slot_elems, int b,
+                                                  int n, int N) {
+  return mode == 0 ? ((int64_t)par * world + rank) * slot_elems + (int64_t)b * N + n
+                   : (int64_t)par * slot_elems + ((int64_t)b * world + rank) * N + n;
+}
+// the value into every rank's slot (peer-memory stores over NVLink; the own rank's
+// buffer is local)
+__device__ __forceinline__ void tp_push(char* const* peer, int world, int64_t off, float v) {
+#pragma unroll 1
+  for (int p = 0; p < world; ++p)
+    reinterpret_cast<float*>(peer[p] + VQB_TP_HEADER_BYTES)[off] = v;
+}
+// End of a producer grid: every CTA fences its pushes system-wide and counts itself;
+// the last one signals arrive[par] on every rank (release at system scope).
+__device__ __forceinline__ void tp_signal(char* const* peer, int world, int rank, int par) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned* done = reinterpret_cast<unsigned*>(peer[rank] + kTpOffDone);
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done) : "memory");
+    if (prev == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned*>(done) = 0u;  // every CTA arrived: reset for the next launch
+      __threadfence_system();
+      for (int p = 0; p < world; ++p) {
+        unsigned long long* arr = reinterpret_cast<unsigned long long*>(peer[p]) + par;
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(arr) : "memory");
+      }
+    }
+  }
+}
+
 }  // namespace vqb

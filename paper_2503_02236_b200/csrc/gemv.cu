@@ -91,6 +91,12 @@ struct GemvFastArgs {
   int n_reg;                  // register tier: entries [0, n_reg) held in registers (REGT kernels, <= 4)
   int total_units;            // grouped launch: units over every problem of the table
   int n_probs;                // grouped launch: problems in the table (0: the single problem above)
+  // tensor-parallel push epilogue (vqb_gemv_tp; tp_world 0 = plain store into y): every
+  // output element goes straight from the reducing CTA into each rank's symmetric
+  // buffer over peer memory, then the grid's last CTA signals every rank (tp.cu)
+  int tp_world, tp_rank, tp_mode;
+  char* tp_peer[kTpMaxWorld];
+  int64_t tp_slot_elems;
 };
 
 // One linear of a grouped launch (vqb_gemv_grouped): same VQ config and batch as
@@ -354,6 +360,8 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     book_commit(0, bb);
   }
   pdl_wait();  // x / y / the partial workspace may belong to the previous kernel
+  // TP push: slot parity of this collective (the epoch the last finish kernel left)
+  const int tp_par = a.tp_world ? (tp_epoch_of(a.tp_peer[a.tp_rank]) & 1) : 0;
   ProbCursor xc = cc;  // x cursor of the prologue (thread 0)
   if (tid == 0)
     for (int idx = 0; idx < pre; ++idx) issue_x(xc, idx);
@@ -372,6 +380,15 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
 #pragma unroll
     for (int j = 0; j < 4; ++j) cacc[q][j] = 0.f;
 
+  // one finished output element: y, or (TP push) every rank's slot of this collective
+  auto emit = [&](int b, int n, float v) {
+    if (a.tp_world == 0) {
+      store_from_f32(cc.y, a.y_dtype, (int64_t)b * cc.N + n, v);
+    } else {
+      tp_push(a.tp_peer, a.tp_world, tp_slot_offset(a.tp_mode, tp_par, a.tp_world, a.tp_rank, a.tp_slot_elems,
+                                                     b, n, cc.N), v);
+    }
+  };
   int cur_buf = 0;
   int span_first = u0;  // first unit of the current span
   int cb = (u0 - cc.base) / cc.n_chunks;
@@ -670,7 +687,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
           const int q = o / (GC * 4), g = (o / 4) % GC, c = o % 4;
           const int col = MMA ? o : g * V + q * 4 + c;
           if (whole) {
-            if (cb * COLS + col < cc.N) store_from_f32(cc.y, a.y_dtype, (int64_t)bb * cc.N + (int64_t)cb * COLS + col, sum);
+            if (cb * COLS + col < cc.N) emit(bb, cb * COLS + col, sum);
           }
           else if (finisher) keep[b] = sum;
           else st_relaxed_u64(a.part + ((int64_t)blockIdx.x * B + bb) * COLS + col, tag_partial(sum));
@@ -711,7 +728,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
                 }
               }
             }
-            if (cb * COLS + col < cc.N) store_from_f32(cc.y, a.y_dtype, (int64_t)b * cc.N + (int64_t)cb * COLS + col, sum);
+            if (cb * COLS + col < cc.N) emit(b, cb * COLS + col, sum);
           }
         }
         if (tid == 0) trace_at(a.trace, 5);
@@ -733,6 +750,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     }
   }
   if (tid == 0) trace_at(a.trace, 6);
+  if (a.tp_world) tp_signal(a.tp_peer, a.tp_world, a.tp_rank, tp_par);
 }
 
 template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool REGT = false>
@@ -969,7 +987,8 @@ static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
 }
 
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
-                  const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast) {
+                  const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast,
+                  const VqbPeerComm* tp, int tp_mode) {
   Geom g;
   int s = make_geom(w, &g);
   if (s) return s;
@@ -982,13 +1001,15 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
   // the activations are TMA-staged: 16-byte aligned rows
   if (kernel && ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (g.rows % 8) != 0)) kernel = nullptr;
   if (used_fast) *used_fast = kernel != nullptr;
+  if (tp && !kernel)
+    return set_error(VQB_ECONFIG, "the tensor-parallel push GEMV needs the fast kernel's configuration");
   if (kernel) {
     const int64_t need = fast_ws_bytes(p, g, rows);
     if ((int64_t)ws_bytes < need || !ws)
       return set_error(VQB_ECAPACITY, "GEMV workspace too small: %zu < %lld", ws_bytes, (long long)need);
     const int64_t units = (int64_t)p.n_cblk * p.n_chunks;
     uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
-    GemvFastArgs a;
+    GemvFastArgs a = {};
     a.codes = reinterpret_cast<const uint8_t*>(w->d_codes);
     a.level_bytes = g.S * g.code_bytes;
     a.books = reinterpret_cast<const __half*>(w->d_codebooks);
@@ -1013,6 +1034,13 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
       return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
     a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
+    if (tp) {
+      a.tp_world = tp->world;
+      a.tp_rank = tp->rank;
+      a.tp_mode = tp_mode;
+      for (int i = 0; i < tp->world; ++i) a.tp_peer[i] = reinterpret_cast<char*>(tp->d_peer[i]);
+      a.tp_slot_elems = tp->slot_elems;
+    }
     return launch_gemv_kernel(kernel, p, a, st, L);
   }
   // generic: per-chunk partials then an ordered reduction
@@ -1197,5 +1225,5 @@ extern "C" int vqb_gemv_grouped(const VqbTensor* w, int32_t n, const void* const
 extern "C" int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows, void* d_y,
                         int32_t y_dtype, const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
   return vqb::gemv_dispatch(w, d_x, x_dtype, rows, d_y, y_dtype, launch, d_ws, ws_bytes,
-                            reinterpret_cast<cudaStream_t>(stream), nullptr);
+                            reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, 0);
 }

@@ -68,6 +68,7 @@ class VQLlamaDecoder:
         # caches and its slice of ffn; o and down are row-parallel and all-reduced
         self.group = group           # None = the default process group when tp_world > 1
         self.world = int(tp_world)
+        self.comm = None             # tp.PeerComm: row-parallel all-reduce fused into the GEMV (peer memory)
         self.local_heads = self.layers[0].k_cache.shape[1] if self.layers else shape.heads
         self.d_len = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.tokens = torch.zeros(batch, dtype=torch.int64, device=self.device)
@@ -125,8 +126,16 @@ class VQLlamaDecoder:
             torch.distributed.all_reduce(y, group=self.group)
         return y
 
+    def _row_linear(self, w: DeviceVQTensor, x: torch.Tensor) -> torch.Tensor:
+        """A row-parallel linear and its all-reduce: fused over peer memory when the
+        decoder holds a PeerComm and the batch takes the GEMV, else GEMV/GEMM + NCCL."""
+        if self.comm is not None and x.shape[0] <= self.gemv_max_rows and x.shape[0] in (1, 2, 4, 8):
+            return self.comm.linear(w, x, "row", out_dtype=torch.float16)
+        return self._reduce(self._linear(w, x))
+
     @classmethod
-    def tensor_parallel(cls, full: "VQLlamaDecoder", group, rank: int = None, world: int = None) -> "VQLlamaDecoder":
+    def tensor_parallel(cls, full: "VQLlamaDecoder", group, rank: int = None, world: int = None,
+                        fused_collectives: bool = False) -> "VQLlamaDecoder":
         """This rank's shard of a decoder (same weights): qkv columns of heads
         [h0, h1) for q, k and v, o rows of those heads, gate/up columns of ffn slice
         [f0, f1), down rows of it, KV caches (and their per-head CQ books) of the
@@ -156,8 +165,12 @@ class VQLlamaDecoder:
         # the collectives run only in a real process group (rank / world given without
         # one emulate a shard, e.g. to check it in a single process)
         live = torch.distributed.is_initialized()
-        return cls(sh, layers, full.embed, full.final_norm, full.lm_head, full.batch, group=group,
-                   tp_world=world if live else 1)
+        dec = cls(sh, layers, full.embed, full.final_norm, full.lm_head, full.batch, group=group,
+                  tp_world=world if live else 1)
+        if fused_collectives and live and world > 1:
+            from .tp import PeerComm
+            dec.comm = PeerComm(full.batch, sh.hidden, group=group, device=full.device)
+        return dec
 
     def step(self) -> torch.Tensor:
         """One decode step for the current tokens; returns (and stores) the next ones.
@@ -183,10 +196,10 @@ class VQLlamaDecoder:
             qkv = self._linear(L.qkv, xn)
             q = ops.qkv_rope_append(qkv, L.k_cache, L.v_cache, self.d_len, sh.rope_theta)
             a = ops.vq_attention(L.k_cache, L.v_cache, q, out_dtype=torch.float16, d_len=self.d_len)
-            o = self._reduce(self._linear(L.o, a.view(b, hc)))
+            o = self._row_linear(L.o, a.view(b, hc))
             xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)
             gu = self._linear(L.gate_up, xn)
-            x = self._reduce(self._linear(L.down, ops.silu_mul(gu)))
+            x = self._row_linear(L.down, ops.silu_mul(gu))
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
         self.tokens.copy_(torch.argmax(self.logits, dim=-1))

@@ -13,6 +13,7 @@ Local compute defaults to the CUDA kernels; ``compute`` can be replaced (the
 multi-process CPU tests run the sharding and collectives with the oracle).
 """
 
+import ctypes
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -187,6 +188,90 @@ def _default_attention(k, v, q):
     return vq_attention(kd, vd, q)
 
 
+class PeerComm:
+    """Fused tensor-parallel collectives over peer memory (csrc/tp.cu, include/vqb.h
+    VqbPeerComm): one symmetric buffer per rank, mapped on every peer through CUDA IPC
+    (handles exchanged over the process group, any backend). ``linear`` runs the
+    decode GEMV whose epilogue pushes each finished output element into every rank's
+    slot, then the finish kernel waits for all ranks and reduces (row-parallel) or
+    gathers (column-parallel) — the NCCL call after the linear disappears from the
+    critical path. One process per GPU on an NVLink node; the tests run two
+    processes on one GPU (IPC within a device)."""
+
+    def __init__(self, max_rows: int, max_n: int, group=None, device=None):
+        from . import _native as N
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > N.TP_MAX_WORLD:
+            raise ConfigError(f"fused TP collectives support up to {N.TP_MAX_WORLD} ranks, got {self.world}")
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # a slot holds rows x N (all-reduce) or rows x N x world (all-gather) fp32
+        self.slot_elems = int(max_rows) * int(max_n) * self.world
+        lib = N.lib()
+        nbytes = N.check(lib.vqb_tp_buffer_bytes(self.world, self.slot_elems))
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        handle = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_int64(0)
+        N.check(lib.vqb_ipc_get_handle(ctypes.c_void_p(self.buf.data_ptr()), handle, ctypes.byref(off)))
+        torch.cuda.synchronize(self.device)
+        mine = (bytes(handle), int(off.value))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        ptrs = []
+        for r, (h, o) in enumerate(allh):
+            if r == self.rank:
+                ptrs.append(self.buf.data_ptr())
+                continue
+            hb = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+            p = ctypes.c_void_p(0)
+            N.check(lib.vqb_ipc_open_handle(hb, int(o), ctypes.byref(p)))
+            self._opened.append(p.value)
+            ptrs.append(p.value)
+        self.c = N.VqbPeerComm()
+        self.c.rank, self.c.world, self.c.slot_elems = self.rank, self.world, self.slot_elems
+        for r, p in enumerate(ptrs):
+            self.c.d_peer[r] = p
+        dist.barrier(group=group)
+
+    def linear(self, w, x: torch.Tensor, mode: str = "row", out_dtype=torch.float16) -> torch.Tensor:
+        """y = collective(x @ dequant(W_shard)): ``row`` sums the partial outputs of
+        every rank, ``column`` concatenates their column blocks along N."""
+        from . import _native as N
+        from .ops import _stream, dtype_enum, torch_dtype, workspace
+        x2 = x.reshape(1, -1) if x.dim() == 1 else x
+        x2 = x2.contiguous()
+        rows = x2.shape[0]
+        m, n = w.shape
+        md = N.TP_ALLREDUCE if mode == "row" else N.TP_ALLGATHER
+        L = N.VqbLaunch()
+        lib = N.lib()
+        s = w.struct()
+        need = N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMV, s, rows, L))
+        ws = workspace(need, w.device)
+        st = _stream(w.device)
+        N.check(lib.vqb_gemv_tp(s, x2.data_ptr(), dtype_enum(x2.dtype), rows, md, ctypes.byref(self.c), L,
+                                ws.data_ptr(), ws.numel(), st))
+        od = torch_dtype(out_dtype)
+        y = torch.empty((rows, n * (self.world if md == N.TP_ALLGATHER else 1)), dtype=od, device=w.device)
+        N.check(lib.vqb_tp_finish(ctypes.byref(self.c), md, rows, n, y.data_ptr(), dtype_enum(od), st))
+        return y[0] if x.dim() == 1 else y
+
+    def take_error(self) -> int:
+        from . import _native as N
+        v = ctypes.c_int32(0)
+        N.check(N.lib().vqb_tp_take_error(ctypes.byref(self.c), ctypes.byref(v)))
+        return int(v.value)
+
+    def close(self) -> None:
+        from . import _native as N
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            N.check(N.lib().vqb_ipc_close_handle(ctypes.c_void_p(p)))
+        self._opened = []
+
+
 @dataclass
 class TPLinear:
     """A VQ linear layer sharded over a process group.
@@ -200,6 +285,7 @@ class TPLinear:
     mode: str = "column"
     group: Optional[object] = None
     compute: Callable = _default_linear
+    comm: Optional[PeerComm] = None  # fused peer-memory collective instead of NCCL (decode GEMV sizes)
 
     @classmethod
     def from_full(cls, q: QuantizedTensor, mode="column", group=None, compute=None, device=None):
@@ -213,6 +299,13 @@ class TPLinear:
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         world = dist.get_world_size(self.group)
+        if self.comm is not None and (x.dim() == 1 or x.shape[0] <= 8):
+            if self.mode == "column":
+                return self.comm.linear(self.weight, x, "column", out_dtype=x.dtype)
+            rank = dist.get_rank(self.group)
+            m_local = self.weight.shape[0]
+            return self.comm.linear(self.weight, x[..., rank * m_local:(rank + 1) * m_local], "row",
+                                    out_dtype=x.dtype)
         if self.mode == "column":
             y = self.compute(self.weight, x).contiguous()
             out = torch.empty((world * y.shape[0],) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)

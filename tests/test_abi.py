@@ -38,9 +38,9 @@ def test_struct_layouts_match_header(tmp_path):
 #include <stddef.h>
 #include "{HEADER}"
 int main(void) {{
-  printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(VqbTensor), offsetof(VqbTensor, dims),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(VqbTensor), offsetof(VqbTensor, dims),
          offsetof(VqbTensor, d_codes), offsetof(VqbTensor, d_codebooks), offsetof(VqbTensor, max_code),
-         sizeof(VqbLaunch), sizeof(VqbUsage));
+         sizeof(VqbLaunch), sizeof(VqbUsage), sizeof(VqbPeerComm), offsetof(VqbPeerComm, slot_elems));
   return 0;
 }}
 """)
@@ -49,7 +49,8 @@ int main(void) {{
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     T = N.VqbTensor
     want = [ctypes.sizeof(T), T.dims.offset, T.d_codes.offset, T.d_codebooks.offset, T.max_code.offset,
-            ctypes.sizeof(N.VqbLaunch), ctypes.sizeof(N.VqbUsage)]
+            ctypes.sizeof(N.VqbLaunch), ctypes.sizeof(N.VqbUsage), ctypes.sizeof(N.VqbPeerComm),
+            N.VqbPeerComm.slot_elems.offset]
     assert got == want
 
 

@@ -296,3 +296,51 @@ def test_qkv_rope_append_matches_separate_kernels(B, dev):
     assert torch.equal(q1, q2)
     for i in range(2):
         assert torch.equal(caches[0][i].codes, caches[1][i].codes)
+
+
+@pytest.mark.parametrize("mode", ["bulk", "token"])
+def test_cq_quantize_near_ties(mode, dev):
+    """Adversarial KV rows for the nearest-centroid screen (V/codec.py:239-253):
+    fp16 midpoints of two entries (exact float64 ties -> lowest index), midpoints
+    nudged by one fp16 ulp either way, rows equal to a duplicated entry, and rows a
+    hair away from an entry. Codes must equal the float64 oracle bit for bit."""
+    N, DeviceVQTensor, ops = _mods()
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    B, H, T, C, v = 2, 4, 64, 128, 2
+    G = C // v
+    rng = np.random.default_rng(123)
+    books = O.round_f16(rng.normal(0, 1, (H * G, 256, v)).astype(np.float32))
+    books[:, 200] = books[:, 17]  # exact duplicates: the lower index must win
+    pts = np.empty((B, H, T, G, v), np.float32)
+    for h in range(H):
+        for g in range(G):
+            bk = books[h * G + g]
+            for b in range(B):
+                for t in range(T):
+                    kind = (b * T + t + g) % 5
+                    i, j = rng.choice(256, 2, replace=False)
+                    if kind == 0:
+                        p = (bk[i].astype(np.float64) + bk[j]) / 2
+                    elif kind in (1, 2):
+                        p = np.nextafter(((bk[i] + bk[j]) / 2).astype(np.float16),
+                                         np.float16(np.inf if kind == 1 else -np.inf)).astype(np.float64)
+                    elif kind == 3:
+                        p = bk[17].astype(np.float64)
+                    else:
+                        p = np.nextafter(bk[i].astype(np.float16), np.float16(np.inf)).astype(np.float64)
+                    pts[b, h, t, g] = p
+    data = O.round_f16(pts.reshape(B, H, T, C))
+    regions = O.region_ids((B, H, T, C), v, "channel_group", group_width=v)
+    ref = O.quantize(data, books, (B, H, T, C), v, H * G, regions, 1)
+    cfg = VQConfig(v, 8, 1, Sharing.per_channel_group(v))
+    cache = DeviceVQTensor.empty_cache((B, H, T, C), cfg, torch.from_numpy(books).to(dev).half())
+    x = torch.from_numpy(data).to(dev).half()
+    if mode == "bulk":
+        ops.vq_quantize_kv(cache, x, tok0=0)
+    else:
+        d_len = torch.zeros(1, dtype=torch.int32, device=dev)
+        for t in range(T):
+            d_len.fill_(t + 1)
+            ops.vq_quantize_kv(cache, x[:, :, t:t + 1], d_len=d_len)
+    got = _codes(cache)
+    assert np.array_equal(got, ref), int((got != ref).sum())
