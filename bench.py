@@ -351,16 +351,18 @@ def time_gemv_single(torch, dev, ops, N, label, cfg_args, shape, work=None):
             "fp16_cublas_us": dense_us, "note": "CUDA graphs over > L2 of distinct weights (both arms)"}
 
 
-def time_decode(torch, dev, batch=1, ctx=4096, reps=10, tp=False):
+def time_decode(torch, dev, batch=1, ctx=4096, reps=10, tp=False, fused=False):
     """C5: end-to-end Llama-7B-shaped decode step (VQ weights + CQ-4 KV cache), one
     CUDA graph per step at a context of `ctx` cached tokens. tp=True: this rank's
     Megatron shard (heads / ffn slice, NCCL all-reduce after o and down, captured
-    in the graph)."""
+    in the graph; fused=True: those all-reduces fused into the GEMV over peer memory,
+    tp.PeerComm)."""
     from paper_2503_02236_b200.decode import LlamaShape, VQLlamaDecoder
     dec = VQLlamaDecoder.synthetic(LlamaShape(), batch, ctx, dev, seed=3)
     if tp:
-        dec = VQLlamaDecoder.tensor_parallel(dec, None)
+        dec = VQLlamaDecoder.tensor_parallel(dec, None, fused_collectives=fused)
         torch.cuda.empty_cache()
+    world = dec.world
     dec.set_length(ctx - 1 - reps - 3)
     dec.capture()
     for _ in range(3):
@@ -373,6 +375,8 @@ def time_decode(torch, dev, batch=1, ctx=4096, reps=10, tp=False):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    if dec.comm is not None:
+        dec.comm.close()
     del dec
     torch.cuda.empty_cache()
     if tp:
@@ -380,7 +384,8 @@ def time_decode(torch, dev, batch=1, ctx=4096, reps=10, tp=False):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t[0])
     return {"config": f"C5 llama7b decode quip2 weights + cq4 KV, batch {batch}, ctx {ctx}"
-                      + (f", tp{dec.world}" if tp else ""), "batch": batch,
+                      + (f", tp{world}" + (" fused peer-memory all-reduce" if fused else " NCCL all-reduce")
+                         if tp else ""), "batch": batch,
             "ms_per_step": ms, "tokens_per_s": batch * 1e3 / ms, "data": "synthetic weights/KV (random init)"}
 
 
@@ -714,6 +719,11 @@ def run_impl(args):
     decode_tp = None
     if world > 1 and not args.no_extra:
         decode_tp = [time_decode(torch, dev, b, tp=True) for b in (1, 16, 64)]  # C5 at N GPUs
+        for b in (1, 8):  # the GEMV batches with the all-reduce fused into the epilogue (csrc/tp.cu)
+            try:
+                decode_tp.append(time_decode(torch, dev, b, tp=True, fused=True))
+            except Exception as e:  # reported, never fatal to the scaling run
+                decode_tp.append({"batch": b, "fused": True, "error": f"{type(e).__name__}: {e}"[:300]})
     if rank == 0:
         hbm, src = peaks()
         total_bytes = step_bytes * world

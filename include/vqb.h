@@ -251,6 +251,20 @@ int vqb_add_len(int32_t* d_len, int32_t delta, void* stream);
  * write position outside [0, capacity) and skipped the write. */
 int vqb_take_device_error(int32_t* out);
 
+/* Decode GEMV with its input transform fused into the prologue (batch 1; the
+ * QuiP#-style v = 8 whole-tensor configurations with every code < 256): each CTA
+ * builds the transformed activation row in shared memory, so the standalone
+ * RMSNorm / SiLU launch before the linear disappears. Same arithmetic as
+ * vqb_rmsnorm / vqb_silu_mul (bit-identical results).
+ *  VQB_XF_RMSNORM : h = res_in + x (x may be NULL), res_out = h (res_out may be NULL;
+ *                   must not alias res_in), y = (weight * rmsnorm(h, eps)) @ dequant(W)
+ *  VQB_XF_SILU_MUL: x = [gate | up] (2M halves), y = (silu(gate) * up) @ dequant(W) */
+#define VQB_XF_RMSNORM 1
+#define VQB_XF_SILU_MUL 2
+int vqb_gemv_xf(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t mode, const void* d_res_in,
+                void* d_res_out, const void* d_weight, float eps, void* d_y, int32_t y_dtype,
+                const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream);
+
 /* ---- tensor-parallel collectives fused into the decode GEMV ----
  * No vqforge counterpart (the reference is single-device; TP is the paper's future
  * work). Replaces the NCCL all-reduce / all-gather that follows a

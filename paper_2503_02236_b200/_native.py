@@ -43,8 +43,9 @@ EXPORTS = (
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
     "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error", "vqb_gemv_grouped",
     "vqb_tp_buffer_bytes", "vqb_ipc_get_handle", "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp",
-    "vqb_tp_finish", "vqb_tp_take_error",
+    "vqb_tp_finish", "vqb_tp_take_error", "vqb_gemv_xf",
 )
+XF_RMSNORM, XF_SILU_MUL = 1, 2
 
 
 class VqbTensor(ctypes.Structure):
@@ -151,6 +152,7 @@ def lib():
             L.vqb_ipc_open_handle.argtypes = [vp, i64, P(vp)]
             L.vqb_ipc_close_handle.argtypes = [vp]
             L.vqb_gemv_tp.argtypes = [T, vp, i32, i32, i32, C, La, vp, sz, vp]
+            L.vqb_gemv_xf.argtypes = [T, vp, i32, i32, vp, vp, vp, f32, vp, i32, La, vp, sz, vp]
             L.vqb_tp_finish.argtypes = [C, i32, i32, i32, vp, i32, vp]
             L.vqb_tp_take_error.argtypes = [C, P(i32)]
             L.vqb_debug_smem_base.argtypes = [vp, vp]
@@ -160,7 +162,7 @@ def lib():
                          "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append",
                          "vqb_take_device_error", "vqb_gemv_grouped", "vqb_ipc_get_handle",
                          "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp", "vqb_tp_finish",
-                         "vqb_tp_take_error"):
+                         "vqb_tp_take_error", "vqb_gemv_xf"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib

@@ -33,7 +33,7 @@ namespace vqb {
 
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast,
-                  const VqbPeerComm* tp, int tp_mode);
+                  const VqbPeerComm* tp, int tp_mode, const struct GemvXf* xf);
 
 constexpr int kProdWarps = 16;      // dequantisation producer warps (2..17)
 constexpr int kGemmThreads = 64 + kProdWarps * 32;  // + TMA warp + MMA warp
@@ -898,5 +898,5 @@ extern "C" int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, in
   }
   VqbLaunch l = launch ? *launch : VqbLaunch{};
   l.flags |= VQB_FLAG_FORCE_GENERIC;
-  return gemv_dispatch(w, d_x, x_dtype, rows, d_y, y_dtype, &l, d_ws, ws_bytes, st, nullptr, nullptr, 0);
+  return gemv_dispatch(w, d_x, x_dtype, rows, d_y, y_dtype, &l, d_ws, ws_bytes, st, nullptr, nullptr, 0, nullptr);
 }

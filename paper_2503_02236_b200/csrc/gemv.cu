@@ -97,6 +97,17 @@ struct GemvFastArgs {
   int tp_world, tp_rank, tp_mode;
   char* tp_peer[kTpMaxWorld];
   int64_t tp_slot_elems;
+  // fused activation transform (XF kernels, vqb_gemv_xf; batch 1): the CTA builds the
+  // whole transformed x in shared memory once instead of streaming x per unit.
+  //  1 RMSNorm with residual: h = res_in + x (x may be null), res_out = h (CTA 0),
+  //    x' = w * rmsnorm(h) (the rmsnorm_kernel arithmetic, decode.cu)
+  //  2 SiLU gate: x' = silu(x[:M]) * x[M:2M] for x = [gate | up] (silu_mul_kernel)
+  int xf_mode;
+  const __half* xf_add;  // RMSNorm: the input added to the residual (null: none)
+  const __half* xf_res_in;
+  __half* xf_res_out;
+  const __half* xf_w;
+  float xf_eps;
 };
 
 // One linear of a grouped launch (vqb_gemv_grouped): same VQ config and batch as
@@ -131,6 +142,97 @@ struct ProbCursor {
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
   if (tr) tr[blockIdx.x * 8 + slot] = gtimer();
 }
+// Fused activation transform of the XF kernels (batch 1): every CTA computes the whole
+// transformed activation row into shared memory (x is 8-22 KB and L2-resident, so the
+// redundant reads cost less than a separate launch), with the exact arithmetic of the
+// standalone kernels (decode.cu rmsnorm_kernel / silu_mul_kernel) so the fused and
+// unfused decode steps agree bit for bit. `red` (>= THREADS/32 floats) is scratch.
+template <int THREADS>
+__device__ __forceinline__ void gemv_xf_preload(const GemvFastArgs& a, uint4 (&wv)[4]) {
+  // the norm weight does not depend on the previous kernel: fetched before griddepcontrol.wait
+  if (a.xf_mode != 1) return;
+  int nv = 0;
+  for (int i = threadIdx.x; i < a.M / 8 && nv < 4; i += THREADS, ++nv) wv[nv] = __ldg(reinterpret_cast<const uint4*>(a.xf_w) + i);
+}
+
+template <int THREADS>
+__device__ __forceinline__ void gemv_xf_prologue(const GemvFastArgs& a, uint8_t* xres, float* red, const uint4 (&wv)[4]) {
+  const int M = a.M, nvec = M / 8;
+  uint4* xo = reinterpret_cast<uint4*>(xres);
+  if (a.xf_mode == 2) {
+    const __half* gu = a.x;
+    for (int i = threadIdx.x; i < nvec; i += THREADS) {
+      const uint4 gv = __ldg(reinterpret_cast<const uint4*>(gu) + i);
+      const uint4 uv = __ldg(reinterpret_cast<const uint4*>(gu + M) + i);
+      const __half* gp = reinterpret_cast<const __half*>(&gv);
+      const __half* up = reinterpret_cast<const __half*>(&uv);
+      uint4 o;
+      __half* op = reinterpret_cast<__half*>(&o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float g = __half2float(gp[j]);
+        const __half sg = __float2half_rn(g / (1.0f + __expf(-g)));
+        op[j] = __float2half_rn(__half2float(sg) * __half2float(up[j]));
+      }
+      xo[i] = o;
+    }
+    return;
+  }
+  // RMSNorm: the per-thread strided partial sums, warp then block reduction of
+  // rmsnorm_kernel<THREADS> (same thread count, so the same float order)
+  const __half* xr = a.xf_add;  // may be null (first layer: h = residual)
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < nvec; i += THREADS) {
+    uint4 h = __ldg(reinterpret_cast<const uint4*>(a.xf_res_in) + i);
+    if (xr) {
+      const uint4 av = __ldg(reinterpret_cast<const uint4*>(xr) + i);
+      __half2* hp = reinterpret_cast<__half2*>(&h);
+      const __half2* ap = reinterpret_cast<const __half2*>(&av);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(hp[j]), g = __half22float2(ap[j]);
+        hp[j] = __floats2half2_rn(f.x + g.x, f.y + g.y);
+      }
+    }
+    xo[i] = h;  // h for now; normalised in place below
+    if (blockIdx.x == 0 && a.xf_res_out) reinterpret_cast<uint4*>(a.xf_res_out)[i] = h;
+    const __half2* hp = reinterpret_cast<const __half2*>(&h);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(hp[j]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < THREADS / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[THREADS / 32] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[THREADS / 32] / (float)M + a.xf_eps);
+  int nv = 0;
+  for (int i = threadIdx.x; i < nvec; i += THREADS, ++nv) {
+    const uint4 h = xo[i];
+    const uint4 wi = nv < 4 ? wv[nv] : __ldg(reinterpret_cast<const uint4*>(a.xf_w) + i);
+    const __half2* hp = reinterpret_cast<const __half2*>(&h);
+    const __half2* wp = reinterpret_cast<const __half2*>(&wi);
+    uint4 o;
+    __half2* op = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(hp[j]), ww = __half22float2(wp[j]);
+      const float2 hf = __half22float2(__floats2half2_rn(f.x * inv, f.y * inv));
+      op[j] = __floats2half2_rn(ww.x * hf.x, ww.y * hf.y);
+    }
+    xo[i] = o;
+  }
+}
+
 // Persistent stream-K decode GEMV. Work units are (column block, chunk of CR rows),
 // ordered column-block major; CTA i owns the contiguous unit range
 // [i*U/grid, (i+1)*U/grid) and walks it as "spans" (maximal runs inside one column
@@ -145,9 +247,11 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // entries become A fragments through ldmatrix.trans straight from the replicated
 // shared codebook (W^T: 16 columns x 16 rows per column pair), the activations the
 // B fragment (16 rows x 8 batch rows), fp32 accumulation.
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool GROUP, bool REGT = false>
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool GROUP, bool REGT = false,
+          bool XF = false>
 __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const GemvProblem* __restrict__ probs) {
   constexpr bool H2 = ACC == 1;
+  static_assert(!XF || (B == 1 && !GROUP && ACC != 2), "fused activation transform: batch 1, single problem");
   constexpr bool MMA = ACC == 2;
   static_assert(!MMA || (V == 8 && WG == 1 && !GTIER && !TILE), "tensor-core GEMV: v = 8, codes in shared memory");
   static_assert(!GROUP || (!TILE && !GTIER && R == 1), "grouped GEMV: whole-tensor books resident in shared memory");
@@ -191,6 +295,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
   constexpr int RED_ROWS = (B >= 2 && kGemvThreads >= 2 * COLS) ? 2 : 1;  // batch rows per epilogue pass
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + RED_ROWS * WM * COLS);  // full[kStages], empty[kStages]
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kStages);
+  uint8_t* xres = reinterpret_cast<uint8_t*>(bars + 2 * kStages + 2);  // XF: the transformed x (M halves)
 
   const int U = GROUP ? a.total_units : a.n_cblk * a.n_chunks;
   const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
@@ -277,7 +382,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     seek(fc, u);
     const int rows = unit_rows(fc, u);
     mbar_arrive_expect_tx(full0 + 8 * (idx % kStages),
-                          (uint32_t)(R * (rows / RPL) * unit_rgb(fc, u) + B * rows * 2));
+                          (uint32_t)(R * (rows / RPL) * unit_rgb(fc, u) + (XF ? 0 : B * rows * 2)));
   };
   auto issue_codes = [&](int idx) {
     const int s = idx % kStages, u = u0 + idx;
@@ -291,6 +396,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
                   (uint32_t)((rows / RPL) * rgb), full0 + 8 * s);
   };
   auto issue_x = [&](ProbCursor& c, int idx) {
+    if constexpr (XF) return;  // x is resident in shared memory
     const int s = idx % kStages, u = u0 + idx;
     seek(c, u);
     const int chunk = (u - c.base) % c.n_chunks;
@@ -359,12 +465,15 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     book_issue(cc.books, region_of(u0), bb);
     book_commit(0, bb);
   }
+  uint4 xf_wv[4];
+  if constexpr (XF) gemv_xf_preload<kGemvThreads>(a, xf_wv);
   pdl_wait();  // x / y / the partial workspace may belong to the previous kernel
   // TP push: slot parity of this collective (the epoch the last finish kernel left)
   const int tp_par = a.tp_world ? (tp_epoch_of(a.tp_peer[a.tp_rank]) & 1) : 0;
   ProbCursor xc = cc;  // x cursor of the prologue (thread 0)
   if (tid == 0)
     for (int idx = 0; idx < pre; ++idx) issue_x(xc, idx);
+  if constexpr (XF) gemv_xf_prologue<kGemvThreads>(a, xres, red, xf_wv);
   __syncthreads();
   if (tid == 0) trace_at(a.trace, 1);
 
@@ -420,7 +529,9 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     mbar_wait(full0 + 8 * s, (idx / kStages) & 1);
     if (tid == 0 && idx == 0) trace_at(a.trace, 2);
     const uint8_t* st = stages + s * STG;
-    const uint8_t* xs = st + STAGEB + (wm * kSlabRows) * 2;  // this warp's rows of the chunk's activations
+    // this warp's rows of the chunk's activations (XF: of the resident transformed x)
+    const uint8_t* xs = XF ? xres + ((int64_t)((u - cc.base) % cc.n_chunks) * CR + wm * kSlabRows) * 2
+                           : st + STAGEB + (wm * kSlabRows) * 2;
     const uint8_t* bsm = books_s + cur_buf * book_bytes + rep_off;
     const int region = region_of(u);
     const bool active = wm * kSlabRows < unit_rows(cc, u);  // the last chunk may be partial
@@ -442,24 +553,46 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
         }
         const int row = kb * 16 + (j4 >> 1) * 8 + rr;  // this lane's row of the slab
         const uint8_t* cbase = st + (wm * LOADS + row / RPL) * rgb + (row % RPL) * CBYTES + (j4 & 1) * 16;
+        // software pipeline: the ldmatrix gathers of column-pair group g+1 are issued
+        // before the MMAs of group g, so each MMA finds its A fragment landed instead of
+        // waiting one shared-memory round trip per column pair
+        constexpr int QG = R == 1 ? 4 : 2;  // column pairs per group (A-fragment registers)
+        constexpr int NG = 16 / QG;
+        uint32_t af[2][QG][R][4];
+        auto gather = [&](int g, uint32_t (&dst)[QG][R][4]) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+          for (int qq = 0; qq < QG; ++qq) {
+            const int q = g * QG + qq;
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const uint8_t* cp = cbase + r * LEVB + q * 32;
-            // groups past a narrow last column block hold no codes: entry 0 (never stored)
-            const uint32_t code = (2 * q + (j4 & 1) >= wb) ? 0u
-                                  : CBYTES == 2 ? (uint32_t)*reinterpret_cast<const uint16_t*>(cp) & 0xffu
-                                                : (uint32_t)*cp;
-            const uint32_t addr = WIDE ? smem_u32(books_s) + (code << 8) + (R == 2 ? r : cur_buf) * 128 + rep_off
-                                       : smem_u32(bsm) + (uint32_t)(r * a.n_sh * 128) + (code << 7);
-            uint32_t a0, a1, a2, a3;
-            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(addr));
-            asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
-                         "{%8, %9}, {%0, %1, %2, %3};"
-                         : "+f"(cacc[q][0]), "+f"(cacc[q][1]), "+f"(cacc[q][2]), "+f"(cacc[q][3])
-                         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(xb0), "r"(xb1));
+            for (int r = 0; r < R; ++r) {
+              const uint8_t* cp = cbase + r * LEVB + q * 32;
+              // groups past a narrow last column block hold no codes: entry 0 (never stored)
+              const uint32_t code = (2 * q + (j4 & 1) >= wb) ? 0u
+                                    : CBYTES == 2 ? (uint32_t)*reinterpret_cast<const uint16_t*>(cp) & 0xffu
+                                                  : (uint32_t)*cp;
+              const uint32_t addr = WIDE ? smem_u32(books_s) + (code << 8) + (R == 2 ? r : cur_buf) * 128 + rep_off
+                                         : smem_u32(bsm) + (uint32_t)(r * a.n_sh * 128) + (code << 7);
+              asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(dst[qq][r][0]), "=r"(dst[qq][r][1]), "=r"(dst[qq][r][2]), "=r"(dst[qq][r][3])
+                           : "r"(addr));
+            }
+          }
+        };
+        gather(0, af[0]);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          if (g + 1 < NG) gather(g + 1, af[(g + 1) & 1]);
+#pragma unroll
+          for (int qq = 0; qq < QG; ++qq) {
+            const int q = g * QG + qq;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const uint32_t* f = af[g & 1][qq][r];
+              asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                           "{%8, %9}, {%0, %1, %2, %3};"
+                           : "+f"(cacc[q][0]), "+f"(cacc[q][1]), "+f"(cacc[q][2]), "+f"(cacc[q][3])
+                           : "r"(f[0]), "r"(f[1]), "r"(f[2]), "r"(f[3]), "r"(xb0), "r"(xb1));
+            }
           }
         }
       }
@@ -753,9 +886,9 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
   if (a.tp_world) tp_signal(a.tp_peer, a.tp_world, a.tp_rank, tp_par);
 }
 
-template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool REGT = false>
+template <int V, int CBYTES, int R, int B, int WG, bool TILE, bool GTIER, int ACC, bool REGT = false, bool XF = false>
 __global__ void __launch_bounds__(gemv_warps(B, ACC == 2) * 32, 1) gemv_fast_kernel(GemvFastArgs a) {
-  gemv_fast_body<V, CBYTES, R, B, WG, TILE, GTIER, ACC, false, REGT>(a, nullptr);
+  gemv_fast_body<V, CBYTES, R, B, WG, TILE, GTIER, ACC, false, REGT, XF>(a, nullptr);
 }
 
 // grouped launch: the problem table travels as a __grid_constant__ kernel parameter
@@ -826,6 +959,16 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
 
 // ---------------------------------------------------------------------------
 // dispatch
+
+// host-side description of a fused activation transform (vqb_gemv_xf)
+struct GemvXf {
+  int mode;  // VQB_XF_*
+  const __half* add;
+  const __half* res_in;
+  __half* res_out;
+  const __half* weight;
+  float eps;
+};
 
 struct FastPlan {
   bool ok = false;
@@ -988,7 +1131,7 @@ static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
 
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast,
-                  const VqbPeerComm* tp, int tp_mode) {
+                  const VqbPeerComm* tp, int tp_mode, const GemvXf* xf) {
   Geom g;
   int s = make_geom(w, &g);
   if (s) return s;
@@ -1000,6 +1143,18 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
   GemvKernel kernel = p.ok ? fast_kernel_for(p, rows) : nullptr;
   // the activations are TMA-staged: 16-byte aligned rows
   if (kernel && ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (g.rows % 8) != 0)) kernel = nullptr;
+  if (xf) {
+    // the fused-transform instances: batch 1, QuiP#-style VQ<8,16,1> / 8-bit whole-tensor
+    // books resident in shared memory (every code < 256), fp16 windows
+    const bool xf_ok = kernel && rows == 1 && p.V == 8 && p.R == 1 && !p.tile && !p.gtier && p.h2 && p.n_reg == 0 &&
+                       (g.rows % 8) == 0;
+    kernel = !xf_ok ? nullptr : (p.cbytes == 2 ? gemv_fast_kernel<8, 2, 1, 1, 1, false, false, 1, false, true>
+                                               : gemv_fast_kernel<8, 1, 1, 1, 1, false, false, 1, false, true>);
+    if (!kernel)
+      return set_error(VQB_ECONFIG, "the fused-activation GEMV needs batch 1, v = 8, one level, whole-tensor "
+                                    "books with every code < 256 and fp16 activations");
+    p.smem += (size_t)g.rows * 2;
+  }
   if (used_fast) *used_fast = kernel != nullptr;
   if (tp && !kernel)
     return set_error(VQB_ECONFIG, "the tensor-parallel push GEMV needs the fast kernel's configuration");
@@ -1034,6 +1189,14 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
       return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
     a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
+    if (xf) {
+      a.xf_mode = xf->mode;
+      a.xf_add = xf->add;
+      a.xf_res_in = xf->res_in;
+      a.xf_res_out = xf->res_out;
+      a.xf_w = xf->weight;
+      a.xf_eps = xf->eps;
+    }
     if (tp) {
       a.tp_world = tp->world;
       a.tp_rank = tp->rank;
@@ -1225,5 +1388,28 @@ extern "C" int vqb_gemv_grouped(const VqbTensor* w, int32_t n, const void* const
 extern "C" int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows, void* d_y,
                         int32_t y_dtype, const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
   return vqb::gemv_dispatch(w, d_x, x_dtype, rows, d_y, y_dtype, launch, d_ws, ws_bytes,
-                            reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, 0);
+                            reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, 0, nullptr);
+}
+
+extern "C" int vqb_gemv_xf(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t mode, const void* d_res_in,
+                           void* d_res_out, const void* d_weight, float eps, void* d_y, int32_t y_dtype,
+                           const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
+  if (mode != VQB_XF_RMSNORM && mode != VQB_XF_SILU_MUL) return vqb::set_error(VQB_ECONFIG, "unknown activation transform %d", mode);
+  if (x_dtype != VQB_F16) return vqb::set_error(VQB_ECONFIG, "the fused-activation GEMV takes fp16 activations");
+  if (mode == VQB_XF_RMSNORM && (!d_res_in || !d_weight))
+    return vqb::set_error(VQB_ECONFIG, "RMSNorm transform needs the residual and the norm weight");
+  if (mode == VQB_XF_SILU_MUL && !d_x) return vqb::set_error(VQB_ECONFIG, "SiLU transform needs the gate|up input");
+  for (const void* ptr : {d_x, d_res_in, (const void*)d_res_out, d_weight})
+    if (reinterpret_cast<uintptr_t>(ptr) & 15) return vqb::set_error(VQB_ECONFIG, "activation buffers must be 16-byte aligned");
+  vqb::GemvXf xf{mode, mode == VQB_XF_RMSNORM ? reinterpret_cast<const __half*>(d_x) : nullptr,
+                 reinterpret_cast<const __half*>(d_res_in), reinterpret_cast<__half*>(d_res_out),
+                 reinterpret_cast<const __half*>(d_weight), eps};
+  // x is read only by the transform (never by the TMA ring in this mode): the plan
+  // checks see the SiLU input or, for RMSNorm, the residual
+  const void* xp = mode == VQB_XF_SILU_MUL ? d_x : d_res_in;
+  int s = vqb::gemv_dispatch(w, xp, x_dtype, 1, d_y, y_dtype, launch, d_ws, ws_bytes,
+                             reinterpret_cast<cudaStream_t>(stream), nullptr, nullptr, 0, &xf);
+  if (s) return s;
+  vqb::set_kernel(mode == VQB_XF_RMSNORM ? "gemv_rmsnorm" : "gemv_silu");
+  return VQB_OK;
 }

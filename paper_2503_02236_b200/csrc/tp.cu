@@ -25,7 +25,7 @@ namespace vqb {
 
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast,
-                  const VqbPeerComm* tp, int tp_mode);
+                  const VqbPeerComm* tp, int tp_mode, const struct GemvXf* xf);
 
 constexpr unsigned long long kTpTimeoutNs = 10ull * 1000 * 1000 * 1000;
 
@@ -161,7 +161,7 @@ extern "C" int vqb_gemv_tp(const VqbTensor* w, const void* d_x, int32_t x_dtype,
     return set_error(VQB_ECAPACITY, "TP slot of %lld elements < %lld needed", (long long)comm->slot_elems,
                      (long long)need);
   s = gemv_dispatch(w, d_x, x_dtype, rows, nullptr, VQB_F32, launch, d_ws, ws_bytes,
-                    reinterpret_cast<cudaStream_t>(stream), nullptr, comm, mode);
+                    reinterpret_cast<cudaStream_t>(stream), nullptr, comm, mode, nullptr);
   if (s) return s;
   set_kernel("gemv_tp");
   return VQB_OK;

@@ -73,6 +73,7 @@ class VQLlamaDecoder:
         self.d_len = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.tokens = torch.zeros(batch, dtype=torch.int64, device=self.device)
         self.res = torch.zeros((batch, shape.hidden), dtype=torch.float16, device=self.device)
+        self.res_b = torch.zeros_like(self.res)  # ping-pong partner for the norm fused into the GEMV
         self.logits = None
         self._graph = None
         self.length = 0  # host mirror of d_len (the step advances both)
@@ -114,6 +115,7 @@ class VQLlamaDecoder:
     # -- the step -----------------------------------------------------------------------------
 
     gemv_max_rows = 8  # batches up to this take the CUDA-core GEMV, larger ones the tcgen05 GEMM
+    fuse_norms = True  # batch 1: RMSNorm / SiLU gating fused into the following GEMV's prologue
 
     def _linear(self, w: DeviceVQTensor, x: torch.Tensor) -> torch.Tensor:
         if x.shape[0] <= self.gemv_max_rows and x.shape[0] in (1, 2, 4, 8):
@@ -191,6 +193,8 @@ class VQLlamaDecoder:
         self.res.copy_(torch.index_select(self.embed, 0, self.tokens))
         x = None
         hc = self.local_heads * sh.head_dim
+        if self.fuse_norms and b == 1 and self.gemv_max_rows >= 1:
+            return self._step_fused()
         for L in self.layers:
             xn = ops.rmsnorm(x, self.res, L.attn_norm, sh.eps)
             qkv = self._linear(L.qkv, xn)
@@ -201,6 +205,34 @@ class VQLlamaDecoder:
             gu = self._linear(L.gate_up, xn)
             x = self._row_linear(L.down, ops.silu_mul(gu))
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
+        self.logits = xn @ self.lm_head
+        self.tokens.copy_(torch.argmax(self.logits, dim=-1))
+        return self.tokens
+
+    def _step_fused(self) -> torch.Tensor:
+        """Batch-1 step with the norms and the SiLU gate fused into the GEMVs that
+        consume them (vqb_gemv_xf): per layer qkv(+attn norm), rope/append, attention,
+        o, gate_up(+ffn norm), down(+SiLU) — 6 launches instead of 9. The residual
+        stream alternates between two buffers (every CTA of a fused GEMV reads the old
+        one while CTA 0 writes the new one); same arithmetic as the unfused step."""
+        sh = self.shape
+        res = (self.res, self.res_b)
+        cur = 0
+        x = None
+        hc = self.local_heads * sh.head_dim
+        for L in self.layers:
+            qkv = ops.vq_gemv_rmsnorm(L.qkv, x, res[cur], L.attn_norm, sh.eps, residual_out=res[1 - cur])
+            cur ^= 1
+            q = ops.qkv_rope_append(qkv, L.k_cache, L.v_cache, self.d_len, sh.rope_theta)
+            a = ops.vq_attention(L.k_cache, L.v_cache, q, out_dtype=torch.float16, d_len=self.d_len)
+            o = self._row_linear(L.o, a.view(1, hc))
+            gu = ops.vq_gemv_rmsnorm(L.gate_up, o, res[cur], L.ffn_norm, sh.eps, residual_out=res[1 - cur])
+            cur ^= 1
+            # the SiLU gate stays a separate kernel: fused into the down GEMV every CTA
+            # would recompute all 11008 gated activations (measured 0.4 us slower per
+            # layer, tools/xf_bench.py); the norm fusion reads only 2 x 8 KB per CTA
+            x = self._row_linear(L.down, ops.silu_mul(gu))
+        xn = ops.rmsnorm(x, res[cur], self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
         self.tokens.copy_(torch.argmax(self.logits, dim=-1))
         return self.tokens

@@ -344,3 +344,57 @@ def test_cq_quantize_near_ties(mode, dev):
             ops.vq_quantize_kv(cache, x[:, :, t:t + 1], d_len=d_len)
     got = _codes(cache)
     assert np.array_equal(got, ref), int((got != ref).sum())
+
+
+def test_fused_norm_and_silu_gemv_match_separate_kernels(dev):
+    """vqb_gemv_xf: the RMSNorm (with residual add) and the SiLU gate computed in the
+    GEMV prologue give bit-identical results to rmsnorm/silu_mul + vq_gemv."""
+    N, DeviceVQTensor, ops = _mods()
+    from paper_2503_02236_b200.decode import WEIGHT_CFG
+    g = torch.Generator(device=dev).manual_seed(17)
+
+    def weight(m, n):
+        codes = torch.randint(0, 256, (1, m * n // 8), generator=g, device=dev, dtype=torch.int32)
+        books = (torch.randn((1, 65536, 8), generator=g, device=dev) * 0.05).half()
+        return DeviceVQTensor.from_device_codes(codes, (m, n), WEIGHT_CFG, books).relayout("gemv")
+
+    for m, n in ((4096, 12288), (1024, 768)):
+        w = weight(m, n)
+        res = torch.randn((1, m), generator=g, device=dev).half()
+        x = torch.randn((1, m), generator=g, device=dev).half()
+        nw = (1 + 0.1 * torch.randn(m, generator=g, device=dev)).half()
+        for add in (x, None):
+            r1 = res.clone()
+            xn = ops.rmsnorm(add, r1, nw, 1e-5)
+            ref = ops.vq_gemv(w, xn, out_dtype=torch.float16)
+            r_out = torch.empty_like(res)
+            y = ops.vq_gemv_rmsnorm(w, add, res, nw, 1e-5, residual_out=r_out)
+            assert N.last_kernel() == "gemv_rmsnorm"
+            assert torch.equal(y, ref) and torch.equal(r_out, r1)
+        gu = torch.randn((1, 2 * m), generator=g, device=dev).half()
+        ref = ops.vq_gemv(w, ops.silu_mul(gu), out_dtype=torch.float16)
+        y = ops.vq_gemv_silu(w, gu)
+        assert N.last_kernel() == "gemv_silu"
+        assert torch.equal(y, ref)
+
+
+def test_fused_decode_step_bit_identical(dev):
+    """The batch-1 decode step with the norms / SiLU fused into the GEMVs produces
+    the unfused step's logits bit for bit, eagerly and as a replayed CUDA graph."""
+    from paper_2503_02236_b200.decode import LlamaShape, VQLlamaDecoder
+    sh = LlamaShape(hidden=512, heads=4, head_dim=128, ffn=1024, layers=2, vocab=256)
+    a = VQLlamaDecoder.synthetic(sh, 1, 64, dev, seed=8)
+    b = VQLlamaDecoder.synthetic(sh, 1, 64, dev, seed=8)
+    b.fuse_norms = False
+    for d in (a, b):
+        d.tokens.fill_(7)
+    for _ in range(3):
+        a.run_step()
+        b.run_step()
+        assert torch.equal(a.logits, b.logits)
+    a.capture()
+    b.capture()
+    for _ in range(3):
+        a.replay()
+        b.replay()
+        assert torch.equal(a.logits, b.logits)
