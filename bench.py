@@ -441,6 +441,23 @@ def time_gemm(torch, dev, N, label, cfg, shapes, rows=1024, work=None, copies=4)
 
         us = graph_time(torch, run, 10) / len(ws)
         kern = N.last_kernel()
+        # both prefill paths at this shape: fused producers vs dequantise + dense pair GEMM
+        paths = {}
+        for pname, flag in (("fused", N.FLAG_GEMM_FUSED), ("two_phase", N.FLAG_GEMM_TWO_PHASE)):
+            L2 = launch_struct()
+            L2.flags |= flag
+            need2 = max(N.check(lib.vqb_workspace_bytes(N.KERNEL_GEMM, st, rows, L2)) for st in structs)
+            buf2 = workspace(need2, dev)
+
+            def run_p():
+                st_ = torch.cuda.current_stream(dev).cuda_stream
+                for st, y in zip(structs, ys):
+                    N.check(lib.vqb_gemm(st, x.data_ptr(), N.F16, rows, y.data_ptr(), N.F16, L2, buf2.data_ptr(),
+                                         buf2.numel(), st_))
+
+            pus = graph_time(torch, run_p, 10) / len(ws)
+            paths[pname] = {"kernel": N.last_kernel(), "us_per_call": round(pus, 2),
+                            "TFLOP_s": round(2.0 * rows * m * n / pus / 1e6, 1)}
         dense = [torch.randn((m, n), device=dev, dtype=torch.float16) for _ in range(copies)]
         outs = [torch.empty((rows, n), device=dev, dtype=torch.float16) for _ in dense]
 
@@ -453,7 +470,7 @@ def time_gemm(torch, dev, N, label, cfg, shapes, rows=1024, work=None, copies=4)
         res[name] = {"shape": [rows, m, n], "kernel": kern, "us_per_call": round(us, 2),
                      "TFLOP_s": round(flops / us / 1e6, 1), "frac": round(flops / us / 1e6 / peak, 3),
                      "fp16_cublas_us": round(dus, 2), "fp16_cublas_TFLOP_s": round(flops / dus / 1e6, 1),
-                     "speedup_vs_fp16": round(dus / us, 3)}
+                     "speedup_vs_fp16": round(dus / us, 3), "paths": paths}
         tot_flops += flops
         tot_us += us
         tot_dense += dus

@@ -131,6 +131,11 @@ typedef struct VqbLaunch {
 #define VQB_FLAG_NO_PAIR 128     /* GEMM: the one-CTA tcgen05 kernel instead of the CTA-pair
                                     (cta_group::2) kernel at prefill sizes */
 #define VQB_FLAG_PAIR_N128 256   /* GEMM: CTA-pair kernel with 256 x 128 tiles (N % 128) */
+#define VQB_FLAG_GEMM_FUSED 512  /* GEMM: keep the fused (dequantise-in-the-producers) kernels at
+                                    prefill sizes where the two-phase path is the default */
+#define VQB_FLAG_GEMM_TWO_PHASE 1024 /* GEMM (rows > 256, v = 8, N % 256 == 0): dequantise W to an fp16
+                                    scratch in the workspace, then the dense CTA-pair tcgen05 GEMM
+                                    (default for two-level / AQLM codes at rows >= 512) */
 #define VQB_FLAG_COOPERATIVE 64  /* GEMV / attention: cooperative launch. The split reduction's
                                     finisher CTAs wait for partials of later CTAs, which needs
                                     the whole (<= 1 CTA per SM) grid resident; the default launch

@@ -25,7 +25,9 @@ FLAG_FORCE_GENERIC = 1
 FLAG_NO_MMA = 16  # GEMV batch 4-8 on CUDA-core FMAs instead of mma.sync
 FLAG_COOPERATIVE = 64
 FLAG_NO_PAIR = 128  # GEMM: one-CTA tcgen05 kernel instead of the CTA-pair kernel
-FLAG_PAIR_N128 = 256  # GEMM: CTA-pair kernel with 256 x 128 tiles  # cooperative launch: the driver guarantees the persistent grid is co-resident
+FLAG_PAIR_N128 = 256  # GEMM: CTA-pair kernel with 256 x 128 tiles
+FLAG_GEMM_FUSED = 512  # GEMM: fused producers at prefill sizes
+FLAG_GEMM_TWO_PHASE = 1024  # GEMM: dequantise to an fp16 scratch, then the dense pair GEMM
 
 _ERRORS = {
     ESHAPE: ShapeError,

@@ -348,7 +348,7 @@ int vqb_query_usage(int32_t kind, const VqbTensor* t, VqbUsage* out) {
 namespace vqb {
 int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L);
 int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH, const VqbLaunch* L);
-int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows);
+int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L);
 }  // namespace vqb
 
 extern "C" int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t rows, const VqbLaunch* launch) {
@@ -357,7 +357,7 @@ extern "C" int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t
     case VQB_KERNEL_GEMM: {
       const int64_t a = vqb::gemv_ws_bytes(t, rows, launch);
       if (a < 0) return a;
-      return std::max(a, vqb::gemm_ws_bytes(t, rows));  // split-K partials, or the generic fallback
+      return std::max(a, vqb::gemm_ws_bytes(t, rows, launch));  // split-K partials / two-phase scratch, or the generic fallback
     }
     case VQB_KERNEL_ATTN: return vqb::attn_ws_bytes(t, rows, launch);
     case VQB_KERNEL_DEQUANT: return 0;

@@ -671,6 +671,194 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Two-phase prefill (dequantise, then a dense tcgen05 GEMM). At prefill sizes the
+// fused kernels above are shared-memory-bound: every W element costs an LDS gather
+// and an STS into the UMMA layout on top of the tensor core's own operand traffic,
+// and with AQLM's two levels (R = 2) the producers do twice the gathers. Written
+// once to HBM as fp16 (the RN cast of the bit-exact fp32 dequantisation) and read
+// back by TMA, the dequantised W costs 2 x M x N x 2 bytes of HBM traffic, which at
+// rows >= 512 is cheaper than the fused producers' shared-memory time (DESIGN.md
+// §3 GEMM; measured in bench.py's c3 / gemm_c2 keys).
+
+// W (M, N) -> fp16/bf16 row-major straight from the GEMV_IL stream (N % 256 == 0, so
+// 16-byte code word w of a level sits at byte 16 w and holds rows rg*RPL .. +RPL of
+// sub-vector group cb*32 + gi, w = (cb * M/RPL + rg) * 32 + gi): one coalesced word
+// load per level, then per row the summed entries (fp32, level order, one RN cast)
+// as one 16-byte store; the 32 lanes of a warp cover one 512-byte row span
+template <typename CB, int CBYTES, int R>
+__global__ void __launch_bounds__(256) dequant_rows_kernel(const uint8_t* __restrict__ codes, int64_t level_bytes,
+                                                           const CB* __restrict__ books, int K, int M, int N,
+                                                           CB* __restrict__ out) {
+  constexpr int RPL = 16 / CBYTES;
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t words = (int64_t)M / RPL * (N / 8);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int rgs = M / RPL;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+    const int gi = (int)(w & 31);
+    const int64_t t = w >> 5;
+    const int rg = (int)(t % rgs), cb = (int)(t / rgs);
+    uint4 cw[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cw[r] = ldg_stream(codes + r * level_bytes + w * 16);
+    CB* o = out + (int64_t)rg * RPL * N + (int64_t)(cb * 32 + gi) * 8;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        uint32_t code;
+        if constexpr (CBYTES == 2) {
+          const uint32_t x = (&cw[r].x)[k / 2];
+          code = (k & 1) ? (x >> 16) : (x & 0xffffu);
+        } else {
+          code = ((&cw[r].x)[k / 4] >> (8 * (k % 4))) & 0xffu;
+        }
+        const uint4 e = __ldg(reinterpret_cast<const uint4*>(books + ((int64_t)r * K + code) * 8));
+        const CB* ep = reinterpret_cast<const CB*>(&e);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], to_f32<CB>(ep[j]));
+      }
+      uint4 v;
+      CB* vp = reinterpret_cast<CB*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if constexpr (std::is_same<CB, __half>::value) vp[j] = __float2half_rn(acc[j]);
+        else vp[j] = __float2bfloat16_rn(acc[j]);
+      }
+      *reinterpret_cast<uint4*>(o + (int64_t)k * N) = v;
+    }
+  }
+}
+
+// Dense CTA-pair GEMM: Y(rows, N) = X(rows, M) @ W(M, N) with both operands by TMA.
+// UMMA 256 x 256 x 16 over the pair (each CTA: 128 X rows, 128 W columns as two
+// 64-column SWIZZLE_128B boxes = the MN-major SW128 canonical layout). Tiles are
+// ordered row-tile fastest, so the pairs working on one W column strip run together
+// and the strip is read from HBM once (L2 serves the other row tiles).
+constexpr int kDenseStages = 5;
+constexpr int kDenseBBytes = kTileK * 128 * 2;  // this CTA's 128 columns x 64 K
+constexpr size_t dense_smem() {
+  return (size_t)kDenseStages * (kPairABytes + kDenseBBytes) + (2 * kDenseStages + 1) * 8 + 16 + 1024;
+}
+
+template <bool BF16, typename OutT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_dense_pair_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                           GemmArgs a) {
+  constexpr int NT = 256, CN = 128, STG = kDenseStages;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sa = smem;
+  uint8_t* sb = sa + STG * kPairABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + STG * kDenseBBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STG + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STG), tmem_full = smem_u32(bars + 2 * STG);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int n_tiles_m = (a.rows + 2 * kPairRowsCta - 1) / (2 * kPairRowsCta);
+  const int tile_m = pair % n_tiles_m, tile_n = pair / n_tiles_m;
+  const int row0 = tile_m * 2 * kPairRowsCta + (int)rank * kPairRowsCta;
+  const int n0 = tile_n * NT + (int)rank * CN;
+  const int k_iters = a.M / kTileK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STG; ++s) {
+      mbar_init(full0 + 8 * s, 1);   // the leader's expect_tx (both CTAs' A and B bytes)
+      mbar_init(empty0 + 8 * s, 1);  // multicast tcgen05.commit
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();  // W was dequantised by the preceding kernel
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bar_l = mapa_rank(full0, 0);
+      for (int it = 0; it < k_iters; ++it) {
+        const int s = it % STG;
+        mbar_wait(empty0 + 8 * s, ((it / STG) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(full0 + 8 * s, 2 * (kPairABytes + kDenseBBytes));
+        tma_load_2d_pair(smem_u32(sa + s * kPairABytes), &tmap_x, it * kTileK, row0, bar_l + 8 * s);
+        tma_load_2d_pair(smem_u32(sb + s * kDenseBBytes), &tmap_w, n0, it * kTileK, bar_l + 8 * s);
+        tma_load_2d_pair(smem_u32(sb + s * kDenseBBytes + kDenseBBytes / 2), &tmap_w, n0 + 64, it * kTileK,
+                         bar_l + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t fmt = BF16 ? 1u : 0u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
+                           ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    if (rank == 0 && lane == 0) {
+      for (int it = 0; it < k_iters; ++it) {
+        const int s = it % STG;
+        mbar_wait(full0 + 8 * s, (it / STG) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sa + s * kPairABytes), b_base = smem_u32(sb + s * kDenseBBytes);
+#pragma unroll
+        for (int k = 0; k < kTileK / 16; ++k) {
+          // B: two 64-column boxes (8 KB apart = LBO), 8-row groups 1 KB apart (SBO)
+          const uint64_t bdesc = umma_desc(b_base + k * 2 * 1024, kDenseBBytes / 2, 1024);
+          const uint64_t adesc = umma_desc(a_base + k * 32, 16, 1024);
+          umma_f16_pair(tmem_base, adesc, bdesc, idesc, (it | k) != 0);
+        }
+        umma_commit_pair(empty0 + 8 * s);
+      }
+      umma_commit_pair(tmem_full);
+    }
+  } else {
+    // epilogue: this CTA's 128 rows x 256 columns of TMEM
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int quarter = warp & 3;
+    constexpr int CPW = (NT / 32) / (kProdWarps / 4);
+    const int cc0 = ((warp - 2) / 4) * CPW;
+    const int row = row0 + quarter * 32 + lane;
+    const int ncol0 = tile_n * NT;
+#pragma unroll
+    for (int c2 = 0; c2 < CPW; ++c2) {
+      const int cc = cc0 + c2;
+      uint32_t v[32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + cc * 32;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+            "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+            "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < a.rows) store_row32<OutT>(a.y, a.y_dtype, (int64_t)row * a.N + ncol0 + cc * 32, v);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NT));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -725,9 +913,24 @@ static int gemm_splits(int tiles, int k_total) {
   return best;
 }
 
-int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows) {
+// the two-phase prefill path (dequantise to an fp16 scratch, dense CTA-pair GEMM):
+// forced by VQB_FLAG_GEMM_TWO_PHASE, else the default for AQLM-style two-level
+// codes at prefill sizes (measured faster than the fused producers)
+static bool gemm_two_phase(const Geom& g, const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
+  if (g.ndim != 2 || g.v != 8 || g.cols % 256 != 0 || g.rows % kTileK != 0 || rows <= kTileM) return false;
+  if (w->codebook_dtype == VQB_F32 || w->layout != VQB_LAYOUT_GEMV_IL || g.sharing != VQB_SHARE_WHOLE) return false;
+  const int flags = L ? L->flags : 0;
+  if (flags & (VQB_FLAG_FORCE_GENERIC | VQB_FLAG_NO_PAIR | VQB_FLAG_PAIR_N128 | VQB_FLAG_GEMM_FUSED)) return false;
+  if (flags & VQB_FLAG_GEMM_TWO_PHASE) return true;
+  return g.R == 2 && rows >= 512;
+}
+
+static int64_t a1k(int64_t x) { return (x + 1023) & ~int64_t(1023); }
+
+int64_t gemm_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
   Geom g;
   if (make_geom(w, &g)) return 0;
+  if (gemm_two_phase(g, w, rows, L)) return VQB_WS_COUNTER_BYTES + a1k(g.rows * g.cols * 2);
   const int tiles = (int)(ceil_div(rows, kTileM) * (g.cols / kTileN));
   const int sp = g.cols % kTileN == 0 && g.rows % kTileK == 0 && rows <= kTileM
                      ? gemm_splits(std::max(tiles, 1), (int)(g.rows / kTileK))
@@ -814,6 +1017,73 @@ static int launch_gemm_out(const CUtensorMap& map, const GemmArgs& a, int grid, 
   return launch_gemm_t<CBYTES, R, BF16, __nv_bfloat16>(map, a, grid, st);
 }
 
+template <bool BF16, typename OutT>
+static int launch_dense_pair(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, cudaStream_t st) {
+  auto kern = gemm_dense_pair_kernel<BF16, OutT>;
+  const size_t smem = dense_smem();
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64] = {};
+  int dev = 0;
+  VQB_CUDA_CHECK(cudaGetDevice(&dev));
+  dev &= 63;
+  std::call_once(once[dev], [&] {
+    attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr_err[dev] != cudaSuccess) return cuda_error(attr_err[dev], "cudaFuncSetAttribute(gemm_dense_pair_kernel)");
+  const int grid = 2 * (int)(ceil_div(a.rows, 2 * kPairRowsCta) * (a.N / 256));
+  VQB_CUDA_CHECK(launch_pdl(kern, dim3(grid), dim3(kGemmThreads), smem, st, mx, mw, a));
+  VQB_LAUNCH_CHECK("gemm_dense_pair_kernel");
+  set_launch(grid, kGemmThreads, 0, 0);
+  set_kernel("gemm_2phase");
+  return VQB_OK;
+}
+
+// dequantise W into the scratch (fp16/bf16 row-major), then the dense pair GEMM
+static int launch_two_phase(const Geom& g, const VqbTensor* w, const void* d_x, int x_dtype, const GemmArgs& a,
+                            void* scratch, cudaStream_t st) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const bool bf = w->codebook_dtype == VQB_BF16;
+  const CUtensorMapDataType dt = bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap mx, mw;
+  const cuuint64_t xd[2] = {(cuuint64_t)g.rows, (cuuint64_t)a.rows};
+  const cuuint64_t xs[1] = {(cuuint64_t)g.rows * 2};
+  const cuuint32_t xb[2] = {(cuuint32_t)kTileK, (cuuint32_t)kPairRowsCta};
+  CUresult cr = enc(&mx, dt, 2, const_cast<void*>(d_x), xd, xs, xb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const cuuint64_t wd[2] = {(cuuint64_t)g.cols, (cuuint64_t)g.rows};
+  const cuuint64_t wsd[1] = {(cuuint64_t)g.cols * 2};
+  const cuuint32_t wb[2] = {64u, (cuuint32_t)kTileK};
+  cr = enc(&mw, dt, 2, scratch, wd, wsd, wb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  (void)x_dtype;
+  const int64_t words = g.rows / (16 / g.code_bytes) * (g.cols / 8);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(words, 256), (int64_t)sm_count() * 8));
+  const uint8_t* cp = reinterpret_cast<const uint8_t*>(w->d_codes);
+  const int64_t lb = g.S * g.code_bytes;
+  const int M = (int)g.rows, N = (int)g.cols, K = g.K;
+#define VQB_DQ(CB, CBY, RR)                                                                                       \
+  VQB_CUDA_CHECK(launch_pdl(dequant_rows_kernel<CB, CBY, RR>, dim3((unsigned)blocks), dim3(256), 0, st, cp, lb,   \
+                            reinterpret_cast<const CB*>(w->d_codebooks), K, M, N, reinterpret_cast<CB*>(scratch)))
+  if (bf) {
+    if (g.code_bytes == 2) VQB_DQ(__nv_bfloat16, 2, 1);
+    else if (g.R == 1) VQB_DQ(__nv_bfloat16, 1, 1);
+    else VQB_DQ(__nv_bfloat16, 1, 2);
+  } else {
+    if (g.code_bytes == 2) VQB_DQ(__half, 2, 1);
+    else if (g.R == 1) VQB_DQ(__half, 1, 1);
+    else VQB_DQ(__half, 1, 2);
+  }
+#undef VQB_DQ
+  VQB_LAUNCH_CHECK("dequant_rows_kernel");
+  if (a.y_dtype == VQB_F32) return bf ? launch_dense_pair<true, float>(mx, mw, a, st) : launch_dense_pair<false, float>(mx, mw, a, st);
+  if (a.y_dtype == VQB_F16) return bf ? launch_dense_pair<true, __half>(mx, mw, a, st) : launch_dense_pair<false, __half>(mx, mw, a, st);
+  return bf ? launch_dense_pair<true, __nv_bfloat16>(mx, mw, a, st) : launch_dense_pair<false, __nv_bfloat16>(mx, mw, a, st);
+}
+
 int gemm_usage(VqbUsage* u) {
   cudaFuncAttributes at;
   auto k = gemm_tc_kernel<2, 1, false, float>;
@@ -871,6 +1141,13 @@ extern "C" int vqb_gemm(const VqbTensor* w, const void* d_x, int32_t x_dtype, in
       }
     }
     const bool bf = w->codebook_dtype == VQB_BF16;
+    if (a.splits == 1 && gemm_two_phase(g, w, rows, launch)) {
+      const int64_t need = VQB_WS_COUNTER_BYTES + a1k(g.rows * g.cols * 2);
+      if (!d_ws || (int64_t)ws_bytes < need)
+        return set_error(VQB_ECAPACITY, "two-phase GEMM workspace too small: %zu < %lld", ws_bytes, (long long)need);
+      void* scratch = reinterpret_cast<uint8_t*>(d_ws) + VQB_WS_COUNTER_BYTES;
+      return launch_two_phase(g, w, d_x, x_dtype, a, scratch, st);
+    }
     // prefill sizes (no split-K): the CTA-pair kernel with 256 x 256 tiles
     // (VQB_FLAG_NO_PAIR keeps the one-CTA kernel)
     // (measured: the pair kernel's 256 x 128 tiles run at ~500 TFLOP/s, latency-bound

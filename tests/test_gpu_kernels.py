@@ -289,6 +289,8 @@ GEMM_CASES = [
     ("C3_aqlm2x8", (1024, 256), 8, 8, 2, None, 300),
     ("aqlm1x8", (768, 640), 8, 8, 1, None, 512),
     ("C2_quip2_prefill_pair", (1024, 768), 8, 16, 1, 256, 600),  # CTA-pair kernel, 256 x 128 tiles
+    ("C3_aqlm2x8_prefill", (1024, 512), 8, 8, 2, None, 700),  # two-phase (dequantise + dense pair GEMM)
+    ("C2_quip2_prefill_wide", (512, 512), 8, 16, 1, 256, 520),  # 256 x 256 pair tiles, partial row tile
 ]
 
 
@@ -315,9 +317,40 @@ def test_gemm_tcgen05(label, shape, v, bits, r, work, rows, dtype, dev):
         n128 = ops.launch_struct()
         n128.flags |= N.FLAG_PAIR_N128
         pair_default = rows > 256 and shape[1] % 256 == 0
-        for L, kerns in ((None, ("gemm_tc2",) if pair_default else ("gemm_tc", "gemm_tc2")),
+        two_phase = pair_default and r == 2 and rows >= 512
+        for L, kerns in ((None, ("gemm_2phase",) if two_phase else ("gemm_tc2",) if pair_default
+                          else ("gemm_tc", "gemm_tc2")),
                          (no_pair, ("gemm_tc",)), (n128, ("gemm_tc2",) if rows > 256 else ("gemm_tc", "gemm_tc2"))):
             y = ops.vq_gemm(d, x.to(dev), out_dtype=out_dtype, launch=L)
             assert N.last_kernel() in kerns, (N.last_kernel(), kerns)
             tol = 2e-3 if dtype == "float16" else 1.6e-2
             assert O.rel_err(y.float().cpu().numpy(), ref) <= tol, (label, out_dtype, kern)
+
+
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+@pytest.mark.parametrize("label,shape,v,bits,r,work,rows", [c for c in GEMM_CASES if c[6] > 256 and c[1][1] % 256 == 0])
+def test_gemm_two_phase_matches_fused(label, shape, v, bits, r, work, rows, dtype, dev):
+    """Prefill sizes through both paths: the fused CTA-pair kernel (VQB_FLAG_GEMM_FUSED)
+    and the two-phase path (dequantise to the fp16 scratch, dense tcgen05 pair GEMM,
+    VQB_FLAG_GEMM_TWO_PHASE), each against the oracle."""
+    from paper_2503_02236_b200.codec import VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    tdt = getattr(torch, dtype)
+    cfg = VQConfig(v, bits, r)
+    codes, books = O.synthetic_codes_books(shape, v, bits, r, 1, 23, working_entries=work)
+    books = torch.from_numpy(books).to(tdt).float().numpy()
+    dense = O.dequantize(codes, books, shape, v, 1, O.region_ids(shape, v, "whole"))
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, 1, shape, cfg), device=dev, codebook_dtype=dtype)
+    x = torch.from_numpy(O.synthetic_tensor((rows, shape[0]), 24)).to(tdt)
+    # the two-phase path rounds the summed levels once (fp32 -> fp16/bf16); the oracle
+    # applies the same rounding to the dense weight the tensor cores consume
+    w16 = torch.from_numpy(dense).to(tdt).float().numpy()
+    ref = O.matmul_ref(x.float().numpy(), w16)
+    tol = 2e-3 if dtype == "float16" else 1.6e-2
+    for flag, kern in ((N.FLAG_GEMM_FUSED, "gemm_tc2"), (N.FLAG_GEMM_TWO_PHASE, "gemm_2phase")):
+        L = ops.launch_struct()
+        L.flags |= flag
+        for out_dtype in (torch.float32, tdt):
+            y = ops.vq_gemm(d, x.to(dev), out_dtype=out_dtype, launch=L)
+            assert N.last_kernel() == kern, (N.last_kernel(), kern)
+            assert O.rel_err(y.float().cpu().numpy(), ref) <= tol, (label, kern, out_dtype)
