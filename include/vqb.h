@@ -177,14 +177,15 @@ int vqb_dequant(const VqbTensor* t, void* d_out, int32_t out_dtype, void* stream
  * workspace are the self-resetting head: split-arrival counters (attention) and
  * tagged split partials (GEMV). Zero it once when the workspace is allocated;
  * kernels restore it to zero after use and never leave anything else there. */
-#define VQB_WS_COUNTER_BYTES 4194304
+#define VQB_WS_COUNTER_BYTES 16777216
 /* Workspace bytes a fused call needs (split partials + arrival counters).
  * kind = VQB_KERNEL_*; rows = batch rows (GEMV/GEMM) or B*H (attention). */
 int64_t vqb_workspace_bytes(int32_t kind, const VqbTensor* t, int64_t rows,
                             const VqbLaunch* launch);
 
-/* y(rows, N) = x(rows, M) @ dequant(W)(M, N). rows in [1, 8] take the CUDA-core
- * decode kernel; larger rows should use vqb_gemm. The workspace must be zeroed
+/* y(rows, N) = x(rows, M) @ dequant(W)(M, N). rows 1, 2, 4, 8 and 16 take the decode
+ * kernel (CUDA cores at 1-2, mma.sync at 4-16); other row counts the generic kernel,
+ * larger batches should use vqb_gemm. The workspace must be zeroed
  * once before first use (counters self-reset afterwards). */
 int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t rows,
              void* d_y, int32_t y_dtype, const VqbLaunch* launch, void* d_ws,

@@ -56,8 +56,10 @@ __host__ __device__ constexpr int gemv_warps(int B, bool mma = false) { return (
 __host__ __device__ constexpr int gemv_slab_rows(int cbytes) { return 32; }
 constexpr uint16_t kHalfOne = 0x3C00;  // fp16 1.0
 // chunk rows: the warps along M each take one 16-row slab (WG = warps across N)
+// (the tensor-core path at batch 16 splits a column block's 16 column pairs over
+// (B + 7) / 8 warps, so fewer warps run along M)
 __host__ __device__ constexpr int gemv_chunk_rows(int WG, int B, int cbytes, bool mma = false) {
-  return gemv_slab_rows(cbytes) * (gemv_warps(B, mma) / WG);
+  return gemv_slab_rows(cbytes) * (gemv_warps(B, mma) / WG / (mma ? (B + 7) / 8 : 1));
 }
 // bytes of one chunk's codes: R levels x chunk rows x 32*WG columns
 __host__ __device__ constexpr int stage_bytes(int R, int cbytes, int WG, int B, bool mma = false) {
@@ -261,7 +263,11 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
   constexpr int EB = V * 2;              // fp16 entry bytes
   constexpr int REP = 128 / EB;          // replicas per bank row
   constexpr int RPL = 16 / CBYTES;       // rows per 16-byte code word
-  constexpr int WM = kGemvWarps / WG;    // warps along M
+  constexpr int QS = MMA ? (B + 7) / 8 : 1;  // MMA: warps sharing a column block's 16 column pairs
+  constexpr int QW = 16 / QS;               // MMA: column pairs per warp
+  constexpr int NTL = QS;                   // MMA: 8-row batch tiles (n8 of m16n8k16)
+  static_assert(!MMA || (16 % QS == 0 && QW * NTL * 4 == 64), "MMA accumulators: 64 registers per lane");
+  constexpr int WM = kGemvWarps / WG / QS;  // warps along M
   constexpr int CR = gemv_chunk_rows(WG, B, CBYTES, MMA);
   constexpr int kSlabRows = gemv_slab_rows(CBYTES);
   constexpr int LOADS = kSlabRows / RPL;  // code words per lane per level per chunk
@@ -414,7 +420,7 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     }
 
   // ===== codebook cache fill =====
-  const int wm = warp / WG, wg = warp % WG;
+  const int wm = warp / (WG * QS), wg = (warp / QS) % WG, wq = warp % QS;
   const uint32_t rep_off = (uint32_t)(lane % REP) * EB;
   const int g_local = wg * 32 + lane;
 
@@ -482,12 +488,14 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
   for (int b = 0; b < (MMA ? 1 : B); ++b)
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
-  // MMA: D fragments (16 columns x 8 batch rows) of the block's 16 column pairs
-  float cacc[MMA ? 16 : 1][4];
+  // MMA: D fragments (16 columns x 8 batch rows) of this warp's column pairs and batch tiles
+  float cacc[MMA ? QW : 1][MMA ? NTL : 1][4];
 #pragma unroll
-  for (int q = 0; q < (MMA ? 16 : 1); ++q)
+  for (int q = 0; q < (MMA ? QW : 1); ++q)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) cacc[q][j] = 0.f;
+    for (int t = 0; t < (MMA ? NTL : 1); ++t)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cacc[q][t][j] = 0.f;
 
   // one finished output element: y, or (TP push) every rank's slot of this collective
   auto emit = [&](int b, int n, float v) {
@@ -545,24 +553,28 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
       const int j4 = lane >> 3, rr = lane & 7, bn = lane >> 2;
 #pragma unroll
       for (int kb = 0; kb < kSlabRows / 16; ++kb) {
-        uint32_t xb0 = 0u, xb1 = 0u;
-        if (bn < B) {
-          const uint8_t* xr = xs + bn * XROWB + (kb * 16 + 2 * (lane & 3)) * 2;
-          xb0 = *reinterpret_cast<const uint32_t*>(xr);
-          xb1 = *reinterpret_cast<const uint32_t*>(xr + 16);
+        uint32_t xb[NTL][2];
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) {
+          xb[t][0] = xb[t][1] = 0u;
+          if (8 * t + bn < B) {
+            const uint8_t* xr = xs + (8 * t + bn) * XROWB + (kb * 16 + 2 * (lane & 3)) * 2;
+            xb[t][0] = *reinterpret_cast<const uint32_t*>(xr);
+            xb[t][1] = *reinterpret_cast<const uint32_t*>(xr + 16);
+          }
         }
         const int row = kb * 16 + (j4 >> 1) * 8 + rr;  // this lane's row of the slab
         const uint8_t* cbase = st + (wm * LOADS + row / RPL) * rgb + (row % RPL) * CBYTES + (j4 & 1) * 16;
         // software pipeline: the ldmatrix gathers of column-pair group g+1 are issued
         // before the MMAs of group g, so each MMA finds its A fragment landed instead of
         // waiting one shared-memory round trip per column pair
-        constexpr int QG = R == 1 ? 4 : 2;  // column pairs per group (A-fragment registers)
-        constexpr int NG = 16 / QG;
+        constexpr int QG = (R == 1 ? 4 : 2) < QW ? (R == 1 ? 4 : 2) : QW;  // column pairs per group
+        constexpr int NG = QW / QG;
         uint32_t af[2][QG][R][4];
         auto gather = [&](int g, uint32_t (&dst)[QG][R][4]) {
 #pragma unroll
           for (int qq = 0; qq < QG; ++qq) {
-            const int q = g * QG + qq;
+            const int q = wq * QW + g * QG + qq;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const uint8_t* cp = cbase + r * LEVB + q * 32;
@@ -584,14 +596,17 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
           if (g + 1 < NG) gather(g + 1, af[(g + 1) & 1]);
 #pragma unroll
           for (int qq = 0; qq < QG; ++qq) {
-            const int q = g * QG + qq;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const uint32_t* f = af[g & 1][qq][r];
-              asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
-                           "{%8, %9}, {%0, %1, %2, %3};"
-                           : "+f"(cacc[q][0]), "+f"(cacc[q][1]), "+f"(cacc[q][2]), "+f"(cacc[q][3])
-                           : "r"(f[0]), "r"(f[1]), "r"(f[2]), "r"(f[3]), "r"(xb0), "r"(xb1));
+#pragma unroll
+              for (int t = 0; t < NTL; ++t) {
+                float (&c)[4] = cacc[g * QG + qq][t];
+                asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                             "{%8, %9}, {%0, %1, %2, %3};"
+                             : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                             : "r"(f[0]), "r"(f[1]), "r"(f[2]), "r"(f[3]), "r"(xb[t][0]), "r"(xb[t][1]));
+              }
             }
           }
         }
@@ -791,14 +806,14 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
           // misaligned stores for the batch-8 instance)
           uint32_t cq;
           asm("shr.b32 %0, %1, 2;" : "=r"(cq) : "r"((uint32_t)lane));
-          float* rp = red + (size_t)wm * COLS + cq;
-          if ((lane & 3) == (b >> 1)) {
+          float* rp = red + (size_t)wm * COLS + cq + 16 * wq * QW;
+          if ((lane & 3) == ((b % 8) >> 1)) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              rp[16 * q] = cacc[q][0];
-              rp[16 * q + 8] = cacc[q][2];
-              rp[WM * COLS + 16 * q] = cacc[q][1];
-              rp[WM * COLS + 16 * q + 8] = cacc[q][3];
+            for (int q = 0; q < QW; ++q) {
+              rp[16 * q] = cacc[q][b / 8][0];
+              rp[16 * q + 8] = cacc[q][b / 8][2];
+              rp[WM * COLS + 16 * q] = cacc[q][b / 8][1];
+              rp[WM * COLS + 16 * q + 8] = cacc[q][b / 8][3];
             }
           }
         } else {
@@ -871,9 +886,11 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[b][j] = 0.f;
 #pragma unroll
-      for (int q = 0; q < (MMA ? 16 : 1); ++q)
+      for (int q = 0; q < (MMA ? QW : 1); ++q)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cacc[q][j] = 0.f;
+        for (int t = 0; t < (MMA ? NTL : 1); ++t)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cacc[q][t][j] = 0.f;
       span_first = u + 1;
       if (u + 1 < u1) {
         seek(cc, u + 1);
@@ -982,7 +999,9 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   FastPlan p;
   if (L && (L->flags & VQB_FLAG_FORCE_GENERIC)) return p;
   if (t->layout != VQB_LAYOUT_GEMV_IL || t->codebook_dtype != VQB_F16 || x_dtype != VQB_F16) return p;
-  if (!(rows == 1 || rows == 2 || rows == 4 || rows == 8)) return p;
+  // batch 32 / 64 on mma.sync measured 1.5-4x slower than the tcgen05 GEMM (the legacy
+  // HMMA path tops out near 50 TFLOP/s on sm_100): those batches take vqb_gemm
+  if (!(rows == 1 || rows == 2 || rows == 4 || rows == 8 || rows == 16)) return p;
   if (!(g.v == 4 || g.v == 8) || g.R > 2) return p;
   if (!(g.bits == 8 || g.bits == 16)) return p;
   if (g.bits == 16 && g.R != 1) return p;
@@ -1020,6 +1039,7 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
   // CUDA cores, batch 4 about even, batch 2 slower (the mma path reads its codes with a
   // 2-way bank conflict per 16-row k-block of the GEMV_IL words).
   p.mma = p.h2 && !p.gtier && !p.tile && g.v == 8 && rows >= 4 && !(L && (L->flags & VQB_FLAG_NO_MMA));
+  if (rows >= 16 && !p.mma) return FastPlan{};  // batch 16-64 exist only on the tensor-core path
   const int CRm = gemv_chunk_rows(p.WG, rows, p.cbytes, p.mma);
   p.n_cblk = (int)ceil_div(g.cols, cols_per_cta);
   p.n_chunks = (int)((g.rows + CRm - 1) / CRm);
@@ -1110,6 +1130,10 @@ static GemvKernel pick_acc(bool gtier, bool h2, bool mma, bool regt) {
 
 template <int V, int CBYTES, int R, int WG, bool TILE>
 static GemvKernel pick_kernel(int rows, bool gtier, bool h2, bool mma, bool regt) {
+  if constexpr (V == 8 && WG == 1 && !TILE) {
+    if (rows == 16) return (mma && !gtier) ? gemv_fast_kernel<V, CBYTES, R, 16, WG, TILE, false, 2> : nullptr;
+  }
+  if (rows >= 16) return nullptr;
   switch (rows) {
     case 1: return pick_acc<V, CBYTES, R, 1, WG, TILE>(gtier, h2, mma, regt);
     case 2: return pick_acc<V, CBYTES, R, 2, WG, TILE>(gtier, h2, mma, regt);

@@ -163,6 +163,25 @@ def test_gemv_fast_kernel(label, shape, v, bits, r, sharing, tile, work, rows, d
     assert torch.equal(y, y2), "split reduction must be deterministic"
 
 
+@pytest.mark.parametrize("label,shape,v,bits,r,sharing,tile,work", FAST_GEMV)
+def test_gemv_batch16(label, shape, v, bits, r, sharing, tile, work, dev):
+    """Batch 16 on the tensor-core GEMV (two n8 batch tiles, the 16 column pairs of a
+    block split over two warps) where every code is in the shared tier; tile-shared
+    and global-tier configurations take the generic kernel, equally exact."""
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    sh = Sharing.per_tile(*tile) if sharing == "tile" else Sharing.whole_tensor()
+    cfg = VQConfig(v, bits, r, sh)
+    codes, books, nreg, dense = _big_weight(shape, v, bits, r, sharing, tile, work)
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev)
+    x = O.round_f16(O.synthetic_tensor((16, shape[0]), 9))
+    y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half())
+    fast = v == 8 and sharing == "whole" and (work is not None or bits == 8)
+    assert N.last_kernel() == ("gemv_fast" if fast else "gemv_generic"), label
+    assert O.rel_err(y.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
+    assert torch.equal(y, ops.vq_gemv(d, torch.from_numpy(x).to(dev).half()))
+
+
 @pytest.mark.parametrize("rows", [4, 8])
 @pytest.mark.parametrize("label,shape,v,bits,r,sharing,tile,work", [c for c in FAST_GEMV if c[2] == 8 and c[5] == "whole"])
 def test_gemv_cuda_core_path_at_mma_batches(label, shape, v, bits, r, sharing, tile, work, rows, dev):
