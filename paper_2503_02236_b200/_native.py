@@ -28,6 +28,8 @@ FLAG_NO_PAIR = 128  # GEMM: one-CTA tcgen05 kernel instead of the CTA-pair kerne
 FLAG_PAIR_N128 = 256  # GEMM: CTA-pair kernel with 256 x 128 tiles
 FLAG_GEMM_FUSED = 512  # GEMM: fused producers at prefill sizes
 FLAG_GEMM_TWO_PHASE = 1024  # GEMM: dequantise to an fp16 scratch, then the dense pair GEMM
+FLAG_GEMV_TC = 2048  # GEMV: the tcgen05 decode GEMV below its default batch range
+FLAG_NO_GEMV_TC = 4096  # GEMV: never the tcgen05 decode GEMV
 
 _ERRORS = {
     ESHAPE: ShapeError,

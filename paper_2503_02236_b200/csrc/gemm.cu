@@ -671,6 +671,247 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Decode GEMV on tcgen05 (batches 4-64): the roles of the GEMM swapped so the batch is
+// the UMMA N dimension — D[n_out, b] = W^T[n_out, k] x X^T[k, b] with M = 128 output
+// columns per UMMA (two halves of a 256-column GEMV_IL block), N = the batch padded to
+// 8..64, K = 16. A CTA owns one column block and a contiguous range of its 64-row
+// chunks (split-K sized to one wave); the chunk's code words arrive by one bulk copy
+// per level, 16 producer warps look them up in the replicated shared codebook and
+// write the W^T tile in the UMMA MN-major SW128 layout (A operand, transposed), X
+// arrives by TMA as the K-major B operand (rows past the batch zero-filled), the fp32
+// accumulator lives in TMEM. Split partials go to the workspace as plain fp32 and an
+// ordered reduce kernel sums them (deterministic). This replaces mma.sync for the
+// batches where the legacy HMMA path (~50 TFLOP/s on sm_100) made the GEMV compute-bound.
+constexpr int kGemvTcMinRows = 9;                // default from 9 rows: at 4-8 the mma.sync GEMV is as fast (measured)
+constexpr int kGtProd = 16;                       // dequantisation producer warps (2..17)
+constexpr int kGtEpi = 4;                         // epilogue warps (18..21)
+constexpr int kGtThreads = (2 + kGtProd + kGtEpi) * 32;
+__host__ __device__ constexpr int gt_stages(int R) { return 3; }  // A / X ring (producer -> MMA hand-off)
+constexpr int kGtCodeStages = 8;                   // code-word ring: the HBM latency is hidden here
+constexpr int kGtK = 64;                          // K rows per stage (one SW128 span)
+constexpr int kGtABytes = 256 * kGtK * 2;         // W^T tile: 256 output columns x 64 K (two 16 KB halves)
+
+struct GemvTcArgs {
+  const uint8_t* codes;  // GEMV_IL, N % 256 == 0
+  int64_t level_bytes;
+  const uint16_t* books;  // (R, K, 8) fp16
+  void* y;
+  int y_dtype;
+  int B, M, N, K, n_sh;
+  int n_cblk, n_chunks, splits;  // 256-column blocks, 64-row chunks, CTAs per block
+  float* part;                    // (splits, B, N) fp32 partials when splits > 1
+};
+
+__host__ __device__ constexpr int gt_code_bytes(int cbytes, int R) { return R * (kGtK / (16 / cbytes)) * 512; }
+__host__ __device__ constexpr size_t gt_smem(int cbytes, int R, int BN) {
+  return 1024 + (size_t)R * kBookBytes + (size_t)gt_stages(R) * (kGtABytes + BN * 128) +
+         (size_t)kGtCodeStages * gt_code_bytes(cbytes, R) + (3 * gt_stages(R) + 2 * kGtCodeStages + 4) * 8 + 16;
+}
+
+template <int CBYTES, int R, int BN>
+__global__ void __launch_bounds__(kGtThreads, 1)
+    gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, GemvTcArgs a) {
+  constexpr int RPL = 16 / CBYTES;
+  constexpr int CODEB = gt_code_bytes(CBYTES, R) / R;  // one level's code bytes per stage
+  constexpr int XB = BN * 128;                          // X tile bytes (BN rows x 64 K, SW128)
+  constexpr int STG = gt_stages(R);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sa = smem;                                   // STG x 32 KB (A: W^T tiles)
+  uint8_t* sx = sa + STG * kGtABytes;                   // STG x XB (B: X tiles)
+  constexpr int CST = kGtCodeStages;
+  uint8_t* sc = sx + STG * XB;                          // CST x R x CODEB (code words)
+  uint8_t* book = sc + CST * R * CODEB;                 // R x 256 entries x 128 B (replicated)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(book + R * kBookBytes);
+  // full[s] (X landed), afull[s] (A written), empty[s] (MMA done with slot s),
+  // cfull[c] (code words landed), cempty[c] (producers read them), tfull (accumulator done)
+  const uint32_t full0 = smem_u32(bars), afull0 = smem_u32(bars + STG), empty0 = smem_u32(bars + 2 * STG);
+  const uint32_t cfull0 = smem_u32(bars + 3 * STG), cempty0 = smem_u32(bars + 3 * STG + CST);
+  const uint32_t tfull = smem_u32(bars + 3 * STG + 2 * CST);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STG + 2 * CST + 2);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cb = blockIdx.x / a.splits, ks = blockIdx.x % a.splits;
+  const int c_lo = ks * a.n_chunks / a.splits, c_hi = (ks + 1) * a.n_chunks / a.splits;
+  const int n = c_hi - c_lo;
+
+  if (tid == 0) {
+    for (int s = 0; s < STG; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(afull0 + 8 * s, kGtProd);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int c = 0; c < CST; ++c) {
+      mbar_init(cfull0 + 8 * c, 1);
+      mbar_init(cempty0 + 8 * c, kGtProd);
+    }
+    mbar_init(tfull, 1);
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN < 32 ? 32 : 2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int idx = tid; idx < R * a.n_sh; idx += kGtThreads) {
+    const int r = idx / a.n_sh, e = idx - r * a.n_sh;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.books + ((int64_t)r * a.K + e) * 8));
+    uint8_t* row = book + ((size_t)r * kBookEntries + e) * 128;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(row + ((q + e) & 7) * 16) = v;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ===== TMA, two independent streams: lane 0 keeps CST chunks of code words in
+    // flight (one bulk copy per level; codes do not depend on the previous kernel, so
+    // the first ones go before griddepcontrol.wait), lane 1 the X tiles (the previous
+    // kernel's output) STG chunks ahead of the MMA
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int c = i % CST, ch = c_lo + i;
+        if (i >= CST) mbar_wait(cempty0 + 8 * c, ((i / CST) & 1) ^ 1);
+        mbar_arrive_expect_tx(cfull0 + 8 * c, (uint32_t)(R * CODEB));
+        const int64_t off = (int64_t)cb * 32 * (a.M / RPL) * 16 + (int64_t)ch * (kGtK / RPL) * 512;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          tma_load_1d(smem_u32(sc + (c * R + r) * CODEB), a.codes + r * a.level_bytes + off, CODEB, cfull0 + 8 * c);
+      }
+    } else if (lane == 1) {
+      pdl_wait();
+      for (int i = 0; i < n; ++i) {
+        const int s = i % STG;
+        if (i >= STG) mbar_wait(empty0 + 8 * s, ((i / STG) & 1) ^ 1);
+        mbar_arrive_expect_tx(full0 + 8 * s, (uint32_t)XB);
+        tma_load_2d(smem_u32(sx + s * XB), &tmap_x, (c_lo + i) * kGtK, 0, full0 + 8 * s);
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: per stage 2 halves x 4 K-steps of UMMA 128 x BN x 16
+    // idesc: D f32, A/B f16, A MN-major (transposed), B K-major, N = BN, M = 128
+    const uint32_t idesc = (1u << 4) | (1u << 15) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int s = i % STG;
+        const uint32_t ph = (i / STG) & 1;
+        mbar_wait(full0 + 8 * s, ph);
+        mbar_wait(afull0 + 8 * s, ph);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sa + s * kGtABytes), x_base = smem_u32(sx + s * XB);
+#pragma unroll
+        for (int k = 0; k < kGtK / 16; ++k) {
+          const uint64_t bdesc = umma_desc(x_base + k * 32, 16, 1024);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t adesc = umma_desc(a_base + h * (kGtABytes / 2) + k * 4096, 1024, 2048);
+            umma_f16(tmem_base + h * BN, adesc, bdesc, idesc, (i | k) != 0);
+          }
+        }
+        umma_commit(empty0 + 8 * s);
+      }
+      umma_commit(tfull);
+    }
+  } else if (warp < 2 + kGtProd) {
+    // ===== dequantisation producers: a stage is 64 K-rows x 32 sub-vector groups
+    const int dtid = (warp - 2) * 32 + lane;
+    constexpr int NPT = kGtProd * 32;
+    constexpr int WORDS = (kGtK / RPL) * 32;   // code words per level per stage
+    constexpr int TPW = NPT / WORDS;           // threads per word
+    constexpr int KR = RPL / TPW;              // rows per thread
+    const int w = dtid % WORDS, part = dtid / WORDS;
+    const int gi = w % 32, rg = w / 32;
+    const int h = gi >> 4, g16 = gi & 15, nb = g16 >> 3, c = g16 & 7;
+    const uint32_t rep = (uint32_t)(lane & 7) * 16;
+    for (int i = 0; i < n; ++i) {
+      const int s = i % STG, cs = i % CST;
+      mbar_wait(cfull0 + 8 * cs, (i / CST) & 1);  // code words landed
+      uint4 cw[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) cw[r] = *reinterpret_cast<const uint4*>(sc + (cs * R + r) * CODEB + w * 16);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cempty0 + 8 * cs);  // the code slot may be refilled
+      if (i >= STG) mbar_wait(empty0 + 8 * s, ((i / STG) & 1) ^ 1);  // the MMA is done with A slot s
+      uint8_t* at = sa + s * kGtABytes + h * (kGtABytes / 2);
+#pragma unroll
+      for (int kk = 0; kk < KR; ++kk) {
+        const int k = part * KR + kk;  // row within the word
+        uint4 e;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint32_t code;
+          if constexpr (CBYTES == 2) {
+            const uint32_t x = (&cw[r].x)[k / 2];
+            code = (k & 1) ? (x >> 16) : (x & 0xffffu);
+          } else {
+            code = ((&cw[r].x)[k / 4] >> (8 * (k % 4))) & 0xffu;
+          }
+          const uint4 q = *reinterpret_cast<const uint4*>(book + ((size_t)r * kBookEntries + code) * 128 + rep);
+          if (r == 0) {
+            e = q;
+          } else {
+            uint32_t* ew = &e.x;
+            const uint32_t* qw = &q.x;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const __half2 hs = __hadd2(*reinterpret_cast<const __half2*>(&ew[j]), *reinterpret_cast<const __half2*>(&qw[j]));
+              ew[j] = *reinterpret_cast<const uint32_t*>(&hs);
+            }
+          }
+        }
+        const int kr = rg * RPL + k;  // K-row within the stage
+        *reinterpret_cast<uint4*>(at + ((kr >> 3) * 2 + nb) * 1024 + (kr & 7) * 128 + ((c ^ (kr & 7)) << 4)) = e;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(afull0 + 8 * s);
+    }
+  } else {
+    // ===== epilogue: TMEM lanes = output columns, columns = batch rows (8 at a time);
+    // y / the partials may still be read by the previous kernel
+    pdl_wait();
+    const int quarter = warp & 3;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int64_t ncol = (int64_t)cb * 256 + hh * 128 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(hh * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 8) {
+        uint32_t r8[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r8[0]), "=r"(r8[1]), "=r"(r8[2]), "=r"(r8[3]), "=r"(r8[4]), "=r"(r8[5]), "=r"(r8[6]),
+                       "=r"(r8[7])
+                     : "r"(taddr + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int b = c0 + j;
+          if (b < a.B) {
+            const float v = __uint_as_float(r8[j]);
+            if (a.splits == 1) store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + ncol, v);
+            else a.part[((int64_t)ks * a.B + b) * a.N + ncol] = v;
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * BN < 32 ? 32 : 2 * BN));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Two-phase prefill (dequantise, then a dense tcgen05 GEMM). At prefill sizes the
 // fused kernels above are shared-memory-bound: every W element costs an LDS gather
 // and an STS into the UMMA layout on top of the tensor core's own operand traffic,
@@ -1082,6 +1323,127 @@ static int launch_two_phase(const Geom& g, const VqbTensor* w, const void* d_x, 
   if (a.y_dtype == VQB_F32) return bf ? launch_dense_pair<true, float>(mx, mw, a, st) : launch_dense_pair<false, float>(mx, mw, a, st);
   if (a.y_dtype == VQB_F16) return bf ? launch_dense_pair<true, __half>(mx, mw, a, st) : launch_dense_pair<false, __half>(mx, mw, a, st);
   return bf ? launch_dense_pair<true, __nv_bfloat16>(mx, mw, a, st) : launch_dense_pair<false, __nv_bfloat16>(mx, mw, a, st);
+}
+
+template <int CBYTES, int R, int BN>
+static int launch_gemv_tc_t(const CUtensorMap& mx, const GemvTcArgs& a, cudaStream_t st, int flags) {
+  auto kern = gemv_tc_kernel<CBYTES, R, BN>;
+  const size_t smem = gt_smem(CBYTES, R, BN);
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64] = {};
+  int dev = 0;
+  VQB_CUDA_CHECK(cudaGetDevice(&dev));
+  dev &= 63;
+  std::call_once(once[dev], [&] {
+    attr_err[dev] = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr_err[dev] != cudaSuccess) return cuda_error(attr_err[dev], "cudaFuncSetAttribute(gemv_tc_kernel)");
+  const int grid = a.n_cblk * a.splits;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGtThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (flags & VQB_FLAG_NO_PDL) ? 0 : 1;
+  VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, mx, a));
+  if (a.splits > 1) {
+    const int64_t n_out = (int64_t)a.B * a.N;
+    const int blocks = (int)std::min<int64_t>(ceil_div(n_out, 256), (int64_t)sm_count() * 4);
+    VQB_CUDA_CHECK(launch_pdl(gemm_splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st,
+                              static_cast<const float*>(a.part), a.splits, n_out, a.y, a.y_dtype));
+  }
+  set_kernel("gemv_tc");
+  set_launch(grid, kGtThreads, a.n_sh, 0);
+  return VQB_OK;
+}
+
+// K splits of the tcgen05 GEMV: one wave of CTAs over the column blocks
+static int gemv_tc_splits(int n_cblk, int n_chunks, int rows, int64_t N) {
+  // modelled time: waves x chunks per CTA x ~0.75 us per 64-row chunk, plus (split) the
+  // fp32 partials written and read back (~5 TB/s) and the reduce launch (~2 us)
+  const int sms = sm_count();
+  int best = 1;
+  double best_t = 1e30;
+  for (int sp = 1; sp <= std::max(1, n_chunks / 4); ++sp) {
+    const double waves = (double)((n_cblk * sp + sms - 1) / sms);
+    double t = waves * (double)((n_chunks + sp - 1) / sp) * 0.75;
+    if (sp > 1) t += (double)sp * rows * N * 8 / 5e6 + 2.0;
+    if (t < best_t - 1e-9) { best_t = t; best = sp; }
+  }
+  return best;
+}
+
+static bool gemv_tc_covers(const Geom& g, const VqbTensor* w, int x_dtype, int rows, const VqbLaunch* L) {
+  const int flags = L ? L->flags : 0;
+  if (flags & (VQB_FLAG_FORCE_GENERIC | VQB_FLAG_NO_GEMV_TC)) return false;
+  if (rows < 2 || rows > 64 || x_dtype != VQB_F16 || w->codebook_dtype != VQB_F16) return false;
+  if (w->layout != VQB_LAYOUT_GEMV_IL || g.v != 8 || g.sharing != VQB_SHARE_WHOLE || g.ndim != 2) return false;
+  if (!(g.R == 1 || g.R == 2) || !(g.bits == 8 || (g.bits == 16 && g.R == 1))) return false;
+  if (g.cols % 256 != 0 || g.rows % kGtK != 0) return false;
+  // every code must be resident in the 256-entry shared table
+  if (!(g.K <= 256 || (w->max_code >= 0 && w->max_code < 256))) return false;
+  // default: batches from kGemvTcMinRows, and every batch the CUDA-core / mma.sync
+  // kernels do not cover (3, 5-7)
+  return (flags & VQB_FLAG_GEMV_TC) || rows >= kGemvTcMinRows || !(rows == 1 || rows == 2 || rows == 4 || rows == 8);
+}
+
+int64_t gemv_tc_ws_bytes(const Geom& g, const VqbTensor* w, int rows, const VqbLaunch* L) {
+  if (!gemv_tc_covers(g, w, VQB_F16, rows, L)) return 0;
+  const int sp = gemv_tc_splits((int)(g.cols / 256), (int)(g.rows / kGtK), rows, g.cols);
+  return VQB_WS_COUNTER_BYTES + (sp > 1 ? (int64_t)sp * rows * g.cols * 4 : 0);
+}
+
+// Decode GEMV on tcgen05 for batches 4-64 (gemv.cu dispatches here). Returns 1 when
+// the configuration is not covered (the caller keeps its own kernels).
+int gemv_tc_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
+                     const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!gemv_tc_covers(g, w, x_dtype, rows, L) || (reinterpret_cast<uintptr_t>(x) & 15)) return 1;
+  const int flags = L ? L->flags : 0;
+  const int BN = rows <= 8 ? 8 : rows <= 16 ? 16 : rows <= 32 ? 32 : 64;
+  GemvTcArgs a;
+  a.n_cblk = (int)(g.cols / 256);
+  a.n_chunks = (int)(g.rows / kGtK);
+  a.splits = gemv_tc_splits(a.n_cblk, a.n_chunks, rows, g.cols);
+  const int64_t need = VQB_WS_COUNTER_BYTES + (a.splits > 1 ? (int64_t)a.splits * rows * g.cols * 4 : 0);
+  if (!ws || (int64_t)ws_bytes < need)
+    return set_error(VQB_ECAPACITY, "tcgen05 GEMV workspace too small: %zu < %lld", ws_bytes, (long long)need);
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap mx;
+  const cuuint64_t dims[2] = {(cuuint64_t)g.rows, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)g.rows * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kGtK, (cuuint32_t)BN};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return set_error(VQB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  a.codes = reinterpret_cast<const uint8_t*>(w->d_codes);
+  a.level_bytes = g.S * g.code_bytes;
+  a.books = reinterpret_cast<const uint16_t*>(w->d_codebooks);
+  a.y = y;
+  a.y_dtype = y_dtype;
+  a.B = rows;
+  a.M = (int)g.rows;
+  a.N = (int)g.cols;
+  a.K = g.K;
+  a.n_sh = std::min(g.K, kBookEntries);
+  a.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + VQB_WS_COUNTER_BYTES);
+#define VQB_GT(CBY, RR)                                                     \
+  switch (BN) {                                                             \
+    case 8: return launch_gemv_tc_t<CBY, RR, 8>(mx, a, st, flags);           \
+    case 16: return launch_gemv_tc_t<CBY, RR, 16>(mx, a, st, flags);         \
+    case 32: return launch_gemv_tc_t<CBY, RR, 32>(mx, a, st, flags);         \
+    default: return launch_gemv_tc_t<CBY, RR, 64>(mx, a, st, flags);         \
+  }
+  if (g.code_bytes == 2) { VQB_GT(2, 1) }
+  if (g.R == 1) { VQB_GT(1, 1) }
+  VQB_GT(1, 2)
+#undef VQB_GT
 }
 
 int gemm_usage(VqbUsage* u) {

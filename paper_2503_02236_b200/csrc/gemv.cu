@@ -977,6 +977,10 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
 // ---------------------------------------------------------------------------
 // dispatch
 
+int gemv_tc_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
+                     const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st);
+int64_t gemv_tc_ws_bytes(const Geom& g, const VqbTensor* w, int rows, const VqbLaunch* L);
+
 // host-side description of a fused activation transform (vqb_gemv_xf)
 struct GemvXf {
   int mode;  // VQB_XF_*
@@ -1059,7 +1063,7 @@ static FastPlan plan_fast(const Geom& g, const VqbTensor* t, int rows, int x_dty
 // workspace: the tagged partials (one B x COLS slot of 8-byte words per CTA) live
 // in the self-resetting head
 static int64_t fast_ws_bytes(const FastPlan& p, const Geom& g, int rows) {
-  if (!p.ok) return 0;
+  if (!p.ok) return VQB_WS_COUNTER_BYTES + 1024 * 64;  // (also the tcgen05 GEMV's partial slots)
   return VQB_WS_COUNTER_BYTES + 1024 * 64;  // tagged partials live in the head; + debug trace
 }
 
@@ -1163,6 +1167,14 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
   if (rows < 1) return set_error(VQB_ESHAPE, "activation rows must be >= 1, got %d", rows);
   if (x_dtype < VQB_F32 || x_dtype > VQB_BF16 || y_dtype < VQB_F32 || y_dtype > VQB_BF16)
     return set_error(VQB_ECONFIG, "unknown activation/output dtype");
+  if (!tp && !xf) {
+    // batches 4-64: the tcgen05 decode GEMV (csrc/gemm.cu) where it covers the configuration
+    const int t = gemv_tc_dispatch(g, w, x, x_dtype, rows, y, y_dtype, L, ws, ws_bytes, st);
+    if (t <= 0) {
+      if (used_fast && t == 0) *used_fast = true;
+      return t;
+    }
+  }
   FastPlan p = plan_fast(g, w, rows, x_dtype, L);
   GemvKernel kernel = p.ok ? fast_kernel_for(p, rows) : nullptr;
   // the activations are TMA-staged: 16-byte aligned rows
@@ -1380,6 +1392,7 @@ int64_t gemv_ws_bytes(const VqbTensor* w, int64_t rows, const VqbLaunch* L) {
   if (s) return s;
   FastPlan p = plan_fast(g, w, (int)rows, VQB_F16, L);
   int64_t a = (p.ok && fast_kernel_for(p, (int)rows)) ? fast_ws_bytes(p, g, (int)rows) : 0;
+  a = std::max(a, gemv_tc_ws_bytes(g, w, (int)rows, L));
   return std::max(a, generic_ws_bytes(g, (int)rows));
 }
 

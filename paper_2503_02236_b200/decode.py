@@ -114,11 +114,11 @@ class VQLlamaDecoder:
 
     # -- the step -----------------------------------------------------------------------------
 
-    gemv_max_rows = 16  # batches up to this take the decode GEMV (mma.sync at 4-16), larger ones the tcgen05 GEMM
+    gemv_max_rows = 64  # batches up to this take the decode GEMV (CUDA cores 1-2, mma.sync 4-8, tcgen05 9-64)
     fuse_norms = True  # batch 1: RMSNorm / SiLU gating fused into the following GEMV's prologue
 
     def _linear(self, w: DeviceVQTensor, x: torch.Tensor) -> torch.Tensor:
-        if x.shape[0] <= self.gemv_max_rows and x.shape[0] in (1, 2, 4, 8, 16):
+        if x.shape[0] <= self.gemv_max_rows:
             return ops.vq_gemv(w, x, out_dtype=torch.float16)
         return ops.vq_gemm(w, x, out_dtype=torch.float16)
 
@@ -131,7 +131,7 @@ class VQLlamaDecoder:
     def _row_linear(self, w: DeviceVQTensor, x: torch.Tensor) -> torch.Tensor:
         """A row-parallel linear and its all-reduce: fused over peer memory when the
         decoder holds a PeerComm and the batch takes the GEMV, else GEMV/GEMM + NCCL."""
-        if self.comm is not None and x.shape[0] <= self.gemv_max_rows and x.shape[0] in (1, 2, 4, 8, 16):
+        if self.comm is not None and x.shape[0] in (1, 2, 4, 8, 16):
             return self.comm.linear(w, x, "row", out_dtype=torch.float16)
         return self._reduce(self._linear(w, x))
 

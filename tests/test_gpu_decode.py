@@ -244,7 +244,7 @@ def _np_decode(sh, host, tokens, steps, capacity):
     return logits_all
 
 
-@pytest.mark.parametrize("batch", [1, 2, 4, 8])  # 4 and 8: tensor-core GEMV
+@pytest.mark.parametrize("batch", [1, 2, 4, 8, 16, 24])  # 4-8: mma.sync GEMV, 16-24: tcgen05 GEMV
 def test_decode_matches_numpy_model(batch, dev):
     capacity, steps = 64, 6
     sh, dec, host = _tiny_model(dev, batch, capacity)

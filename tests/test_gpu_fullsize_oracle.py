@@ -58,8 +58,8 @@ def test_full_size_gemv_vs_c_oracle(label, shape, v, bits, r, sharing, work, row
     w, codes, books, nreg, regions = _weight(dev, shape, v, bits, r, sharing, work)
     x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))
     y = ops.vq_gemv(w, torch.from_numpy(x).to(dev).half(), out_dtype=torch.float32)
-    fast = rows <= 8 or sharing == "whole"
-    assert N.last_kernel() == ("gemv_fast" if fast else "gemv_generic"), label
+    want = "gemv_fast" if rows <= 8 else "gemv_tc" if sharing == "whole" else "gemv_generic"
+    assert N.last_kernel() == want, label
     ref = CO.gemv(codes, books, shape, v, nreg, regions, x)
     assert _rel(y, ref) <= 1e-3, label
 

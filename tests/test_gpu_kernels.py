@@ -165,9 +165,9 @@ def test_gemv_fast_kernel(label, shape, v, bits, r, sharing, tile, work, rows, d
 
 @pytest.mark.parametrize("label,shape,v,bits,r,sharing,tile,work", FAST_GEMV)
 def test_gemv_batch16(label, shape, v, bits, r, sharing, tile, work, dev):
-    """Batch 16 on the tensor-core GEMV (two n8 batch tiles, the 16 column pairs of a
-    block split over two warps) where every code is in the shared tier; tile-shared
-    and global-tier configurations take the generic kernel, equally exact."""
+    """Batch 16: the tcgen05 decode GEMV where every code is in the shared tier and
+    N % 256 == 0 (the mma.sync kernel with two n8 batch tiles under VQB_FLAG_NO_GEMV_TC);
+    tile-shared and global-tier configurations take the generic kernel, equally exact."""
     from paper_2503_02236_b200.codec import Sharing, VQConfig
     N, DeviceVQTensor, ops = _mods()
     sh = Sharing.per_tile(*tile) if sharing == "tile" else Sharing.whole_tensor()
@@ -177,7 +177,7 @@ def test_gemv_batch16(label, shape, v, bits, r, sharing, tile, work, dev):
     x = O.round_f16(O.synthetic_tensor((16, shape[0]), 9))
     y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half())
     fast = v == 8 and sharing == "whole" and (work is not None or bits == 8)
-    assert N.last_kernel() == ("gemv_fast" if fast else "gemv_generic"), label
+    assert N.last_kernel() == ("gemv_tc" if fast else "gemv_generic"), label
     assert O.rel_err(y.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
     assert torch.equal(y, ops.vq_gemv(d, torch.from_numpy(x).to(dev).half()))
 
@@ -373,3 +373,27 @@ def test_gemm_two_phase_matches_fused(label, shape, v, bits, r, work, rows, dtyp
             y = ops.vq_gemm(d, x.to(dev), out_dtype=out_dtype, launch=L)
             assert N.last_kernel() == kern, (N.last_kernel(), kern)
             assert O.rel_err(y.float().cpu().numpy(), ref) <= tol, (label, kern, out_dtype)
+
+
+@pytest.mark.parametrize("rows", [3, 9, 16, 33, 64])
+@pytest.mark.parametrize("label,shape,v,bits,r,sharing,tile,work", [c for c in FAST_GEMV if c[5] == "whole" and (c[7] is not None or c[3] == 8)])
+def test_gemv_tcgen05(label, shape, v, bits, r, sharing, tile, work, rows, dev):
+    """The tcgen05 decode GEMV (batch = UMMA N, padded to 8..64; split-K partials reduced
+    in order): oracle parity, determinism, and the mma.sync kernel at 16 rows agrees."""
+    from paper_2503_02236_b200.codec import Sharing, VQConfig
+    N, DeviceVQTensor, ops = _mods()
+    cfg = VQConfig(v, bits, r, Sharing.whole_tensor())
+    codes, books, nreg, dense = _big_weight(shape, v, bits, r, sharing, tile, work)
+    d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev)
+    x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 11))
+    xt = torch.from_numpy(x).to(dev).half()
+    y = ops.vq_gemv(d, xt, out_dtype=torch.float32)
+    assert N.last_kernel() == "gemv_tc", label
+    assert O.rel_err(y.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
+    assert torch.equal(y, ops.vq_gemv(d, xt, out_dtype=torch.float32))
+    if rows == 16:
+        L = ops.launch_struct()
+        L.flags |= N.FLAG_NO_GEMV_TC
+        y2 = ops.vq_gemv(d, xt, out_dtype=torch.float32, launch=L)
+        assert N.last_kernel() == "gemv_fast"
+        assert O.rel_err(y2.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
