@@ -686,7 +686,11 @@ constexpr int kGemvTcMinRows = 9;                // default from 9 rows: at 4-8 
 constexpr int kGtProd = 16;                       // dequantisation producer warps (2..17)
 constexpr int kGtEpi = 4;                         // epilogue warps (18..21)
 constexpr int kGtThreads = (2 + kGtProd + kGtEpi) * 32;
-__host__ __device__ constexpr int gt_stages(int R) { return 3; }  // A / X ring (producer -> MMA hand-off)
+// producer groups: the 16 dequantisation warps form gt_stages(R) groups that work on
+// consecutive stages concurrently (one group's latency chain — code LDS, gathers, STS,
+// proxy fence, barrier — no longer serialises the stages); the A / X ring has one slot
+// per group
+__host__ __device__ constexpr int gt_stages(int R) { return R == 1 ? 4 : 2; }
 constexpr int kGtCodeStages = 8;                   // code-word ring: the HBM latency is hidden here
 constexpr int kGtK = 64;                          // K rows per stage (one SW128 span)
 constexpr int kGtABytes = 256 * kGtK * 2;         // W^T tile: 256 output columns x 64 K (two 16 KB halves)
@@ -725,6 +729,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(book + R * kBookBytes);
   // full[s] (X landed), afull[s] (A written), empty[s] (MMA done with slot s),
   // cfull[c] (code words landed), cempty[c] (producers read them), tfull (accumulator done)
+  constexpr int GW = kGtProd / STG;  // warps per producer group
   const uint32_t full0 = smem_u32(bars), afull0 = smem_u32(bars + STG), empty0 = smem_u32(bars + 2 * STG);
   const uint32_t cfull0 = smem_u32(bars + 3 * STG), cempty0 = smem_u32(bars + 3 * STG + CST);
   const uint32_t tfull = smem_u32(bars + 3 * STG + 2 * CST);
@@ -738,12 +743,12 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < STG; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(afull0 + 8 * s, kGtProd);
+      mbar_init(afull0 + 8 * s, GW);
       mbar_init(empty0 + 8 * s, 1);
     }
     for (int c = 0; c < CST; ++c) {
       mbar_init(cfull0 + 8 * c, 1);
-      mbar_init(cempty0 + 8 * c, kGtProd);
+      mbar_init(cempty0 + 8 * c, GW);
     }
     mbar_init(tfull, 1);
     mbar_fence_init();
@@ -817,54 +822,65 @@ __global__ void __launch_bounds__(kGtThreads, 1)
       umma_commit(tfull);
     }
   } else if (warp < 2 + kGtProd) {
-    // ===== dequantisation producers: a stage is 64 K-rows x 32 sub-vector groups
-    const int dtid = (warp - 2) * 32 + lane;
-    constexpr int NPT = kGtProd * 32;
-    constexpr int WORDS = (kGtK / RPL) * 32;   // code words per level per stage
-    constexpr int TPW = NPT / WORDS;           // threads per word
-    constexpr int KR = RPL / TPW;              // rows per thread
-    const int w = dtid % WORDS, part = dtid / WORDS;
-    const int gi = w % 32, rg = w / 32;
-    const int h = gi >> 4, g16 = gi & 15, nb = g16 >> 3, c = g16 & 7;
+    // ===== dequantisation producers: a stage is 64 K-rows x 32 sub-vector groups;
+    // group grp takes stages grp, grp + STG, ... (its own A slot)
+    const int pw = warp - 2, grp = pw / GW;
+    const int gtid = (pw % GW) * 32 + lane;
+    constexpr int NPT = GW * 32;
+    constexpr int WORDS = (kGtK / RPL) * 32;        // code words per level per stage
+    constexpr int TPW = NPT >= WORDS ? NPT / WORDS : 1;  // threads per word
+    constexpr int WPT = NPT >= WORDS ? 1 : WORDS / NPT;  // words per thread
+    constexpr int KR = RPL / TPW;                   // rows per thread per word
     const uint32_t rep = (uint32_t)(lane & 7) * 16;
-    for (int i = 0; i < n; ++i) {
+    for (int i = grp; i < n; i += STG) {
       const int s = i % STG, cs = i % CST;
       mbar_wait(cfull0 + 8 * cs, (i / CST) & 1);  // code words landed
-      uint4 cw[R];
+      uint4 cw[WPT][R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) cw[r] = *reinterpret_cast<const uint4*>(sc + (cs * R + r) * CODEB + w * 16);
+      for (int ww = 0; ww < WPT; ++ww) {
+        const int w = (gtid + ww * NPT) % WORDS;
+#pragma unroll
+        for (int r = 0; r < R; ++r) cw[ww][r] = *reinterpret_cast<const uint4*>(sc + (cs * R + r) * CODEB + w * 16);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(cempty0 + 8 * cs);  // the code slot may be refilled
       if (i >= STG) mbar_wait(empty0 + 8 * s, ((i / STG) & 1) ^ 1);  // the MMA is done with A slot s
-      uint8_t* at = sa + s * kGtABytes + h * (kGtABytes / 2);
 #pragma unroll
-      for (int kk = 0; kk < KR; ++kk) {
-        const int k = part * KR + kk;  // row within the word
-        uint4 e;
+      for (int ww = 0; ww < WPT; ++ww) {
+        const int idx = gtid + ww * NPT;
+        const int w = idx % WORDS, part = (idx / WORDS) % TPW;
+        const int gi = w % 32, rg = w / 32;
+        const int h = gi >> 4, g16 = gi & 15, nb = g16 >> 3, c = g16 & 7;
+        uint8_t* at = sa + s * kGtABytes + h * (kGtABytes / 2);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          uint32_t code;
-          if constexpr (CBYTES == 2) {
-            const uint32_t x = (&cw[r].x)[k / 2];
-            code = (k & 1) ? (x >> 16) : (x & 0xffffu);
-          } else {
-            code = ((&cw[r].x)[k / 4] >> (8 * (k % 4))) & 0xffu;
-          }
-          const uint4 q = *reinterpret_cast<const uint4*>(book + ((size_t)r * kBookEntries + code) * 128 + rep);
-          if (r == 0) {
-            e = q;
-          } else {
-            uint32_t* ew = &e.x;
-            const uint32_t* qw = &q.x;
+        for (int kk = 0; kk < KR; ++kk) {
+          const int k = part * KR + kk;  // row within the word
+          uint4 e;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const __half2 hs = __hadd2(*reinterpret_cast<const __half2*>(&ew[j]), *reinterpret_cast<const __half2*>(&qw[j]));
-              ew[j] = *reinterpret_cast<const uint32_t*>(&hs);
+          for (int r = 0; r < R; ++r) {
+            uint32_t code;
+            if constexpr (CBYTES == 2) {
+              const uint32_t x = (&cw[ww][r].x)[k / 2];
+              code = (k & 1) ? (x >> 16) : (x & 0xffffu);
+            } else {
+              code = ((&cw[ww][r].x)[k / 4] >> (8 * (k % 4))) & 0xffu;
+            }
+            const uint4 q = *reinterpret_cast<const uint4*>(book + ((size_t)r * kBookEntries + code) * 128 + rep);
+            if (r == 0) {
+              e = q;
+            } else {
+              uint32_t* ew = &e.x;
+              const uint32_t* qw = &q.x;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const __half2 hs = __hadd2(*reinterpret_cast<const __half2*>(&ew[j]), *reinterpret_cast<const __half2*>(&qw[j]));
+                ew[j] = *reinterpret_cast<const uint32_t*>(&hs);
+              }
             }
           }
+          const int kr = rg * RPL + k;  // K-row within the stage
+          *reinterpret_cast<uint4*>(at + ((kr >> 3) * 2 + nb) * 1024 + (kr & 7) * 128 + ((c ^ (kr & 7)) << 4)) = e;
         }
-        const int kr = rg * RPL + k;  // K-row within the stage
-        *reinterpret_cast<uint4*>(at + ((kr >> 3) * 2 + nb) * 1024 + (kr & 7) * 128 + ((c ^ (kr & 7)) << 4)) = e;
       }
       fence_proxy_async();
       __syncwarp();
