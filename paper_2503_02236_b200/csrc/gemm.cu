@@ -682,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // accumulator lives in TMEM. Split partials go to the workspace as plain fp32 and an
 // ordered reduce kernel sums them (deterministic). This replaces mma.sync for the
 // batches where the legacy HMMA path (~50 TFLOP/s on sm_100) made the GEMV compute-bound.
-constexpr int kGemvTcMinRows = 9;                // default from 9 rows: at 4-8 the mma.sync GEMV is as fast (measured)
+constexpr int kGemvTcMinRows = 5;                // default from 5 rows: at 4 the mma.sync GEMV is faster (measured)
 constexpr int kGtProd = 16;                       // dequantisation producer warps (2..17)
 constexpr int kGtEpi = 4;                         // epilogue warps (18..21)
 constexpr int kGtThreads = (2 + kGtProd + kGtEpi) * 32;

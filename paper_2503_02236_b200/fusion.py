@@ -13,11 +13,11 @@ On B200 the level selects a kernel family (``b200_fusion``):
 * ``register`` — looked-up entries go straight into the consumer's registers:
   CUDA-core FMAs where a lane owns whole sub-vectors (GEMV batch 1-2, decode
   attention: zero exchanges needed), or mma.sync A fragments gathered by
-  ``ldmatrix.trans`` from the replicated table (GEMV batch 4-8: the hardware
+  ``ldmatrix.trans`` from the replicated table (GEMV batch 4: the hardware
   transpose replaces the xor exchange schedule);
 * ``shared`` — the dequantized W tile is written to shared memory in the UMMA
-  canonical layout for tcgen05 (prefill GEMM): tcgen05.mma reads operands only
-  from shared memory / TMEM.
+  canonical layout for tcgen05 (decode GEMV at 5-64 rows with the batch as the
+  UMMA N, prefill GEMM): tcgen05.mma reads operands only from shared memory / TMEM.
 """
 
 import json
@@ -31,7 +31,8 @@ WARP = 32
 THRES_SHUFFLE = 5
 STYLE_STRIDED = "strided"
 STYLE_MMA = "mma"
-B200_GEMV_MAX_ROWS = 8  # rows above this take the tcgen05 GEMM (shared-level fusion)
+B200_GEMV_MAX_ROWS = 4  # rows above this take tcgen05 (shared-level fusion): the decode GEMV to 64 rows, then the GEMM
+B200_GEMV_TC_MAX_ROWS = 64
 
 
 def _pow2(n: int) -> bool:
@@ -75,8 +76,11 @@ def choose_fusion_level(layouts: LayoutPair, thres_shuffle: int = THRES_SHUFFLE)
 
 
 def b200_fusion(op_kind: str, rows: int = 1) -> str:
-    """Fusion level of the sm_100a kernel that serves the op (see module doc)."""
-    if op_kind == "gemm" and rows > B200_GEMV_MAX_ROWS:
+    """Fusion level of the sm_100a kernel that serves the op (see module doc): up to
+    4 rows the lookups feed registers (CUDA cores / mma.sync); above, the dequantized
+    W tile is staged in shared memory for tcgen05 (the decode GEMV with the batch as
+    the UMMA N to 64 rows, the GEMM beyond)."""
+    if rows > B200_GEMV_MAX_ROWS:
         return "shared"
     return "register"
 

@@ -25,7 +25,7 @@ from .cacheplan import CachePlan, compute_slack, plan_b200_tiers, plan_cache
 from .codec import Codebook, QuantizedTensor, VQConfig
 from .dataflow import ATTENTION, GEMM, GEMV, ComputeOp, DataflowPlan, b200_split, build_dataflow
 from .errors import CapacityError, ConfigError, ShapeError
-from .fusion import (B200_GEMV_MAX_ROWS, STYLE_MMA, STYLE_STRIDED, THRES_SHUFFLE, LayoutPair, MappingError,
+from .fusion import (B200_GEMV_MAX_ROWS, B200_GEMV_TC_MAX_ROWS, STYLE_MMA, STYLE_STRIDED, THRES_SHUFFLE, LayoutPair, MappingError,
                      ShuffleSchedule, b200_fusion, build_shuffle_schedule, choose_fusion_level)
 from .gpumodel import GpuModel, KernelUsage, load_gpu_model
 from .report import SimReport
@@ -292,12 +292,14 @@ class B200Machine:
             wd = self.to_device(w)
             at, host = self._operand(a)
             # fusion level -> kernel family: "register" = lookups feed the consumer's
-            # registers (GEMV kernels, rows <= 8); "shared" = dequantized tiles staged
-            # in shared memory for tcgen05 (GEMM). One activation row always takes the
+            # registers (GEMV kernels, rows <= 4); "shared" = dequantized tiles staged
+            # in shared memory for tcgen05 (the decode GEMV to 64 rows, then the GEMM). One activation row always takes the
             # GEMV (a 128-row MMA tile would be 1/128 used).
             rows = 1 if at.dim() == 1 else at.shape[0]
-            gemv_ok = rows <= B200_GEMV_MAX_ROWS and rows in (1, 2, 4, 8)
-            use_gemv = op.kind == GEMV or (gemv_ok and (plans.fusion_level == "register" or rows == 1))
+            gemv_ok = rows <= B200_GEMV_MAX_ROWS and rows in (1, 2, 4)
+            # shared level at 5-64 rows: the tcgen05 decode GEMV (batch = UMMA N)
+            tc_gemv = plans.fusion_level == "shared" and B200_GEMV_MAX_ROWS < rows <= B200_GEMV_TC_MAX_ROWS
+            use_gemv = op.kind == GEMV or tc_gemv or (gemv_ok and (plans.fusion_level == "register" or rows == 1))
             fn = vq_gemv if use_gemv else vq_gemm
             if ev:
                 ev[0].record()

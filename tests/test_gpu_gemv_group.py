@@ -46,7 +46,8 @@ def test_partial_column_block_stays_fast(shape, rows, dev):
     w, dense = _weight(m, n, 5 + rows, dev)
     x = O.round_f16(O.synthetic_tensor((rows, m), 7))
     y = vq_gemv(w, torch.from_numpy(x).to(dev).half(), out_dtype=torch.float32)
-    assert N.last_kernel() == "gemv_fast"
+    # never the generic kernel: the decode GEMV families (tcgen05 from 5 rows where N % 256 == 0)
+    assert N.last_kernel() in ("gemv_fast", "gemv_tc")
     assert O.rel_err(y.cpu().numpy(), O.matmul_ref(x, dense)) <= TOL_F16
 
 

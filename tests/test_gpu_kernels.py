@@ -154,12 +154,14 @@ def test_gemv_fast_kernel(label, shape, v, bits, r, sharing, tile, work, rows, d
     d = DeviceVQTensor.from_quantized(_qt(codes, books, nreg, shape, cfg), device=dev)
     assert d.layout == "gemv"
     x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))
-    y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half())
+    L = ops.launch_struct()
+    L.flags |= N.FLAG_NO_GEMV_TC  # this kernel family (batch 8 defaults to the tcgen05 GEMV)
+    y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half(), launch=L)
     assert N.last_kernel() == "gemv_fast"
     ref = O.matmul_ref(x, dense)
     assert O.rel_err(y.cpu().numpy(), ref) <= TOL_F16
     # second launch reuses the self-reset split counters
-    y2 = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half())
+    y2 = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half(), launch=L)
     assert torch.equal(y, y2), "split reduction must be deterministic"
 
 
@@ -195,9 +197,11 @@ def test_gemv_cuda_core_path_at_mma_batches(label, shape, v, bits, r, sharing, t
     x = torch.from_numpy(O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))).to(dev).half()
     ref = O.matmul_ref(x.float().cpu().numpy(), dense)
     L = ops.launch_struct()
-    L.flags = N.FLAG_NO_MMA
+    L.flags = N.FLAG_NO_MMA | N.FLAG_NO_GEMV_TC
     y_fma = ops.vq_gemv(d, x, launch=L)
-    y_mma = ops.vq_gemv(d, x)
+    L2 = ops.launch_struct()
+    L2.flags = N.FLAG_NO_GEMV_TC
+    y_mma = ops.vq_gemv(d, x, launch=L2)
     assert N.last_kernel() == "gemv_fast"
     assert O.rel_err(y_fma.cpu().numpy(), ref) <= TOL_F16
     assert O.rel_err(y_mma.cpu().numpy(), ref) <= TOL_F16
