@@ -315,46 +315,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   }
   pdl_launch_dependents();
   attn_trace(a, 0);
-  // L2 prefetch hints, issued before waiting on the preceding kernel: this CTA's code
-  // ranges (K and V) and the books of its first head. The length is read early and
-  // only steers the hints (a stale value prefetches a slightly different range, it
-  // never changes a result); at small batch this takes the HBM latency of the first
-  // code batches and the book copy off the CTA's critical path.
-  {
-    const int Th = a.len_ptr ? max(1, min(*reinterpret_cast<const volatile int*>(a.len_ptr), a.T_cap)) : a.T;
-    const int NTh = (Th + kAttnChunk - 1) / kAttnChunk;
-    const int Uh = a.H * a.B * NTh;
-    const int GEh = min((int)gridDim.x, Uh);
-    if ((int)blockIdx.x < GEh && lane == 0) {
-      const int v0 = (int)((int64_t)blockIdx.x * Uh / GEh), v1 = (int)((int64_t)(blockIdx.x + 1) * Uh / GEh);
-      // one 8 KB piece (128 tokens of one stream) per warp and step, K and V alternating
-      const int64_t TG = (int64_t)a.T_cap * G;
-      int piece = 0;
-      int budget = 2 * kAttnChunk;  // tokens hinted per CTA: the first two chunks (~19 MB of L2 over 148 CTAs)
-      for (int u = v0; u < v1 && budget > 0;) {
-        const int h = u / (a.B * NTh), b = (u / NTh) % a.B, tc0 = u % NTh;
-        const int se = min(v1, (u / NTh + 1) * NTh);
-        const int64_t t0 = (int64_t)tc0 * kAttnChunk;
-        const int64_t t1 = min(min((int64_t)(tc0 + se - u) * kAttnChunk, (int64_t)Th), t0 + budget);
-        budget -= (int)(t1 - t0);
-        const int64_t base = (int64_t)(b * a.H + h) * TG;
-        for (int64_t off = t0 * G; off < t1 * G; off += 8192, piece += 2) {
-          const uint32_t bytes = (uint32_t)min((int64_t)8192, t1 * G - off);
-          if (piece % kAttnWarps == warp)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.kc + base + off), "r"(bytes) : "memory");
-          if ((piece + 1) % kAttnWarps == warp)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.vc + base + off), "r"(bytes) : "memory");
-        }
-        u = se;
-      }
-      if (warp == kAttnWarps - 1 && a.kbt && a.vbt && v0 < v1) {
-        const int h0 = v0 / (a.B * NTh);
-        const uint32_t bb = 256u * G * EPB;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.kbt + (int64_t)h0 * 256 * G * V), "r"(bb) : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.vbt + (int64_t)h0 * 256 * G * V), "r"(bb) : "memory");
-      }
-    }
-  }
   pdl_wait();  // q, the fresh KV codes and the length come from the preceding kernels
   attn_trace(a, 1);
   const uint32_t lut_base = smem_u32(lut_s);
@@ -404,9 +364,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     constexpr int KPER = (256 / EPL + KSTEP - 1) / KSTEP;
     const bool switch_h = (h != cur_h);
     const int g = tid % G;  // constant per thread since kAttnThreads % G == 0
-    // the warp's first code batch is requested before the books / LUT are ready
-    uint4 ka[2 * GPL], va[2 * GPL];
-    if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va);
     float qv[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) qv[j] = load_as_f32(a.q, a.q_dtype, (int64_t)bh * C + g * V + j) * a.scale_log2;
@@ -491,6 +448,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     for (int j = 0; j < GPL; ++j)
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+    uint4 ka[2 * GPL], va[2 * GPL];
+    if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va);
     if (aligned) attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
     else attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
 

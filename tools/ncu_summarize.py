@@ -34,7 +34,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 def main():
     name, path = sys.argv[1], sys.argv[2]
-    alg = int(sys.argv[3]) if len(sys.argv) > 3 else None
+    alg = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] else None
     desc = sys.argv[4] if len(sys.argv) > 4 else ""
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
