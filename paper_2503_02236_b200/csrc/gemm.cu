@@ -691,7 +691,8 @@ constexpr int kGtThreads = (2 + kGtProd + kGtEpi) * 32;
 // proxy fence, barrier — no longer serialises the stages); the A / X ring has one slot
 // per group
 __host__ __device__ constexpr int gt_stages(int R) { return R == 1 ? 4 : 2; }
-constexpr int kGtCodeStages = 8;                   // code-word ring: the HBM latency is hidden here
+__host__ __device__ constexpr int gt_code_stages(int BN) { return BN <= 32 ? 8 : 4; }  // code-word ring (HBM latency)
+__host__ __device__ constexpr int gt_x_stages(int BN) { return BN <= 32 ? 8 : 6; }     // X ring (its own depth)
 constexpr int kGtK = 64;                          // K rows per stage (one SW128 span)
 constexpr int kGtABytes = 256 * kGtK * 2;         // W^T tile: 256 output columns x 64 K (two 16 KB halves)
 
@@ -708,8 +709,9 @@ struct GemvTcArgs {
 
 __host__ __device__ constexpr int gt_code_bytes(int cbytes, int R) { return R * (kGtK / (16 / cbytes)) * 512; }
 __host__ __device__ constexpr size_t gt_smem(int cbytes, int R, int BN) {
-  return 1024 + (size_t)R * kBookBytes + (size_t)gt_stages(R) * (kGtABytes + BN * 128) +
-         (size_t)kGtCodeStages * gt_code_bytes(cbytes, R) + (3 * gt_stages(R) + 2 * kGtCodeStages + 4) * 8 + 16;
+  return 1024 + (size_t)R * kBookBytes + (size_t)gt_stages(R) * kGtABytes + (size_t)gt_x_stages(BN) * BN * 128 +
+         (size_t)gt_code_stages(BN) * gt_code_bytes(cbytes, R) +
+         (2 * gt_stages(R) + 2 * gt_x_stages(BN) + 2 * gt_code_stages(BN) + 4) * 8 + 16;
 }
 
 template <int CBYTES, int R, int BN>
@@ -721,19 +723,22 @@ __global__ void __launch_bounds__(kGtThreads, 1)
   constexpr int STG = gt_stages(R);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  constexpr int CST = gt_code_stages(BN), XST = gt_x_stages(BN);
   uint8_t* sa = smem;                                   // STG x 32 KB (A: W^T tiles)
-  uint8_t* sx = sa + STG * kGtABytes;                   // STG x XB (B: X tiles)
-  constexpr int CST = kGtCodeStages;
-  uint8_t* sc = sx + STG * XB;                          // CST x R x CODEB (code words)
+  uint8_t* sx = sa + STG * kGtABytes;                   // XST x XB (B: X tiles)
+  uint8_t* sc = sx + XST * XB;                          // CST x R x CODEB (code words)
   uint8_t* book = sc + CST * R * CODEB;                 // R x 256 entries x 128 B (replicated)
   uint64_t* bars = reinterpret_cast<uint64_t*>(book + R * kBookBytes);
-  // full[s] (X landed), afull[s] (A written), empty[s] (MMA done with slot s),
-  // cfull[c] (code words landed), cempty[c] (producers read them), tfull (accumulator done)
-  constexpr int GW = kGtProd / STG;  // warps per producer group
-  const uint32_t full0 = smem_u32(bars), afull0 = smem_u32(bars + STG), empty0 = smem_u32(bars + 2 * STG);
-  const uint32_t cfull0 = smem_u32(bars + 3 * STG), cempty0 = smem_u32(bars + 3 * STG + CST);
-  const uint32_t tfull = smem_u32(bars + 3 * STG + 2 * CST);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STG + 2 * CST + 2);
+  // afull[s] (A written), empty[s] (MMA done with A slot s), full[x] (X landed),
+  // xempty[x] (MMA done with X slot x), cfull[c] (code words landed), cempty[c]
+  // (producers read them), tfull (accumulator done)
+  constexpr int NGRP = STG >= 2 ? STG / 2 : 1;  // producer groups, two A slots each (fill one while the MMA reads the other)
+  constexpr int GW = kGtProd / NGRP;           // warps per producer group
+  const uint32_t afull0 = smem_u32(bars), empty0 = smem_u32(bars + STG);
+  const uint32_t full0 = smem_u32(bars + 2 * STG), xempty0 = smem_u32(bars + 2 * STG + XST);
+  const uint32_t cfull0 = smem_u32(bars + 2 * STG + 2 * XST), cempty0 = smem_u32(bars + 2 * STG + 2 * XST + CST);
+  const uint32_t tfull = smem_u32(bars + 2 * STG + 2 * XST + 2 * CST);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STG + 2 * XST + 2 * CST + 2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cb = blockIdx.x / a.splits, ks = blockIdx.x % a.splits;
@@ -742,9 +747,12 @@ __global__ void __launch_bounds__(kGtThreads, 1)
 
   if (tid == 0) {
     for (int s = 0; s < STG; ++s) {
-      mbar_init(full0 + 8 * s, 1);
       mbar_init(afull0 + 8 * s, GW);
       mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int x = 0; x < XST; ++x) {
+      mbar_init(full0 + 8 * x, 1);
+      mbar_init(xempty0 + 8 * x, 1);
     }
     for (int c = 0; c < CST; ++c) {
       mbar_init(cfull0 + 8 * c, 1);
@@ -790,10 +798,10 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     } else if (lane == 1) {
       pdl_wait();
       for (int i = 0; i < n; ++i) {
-        const int s = i % STG;
-        if (i >= STG) mbar_wait(empty0 + 8 * s, ((i / STG) & 1) ^ 1);
-        mbar_arrive_expect_tx(full0 + 8 * s, (uint32_t)XB);
-        tma_load_2d(smem_u32(sx + s * XB), &tmap_x, (c_lo + i) * kGtK, 0, full0 + 8 * s);
+        const int x = i % XST;
+        if (i >= XST) mbar_wait(xempty0 + 8 * x, ((i / XST) & 1) ^ 1);
+        mbar_arrive_expect_tx(full0 + 8 * x, (uint32_t)XB);
+        tma_load_2d(smem_u32(sx + x * XB), &tmap_x, (c_lo + i) * kGtK, 0, full0 + 8 * x);
       }
     }
   } else if (warp == 1) {
@@ -802,12 +810,11 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     const uint32_t idesc = (1u << 4) | (1u << 15) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     if (lane == 0) {
       for (int i = 0; i < n; ++i) {
-        const int s = i % STG;
-        const uint32_t ph = (i / STG) & 1;
-        mbar_wait(full0 + 8 * s, ph);
-        mbar_wait(afull0 + 8 * s, ph);
+        const int s = i % STG, x = i % XST;
+        mbar_wait(full0 + 8 * x, (i / XST) & 1);
+        mbar_wait(afull0 + 8 * s, (i / STG) & 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sa + s * kGtABytes), x_base = smem_u32(sx + s * XB);
+        const uint32_t a_base = smem_u32(sa + s * kGtABytes), x_base = smem_u32(sx + x * XB);
 #pragma unroll
         for (int k = 0; k < kGtK / 16; ++k) {
           const uint64_t bdesc = umma_desc(x_base + k * 32, 16, 1024);
@@ -818,12 +825,13 @@ __global__ void __launch_bounds__(kGtThreads, 1)
           }
         }
         umma_commit(empty0 + 8 * s);
+        umma_commit(xempty0 + 8 * x);
       }
       umma_commit(tfull);
     }
   } else if (warp < 2 + kGtProd) {
     // ===== dequantisation producers: a stage is 64 K-rows x 32 sub-vector groups;
-    // group grp takes stages grp, grp + STG, ... (its own A slot)
+    // group grp takes stages grp, grp + NGRP, ... (two A slots of its own)
     const int pw = warp - 2, grp = pw / GW;
     const int gtid = (pw % GW) * 32 + lane;
     constexpr int NPT = GW * 32;
@@ -832,7 +840,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     constexpr int WPT = NPT >= WORDS ? 1 : WORDS / NPT;  // words per thread
     constexpr int KR = RPL / TPW;                   // rows per thread per word
     const uint32_t rep = (uint32_t)(lane & 7) * 16;
-    for (int i = grp; i < n; i += STG) {
+    for (int i = grp; i < n; i += NGRP) {
       const int s = i % STG, cs = i % CST;
       mbar_wait(cfull0 + 8 * cs, (i / CST) & 1);  // code words landed
       uint4 cw[WPT][R];
