@@ -230,6 +230,17 @@ int vqb_attn_decode_len(const VqbTensor* k, const VqbTensor* v, const void* d_q,
                         int32_t H, int32_t T, int32_t C, const int32_t* d_len, void* d_out, int32_t out_dtype,
                         const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Fused decode front end + attention: d_qkv is the fused qkv projection output
+ * (B, 3*H*C) fp16 of the new token; the kernel ropes q, and the CTA covering position
+ * d_len[0]-1 of each (b, h) ropes k and quantizes the new K and V rows (as
+ * vqb_qkv_rope_append) against the books it holds in shared memory, writes the codes
+ * into the caches and attends over the first d_len[0] tokens (as vqb_attn_decode_len).
+ * CQ-4 configuration (v = 2, C = 128, KV_IL caches, fp16 books); one launch instead of
+ * two, and the books are read once per step. */
+int vqb_attn_decode_append(const VqbTensor* k_cache, const VqbTensor* v_cache, const void* d_qkv, int32_t B,
+                           int32_t H, int32_t C, const int32_t* d_len, float theta, void* d_out, int32_t out_dtype,
+                           const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Online KV quantization (codec.py:367-389): nearest centroid (float64 distance,
  * lowest index on ties) of n_tok new rows per (b, h) into the (B, H, T_cap, C) code
  * stream of t (KV_IL or PLAIN layout, fp16 codebooks, any R). Row (b, h, j) of the

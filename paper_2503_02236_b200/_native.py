@@ -47,7 +47,7 @@ EXPORTS = (
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
     "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error", "vqb_gemv_grouped",
     "vqb_tp_buffer_bytes", "vqb_ipc_get_handle", "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp",
-    "vqb_tp_finish", "vqb_tp_take_error", "vqb_gemv_xf",
+    "vqb_tp_finish", "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append",
 )
 XF_RMSNORM, XF_SILU_MUL = 1, 2
 
@@ -157,6 +157,7 @@ def lib():
             L.vqb_ipc_close_handle.argtypes = [vp]
             L.vqb_gemv_tp.argtypes = [T, vp, i32, i32, i32, C, La, vp, sz, vp]
             L.vqb_gemv_xf.argtypes = [T, vp, i32, i32, vp, vp, vp, f32, vp, i32, La, vp, sz, vp]
+            L.vqb_attn_decode_append.argtypes = [T, T, vp, i32, i32, i32, vp, f32, vp, i32, La, vp, sz, vp]
             L.vqb_tp_finish.argtypes = [C, i32, i32, i32, vp, i32, vp]
             L.vqb_tp_take_error.argtypes = [C, P(i32)]
             L.vqb_debug_smem_base.argtypes = [vp, vp]
@@ -166,7 +167,7 @@ def lib():
                          "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append",
                          "vqb_take_device_error", "vqb_gemv_grouped", "vqb_ipc_get_handle",
                          "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp", "vqb_tp_finish",
-                         "vqb_tp_take_error", "vqb_gemv_xf"):
+                         "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib

@@ -62,6 +62,15 @@ struct AttnArgs {
   const int* len_ptr;     // optional device-resident valid length (decode loops in CUDA graphs)
   float scale_log2;
   unsigned long long* trace;  // debug (VqbLaunch.flags & 32): per-CTA phase timestamps, 8 per CTA
+  // fused decode front end (vqb_attn_decode_append): q, k, v come raw from the fused qkv
+  // projection (B, 3*H*C); q is roped by every CTA of its (b, h), and the CTA whose span
+  // holds position len-1 ropes k and quantizes the new K and V rows against the books
+  // it already has in shared memory (the qkv_rope_append arithmetic), writing the codes
+  // into the caches before it streams that token
+  const __half* qkv;
+  float log2_theta;
+  uint8_t* kc_w;
+  uint8_t* vc_w;
 };
 
 // per-CTA phase sums: slot 2 prologue (books + LUT), 3 streaming, 4 merge, 6 spans
@@ -107,6 +116,18 @@ struct AttnSmem {
   static_assert(256 * G * 4 <= region && 256 * G * EPB <= region, "region overflow");
 };
 
+// RoPE (rotate-half) of channel c at position pos, fp32 angle like the HF rotary
+// embedding — the arithmetic of decode.cu's rope kernels
+__device__ __forceinline__ float rope_channel_attn(const __half* x, int c, int C, float log2_theta, int pos) {
+  const int half = C / 2;
+  const int i = c < half ? c : c - half;
+  const float inv_freq = exp2f(-log2_theta * (2.0f * i) / (float)C);
+  float sn, cs;
+  sincosf((float)pos * inv_freq, &sn, &cs);
+  const float x0 = __half2float(x[i]), x1 = __half2float(x[i + half]);
+  return c < half ? x0 * cs - x1 * sn : x1 * cs + x0 * sn;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -133,16 +154,23 @@ __device__ __forceinline__ uint32_t row_addr(uint32_t w, int k, uint32_t colbase
 }
 
 // A warp's 32-token batch of K and V codes (KV_IL: 2*GPL 16-byte words per lane each).
+// (the batch holding a token appended by this kernel is read from L2 with ld.global.cg:
+// the non-coherent streaming path may not see the kernel's own writes)
 template <int V, int GPL>
 __device__ __forceinline__ void attn_load_batch(const AttnArgs& a, int bh, int t0, uint4 (&kc)[2 * GPL],
-                                                uint4 (&vc)[2 * GPL]) {
+                                                uint4 (&vc)[2 * GPL], bool fresh = false) {
   constexpr int G = 32 * GPL;
   const int lane = threadIdx.x & 31;
   const int64_t base = (int64_t)bh * a.T_cap * G + (int64_t)(t0 / 32) * 32 * G + lane * 16;
 #pragma unroll
   for (int q = 0; q < 2 * GPL; ++q) {
-    kc[q] = ldg_stream(a.kc + base + q * 512);
-    vc[q] = ldg_stream(a.vc + base + q * 512);
+    if (fresh) {
+      kc[q] = __ldcg(reinterpret_cast<const uint4*>(a.kc + base + q * 512));
+      vc[q] = __ldcg(reinterpret_cast<const uint4*>(a.vc + base + q * 512));
+    } else {
+      kc[q] = ldg_stream(a.kc + base + q * 512);
+      vc[q] = ldg_stream(a.vc + base + q * 512);
+    }
   }
 }
 
@@ -150,7 +178,7 @@ template <int V, int GPL, bool PRMT>
 __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int bh, int tok0, int tok1, uint32_t lut_base,
                                                  uint32_t vbook_base, float& m_w, float& l_lane,
                                                  float (&acc)[GPL][V], uint4 (&ka)[2 * GPL],
-                                                 uint4 (&va)[2 * GPL]) {
+                                                 uint4 (&va)[2 * GPL], int fresh_t0) {
   using SM = AttnSmem<V, GPL>;
   constexpr int G = SM::G, EPB = SM::EPB;
   constexpr int Q = 2 * GPL;  // 16-byte loads per lane per 32-token batch
@@ -266,12 +294,14 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
   auto load_k = [&](uint4 (&kc)[Q], int t0) {
     const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) kc[q] = ldg_stream(kbase + off + q * 512);
+    for (int q = 0; q < Q; ++q)
+      kc[q] = t0 == fresh_t0 ? __ldcg(reinterpret_cast<const uint4*>(kbase + off + q * 512)) : ldg_stream(kbase + off + q * 512);
   };
   auto load_v = [&](uint4 (&vc)[Q], int t0) {
     const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) vc[q] = ldg_stream(vbase + off + q * 512);
+    for (int q = 0; q < Q; ++q)
+      vc[q] = t0 == fresh_t0 ? __ldcg(reinterpret_cast<const uint4*>(vbase + off + q * 512)) : ldg_stream(vbase + off + q * 512);
   };
   // warp w takes 32-token batches w, w+kAttnWarps, ... of the span. One register set
   // per stream: the next batch's K codes load during this batch's V phase and its V
@@ -289,6 +319,78 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     vphase(va, ph);
     if (tn < tok1) load_v(va, tn);
   }
+}
+
+// Nearest of the 256 fp16 pairs book[e] (e at byte offset e * stride) to p = (p0, p1),
+// found by a team of TS consecutive lanes (lane `split` of the team scans entries
+// split, split + TS, ...): fp32 screen keeping the best and second-best distance, then
+// float64 rescoring of the entries inside the fp32 error band — the reference quantize's
+// float64 argmin with the lowest index on ties (V/codec.py:239-253), the arithmetic of
+// qkv_rope_append_cq_kernel (csrc/decode.cu). Returns the code on every lane of the team.
+template <int TS>
+__device__ __forceinline__ int cq_nearest_team(const uint8_t* book, int stride, float p0, float p1, int split) {
+  const float m0 = -2.f * p0, m1 = -2.f * p1;
+  float d1 = FLT_MAX, d2 = FLT_MAX, cmax2 = 0.f;
+  int e1 = 0x7fffffff;
+#pragma unroll 4
+  for (int e = split; e < 256; e += TS) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(book + e * stride);
+    const float c0 = __half2float(__ushort_as_half((unsigned short)(w & 0xffff)));
+    const float c1 = __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+    const float cn = c0 * c0 + c1 * c1;
+    cmax2 = fmaxf(cmax2, cn);
+    const float d = fmaf(m0, c0, fmaf(m1, c1, cn));
+    if (d < d1) {
+      d2 = d1;
+      d1 = d;
+      e1 = e;
+    } else if (d < d2) {
+      d2 = d;
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < TS; o <<= 1) {
+    const float od1 = __shfl_xor_sync(0xffffffffu, d1, o), od2 = __shfl_xor_sync(0xffffffffu, d2, o);
+    const int oe1 = __shfl_xor_sync(0xffffffffu, e1, o);
+    cmax2 = fmaxf(cmax2, __shfl_xor_sync(0xffffffffu, cmax2, o));
+    d2 = fminf(fmaxf(d1, od1), fminf(d2, od2));
+    if (od1 < d1 || (od1 == d1 && oe1 < e1)) {
+      d1 = od1;
+      e1 = oe1;
+    }
+  }
+  const float tol = 2e-5f * (cmax2 + p0 * p0 + p1 * p1) + 1e-30f;
+  const bool need64 = d2 - d1 <= tol;  // uniform over a team, not over the warp:
+  if (!__any_sync(0xffffffffu, need64)) return e1;  // every lane takes the shuffles below
+  const double r0 = p0, r1 = p1;
+  const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
+  double best = DBL_MAX;
+  int be = 0x7fffffff;
+  for (int e = split; e < 256; e += TS) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(book + e * stride);
+    const float c0 = __half2float(__ushort_as_half((unsigned short)(w & 0xffff)));
+    const float c1 = __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+    if (need64 && fmaf(m0, c0, fmaf(m1, c1, c0 * c0 + c1 * c1)) <= d1 + tol) {
+      const double a0 = c0, a1 = c1;
+      const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
+      const double cnd = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
+      const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cnd), pn);
+      if (d < best) {  // entries ascend within a lane: the first minimum is the lowest index
+        best = d;
+        be = e;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < TS; o <<= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+    if (ob < best || (ob == best && oe < be)) {
+      best = ob;
+      be = oe;
+    }
+  }
+  return need64 ? be : e1;
 }
 
 template <int V, int GPL>
@@ -365,8 +467,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     const bool switch_h = (h != cur_h);
     const int g = tid % G;  // constant per thread since kAttnThreads % G == 0
     float qv[V];
+    if (a.qkv) {
+      // fused front end: q roped here (fp16-rounded like the separate rope kernel)
+      const __half* qr = a.qkv + (int64_t)b * 3 * a.H * C + (int64_t)h * C;
 #pragma unroll
-    for (int j = 0; j < V; ++j) qv[j] = load_as_f32(a.q, a.q_dtype, (int64_t)bh * C + g * V + j) * a.scale_log2;
+      for (int j = 0; j < V; ++j)
+        qv[j] = __half2float(__float2half_rn(rope_channel_attn(qr, g * V + j, C, a.log2_theta, T - 1))) * a.scale_log2;
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) qv[j] = load_as_f32(a.q, a.q_dtype, (int64_t)bh * C + g * V + j) * a.scale_log2;
+    }
+    const int pos = T - 1;  // the new token of a fused decode step
+    const bool append_here = a.qkv != nullptr && tok0 <= pos && pos < tok1;
     if (bulk_books) {
       // ---- books by bulk copy: the head's K book lands in the LUT region and its V
       // book in the V-book region, both already [e][g]; the LUT is then computed in
@@ -379,6 +491,29 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       cur_h = h;
       mbar_wait(book_bar, book_phase);
       book_phase ^= 1;
+      if constexpr (V == 2 && GPL == 2 && kAttnThreads == 512) if (append_here) {
+        // the new K row (roped) and V row of (b, h): nearest centroids against the books in
+        // shared memory ([e][g] fp16 pairs), teams of 4 lanes per group, K on threads
+        // 0..255 and V on 256..511; codes written into the caches (KV_IL, token pos)
+        const bool is_k = tid < 256;
+        const int gg = (tid & 255) >> 2, split = tid & 3;
+        const __half* row = a.qkv + (int64_t)b * 3 * a.H * C + (int64_t)((is_k ? a.H : 2 * a.H) + h) * C;
+        float p[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = gg * 2 + j;
+          p[j] = is_k ? __half2float(__float2half_rn(rope_channel_attn(row, c, C, a.log2_theta, pos)))
+                      : __half2float(row[c]);
+        }
+        const uint8_t* bk = is_k ? reinterpret_cast<const uint8_t*>(lut_s) : vbook_s;
+        const int code = cq_nearest_team<4>(bk + gg * 4, G * 4, p[0], p[1], split);
+        if (split == 0) {
+          const int l = gg & 31, jj = gg >> 5, slot = (pos & 31) ^ l, byte = slot * GPL + jj;
+          const int64_t off = (int64_t)bh * a.T_cap * G + (int64_t)(pos >> 5) * 32 * G + ((byte >> 4) * 32 + l) * 16 + (byte & 15);
+          (is_k ? a.kc_w : a.vc_w)[off] = (uint8_t)code;
+        }
+        __syncthreads();  // the codes are in global memory before any warp loads that batch
+      }
       uint32_t* lw = reinterpret_cast<uint32_t*>(lut_s);
       for (int idx = tid; idx < 256 * G; idx += kAttnThreads) {  // idx % G == g for every idx of a thread
         const uint32_t w = lw[idx];
@@ -449,9 +584,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
     uint4 ka[2 * GPL], va[2 * GPL];
-    if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va);
-    if (aligned) attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
-    else attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va);
+    const int fresh_t0 = append_here ? (pos & ~31) : -1;  // the batch holding the appended token
+    if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va, tok0 + warp * 32 == fresh_t0);
+    if (aligned)
+      attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va, fresh_t0);
+    else
+      attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va, fresh_t0);
 
     ph.mark(a, 1);
     // ---- merge the warps of this span
@@ -673,14 +811,14 @@ static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit, int flags
   cfg.attrs = attr;
   cfg.numAttrs = persistent_attrs(attr, flags);
   VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
-  set_kernel("attn_cq");
+  set_kernel(a.qkv ? "attn_cq_append" : "attn_cq");
   set_launch(grid, kAttnThreads, 256, 0);
   return VQB_OK;
 }
 
 int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_dtype, int B, int H, int T, int C,
                   const int* d_len, void* out, int out_dtype, const VqbLaunch* L, void* ws, size_t ws_bytes,
-                  cudaStream_t st, bool* used_fast) {
+                  cudaStream_t st, bool* used_fast, const __half* qkv = nullptr, float log2_theta = 0.f) {
   Geom gk, gv;
   int s = make_geom(k, &gk);
   if (s) return s;
@@ -703,6 +841,10 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
   if (used_fast) *used_fast = fast;
   if (!fast && d_len)
     return set_error(VQB_ECONFIG, "a device-resident KV length needs the fast attention configuration");
+  if (qkv && (!fast || !d_len || !k->d_codebooks_t || !v->d_codebooks_t || gk.v != 2 || gk.gpr != 64 ||
+              k->layout != VQB_LAYOUT_KV_IL || v->layout != VQB_LAYOUT_KV_IL || k->codebook_dtype != VQB_F16))
+    return set_error(VQB_ECONFIG, "the fused rope + KV append attention needs the CQ-4 fast configuration (v = 2, "
+                                  "C = 128, KV_IL caches with per-head books) and a device length");
   if (fast) {
     AttnArgs a;
     a.kc = reinterpret_cast<const uint8_t*>(k->d_codes);
@@ -726,6 +868,10 @@ int attn_dispatch(const VqbTensor* k, const VqbTensor* v, const void* q, int q_d
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(ws) + 8192)
                                      : nullptr;
     a.scale_log2 = 1.4426950408889634f / sqrtf((float)C);
+    a.qkv = qkv;
+    a.log2_theta = log2_theta;
+    a.kc_w = const_cast<uint8_t*>(reinterpret_cast<const uint8_t*>(k->d_codes));
+    a.vc_w = const_cast<uint8_t*>(reinterpret_cast<const uint8_t*>(v->d_codes));
     int gl = L ? L->grid_limit : 0;
     // the planner's split of T (VqbLaunch split over T): each (b, h) span is shared
     // by ~split_factor CTAs of the persistent schedule
@@ -783,4 +929,15 @@ extern "C" int vqb_attn_decode_len(const VqbTensor* k, const VqbTensor* v, const
                                    void* stream) {
   return vqb::attn_dispatch(k, v, d_q, q_dtype, B, H, T, C, d_len, d_out, out_dtype, launch, d_ws, ws_bytes,
                             reinterpret_cast<cudaStream_t>(stream), nullptr);
+}
+
+extern "C" int vqb_attn_decode_append(const VqbTensor* k_cache, const VqbTensor* v_cache, const void* d_qkv, int32_t B,
+                                      int32_t H, int32_t C, const int32_t* d_len, float theta, void* d_out,
+                                      int32_t out_dtype, const VqbLaunch* launch, void* d_ws, size_t ws_bytes,
+                                      void* stream) {
+  if (!d_qkv || !d_len || theta <= 0.f) return vqb::set_error(VQB_ECONFIG, "fused append attention needs qkv, d_len and theta");
+  const int T = k_cache ? (int)k_cache->dims[2] : 1;
+  return vqb::attn_dispatch(k_cache, v_cache, nullptr, VQB_F16, B, H, T, C, d_len, d_out, out_dtype, launch, d_ws,
+                            ws_bytes, reinterpret_cast<cudaStream_t>(stream), nullptr,
+                            reinterpret_cast<const __half*>(d_qkv), log2f(theta));
 }

@@ -242,6 +242,27 @@ def qkv_rope_append(qkv: torch.Tensor, k_cache: DeviceVQTensor, v_cache: DeviceV
     return q_out
 
 
+def vq_attention_append(k_cache: DeviceVQTensor, v_cache: DeviceVQTensor, qkv: torch.Tensor, d_len: torch.Tensor,
+                        theta: float = 10000.0, out_dtype=torch.float16, launch=None) -> torch.Tensor:
+    """One launch for ``qkv_rope_append`` + ``vq_attention(..., d_len=d_len)``: the
+    attention kernel ropes q, and the CTA covering the new token of each (b, h) ropes k,
+    quantizes the new K / V rows against the books it already holds and writes the codes
+    before attending (CQ-4 caches). Same results as the two-kernel form."""
+    b, h, t, c = k_cache.shape
+    if qkv.shape != (b, 3 * h * c) or qkv.dtype != torch.float16 or not qkv.is_contiguous():
+        raise ShapeError(f"fused qkv {tuple(qkv.shape)} {qkv.dtype} does not match (B, 3*H*C) = {(b, 3 * h * c)} fp16")
+    od = torch_dtype(out_dtype or torch.float16)
+    out = torch.empty((b, h, c), dtype=od, device=k_cache.device)
+    L = launch if launch is not None else N.VqbLaunch()
+    lib = N.lib()
+    ks, vs = k_cache.struct(), v_cache.struct()
+    need = N.check(lib.vqb_workspace_bytes(N.KERNEL_ATTN, ks, b * h, L))
+    ws = workspace(need, k_cache.device)
+    N.check(lib.vqb_attn_decode_append(ks, vs, qkv.data_ptr(), b, h, c, d_len.data_ptr(), float(theta), out.data_ptr(),
+                                       dtype_enum(od), L, ws.data_ptr(), ws.numel(), _stream(k_cache.device)))
+    return out
+
+
 def silu_mul(gate_up: torch.Tensor, out=None) -> torch.Tensor:
     rows, f2 = gate_up.shape
     out = torch.empty((rows, f2 // 2), dtype=gate_up.dtype, device=gate_up.device) if out is None else out

@@ -398,3 +398,31 @@ def test_fused_decode_step_bit_identical(dev):
         a.replay()
         b.replay()
         assert torch.equal(a.logits, b.logits)
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_fused_append_attention_bit_identical(batch, dev):
+    """vqb_attn_decode_append (RoPE + KV append inside the attention kernel) gives the
+    two-kernel step's logits and KV-cache codes bit for bit, eagerly and replayed."""
+    from paper_2503_02236_b200.decode import LlamaShape, VQLlamaDecoder
+    sh = LlamaShape(hidden=512, heads=4, head_dim=128, ffn=1024, layers=2, vocab=256)
+    a = VQLlamaDecoder.synthetic(sh, batch, 96, dev, seed=12)
+    b = VQLlamaDecoder.synthetic(sh, batch, 96, dev, seed=12)
+    b.fuse_append = False
+    for d in (a, b):
+        d.tokens.copy_(torch.arange(5, 5 + batch, device=dev))
+        d.set_length(29)  # the new tokens cross a 32-token batch boundary
+    from paper_2503_02236_b200 import _native as N
+    for _ in range(4):
+        a.run_step()
+        assert N.last_kernel() != "qkv_rope_append"
+        b.run_step()
+        assert torch.equal(a.logits, b.logits)
+    for La, Lb in zip(a.layers, b.layers):
+        assert torch.equal(La.k_cache.codes, Lb.k_cache.codes) and torch.equal(La.v_cache.codes, Lb.v_cache.codes)
+    a.capture()
+    b.capture()
+    for _ in range(3):
+        a.replay()
+        b.replay()
+        assert torch.equal(a.logits, b.logits)
