@@ -174,7 +174,7 @@ __device__ __forceinline__ void attn_load_batch(const AttnArgs& a, int bh, int t
   }
 }
 
-template <int V, int GPL, bool PRMT>
+template <int V, int GPL, bool PRMT, bool APPEND>
 __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int bh, int tok0, int tok1, uint32_t lut_base,
                                                  uint32_t vbook_base, float& m_w, float& l_lane,
                                                  float (&acc)[GPL][V], uint4 (&ka)[2 * GPL],
@@ -295,13 +295,15 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
 #pragma unroll
     for (int q = 0; q < Q; ++q)
-      kc[q] = t0 == fresh_t0 ? __ldcg(reinterpret_cast<const uint4*>(kbase + off + q * 512)) : ldg_stream(kbase + off + q * 512);
+      kc[q] = (APPEND && t0 == fresh_t0) ? __ldcg(reinterpret_cast<const uint4*>(kbase + off + q * 512))
+                                         : ldg_stream(kbase + off + q * 512);
   };
   auto load_v = [&](uint4 (&vc)[Q], int t0) {
     const int64_t off = (int64_t)(t0 / 32) * 32 * G + lane * 16;
 #pragma unroll
     for (int q = 0; q < Q; ++q)
-      vc[q] = t0 == fresh_t0 ? __ldcg(reinterpret_cast<const uint4*>(vbase + off + q * 512)) : ldg_stream(vbase + off + q * 512);
+      vc[q] = (APPEND && t0 == fresh_t0) ? __ldcg(reinterpret_cast<const uint4*>(vbase + off + q * 512))
+                                         : ldg_stream(vbase + off + q * 512);
   };
   // warp w takes 32-token batches w, w+kAttnWarps, ... of the span. One register set
   // per stream: the next batch's K codes load during this batch's V phase and its V
@@ -393,7 +395,7 @@ __device__ __forceinline__ int cq_nearest_team(const uint8_t* book, int stride, 
   return need64 ? be : e1;
 }
 
-template <int V, int GPL>
+template <int V, int GPL, bool APPEND = false>
 __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   using SM = AttnSmem<V, GPL>;
   constexpr int G = SM::G, C = SM::C, EPB = SM::EPB;
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     const bool switch_h = (h != cur_h);
     const int g = tid % G;  // constant per thread since kAttnThreads % G == 0
     float qv[V];
-    if (a.qkv) {
+    if (APPEND) {
       // fused front end: q roped here (fp16-rounded like the separate rope kernel)
       const __half* qr = a.qkv + (int64_t)b * 3 * a.H * C + (int64_t)h * C;
 #pragma unroll
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       for (int j = 0; j < V; ++j) qv[j] = load_as_f32(a.q, a.q_dtype, (int64_t)bh * C + g * V + j) * a.scale_log2;
     }
     const int pos = T - 1;  // the new token of a fused decode step
-    const bool append_here = a.qkv != nullptr && tok0 <= pos && pos < tok1;
+    const bool append_here = APPEND && tok0 <= pos && pos < tok1;
     if (bulk_books) {
       // ---- books by bulk copy: the head's K book lands in the LUT region and its V
       // book in the V-book region, both already [e][g]; the LUT is then computed in
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       cur_h = h;
       mbar_wait(book_bar, book_phase);
       book_phase ^= 1;
-      if constexpr (V == 2 && GPL == 2 && kAttnThreads == 512) if (append_here) {
+      if constexpr (APPEND && V == 2 && GPL == 2 && kAttnThreads == 512) if (append_here) {
         // the new K row (roped) and V row of (b, h): nearest centroids against the books in
         // shared memory ([e][g] fp16 pairs), teams of 4 lanes per group, K on threads
         // 0..255 and V on 256..511; codes written into the caches (KV_IL, token pos)
@@ -585,11 +587,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
     uint4 ka[2 * GPL], va[2 * GPL];
     const int fresh_t0 = append_here ? (pos & ~31) : -1;  // the batch holding the appended token
-    if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va, tok0 + warp * 32 == fresh_t0);
+    if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va, APPEND && tok0 + warp * 32 == fresh_t0);
     if (aligned)
-      attn_stream_span<V, GPL, true>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va, fresh_t0);
+      attn_stream_span<V, GPL, true, APPEND>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va,
+                                              fresh_t0);
     else
-      attn_stream_span<V, GPL, false>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va, fresh_t0);
+      attn_stream_span<V, GPL, false, APPEND>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va,
+                                               fresh_t0);
 
     ph.mark(a, 1);
     // ---- merge the warps of this span
@@ -790,14 +794,15 @@ int64_t attn_ws_bytes(const VqbTensor* k, int64_t BH, const VqbLaunch* L) {
 
 template <int V, int GPL>
 static int launch_attn_t(AttnArgs& a, cudaStream_t st, int grid_limit, int flags) {
-  auto kern = attn_cq_kernel<V, GPL>;
+  auto kern = a.qkv ? attn_cq_kernel<V, GPL, true> : attn_cq_kernel<V, GPL, false>;
   constexpr size_t smem = AttnSmem<V, GPL>::total;
-  static bool configured[64] = {false};
+  static bool configured[2][64] = {};  // per kernel (plain / fused append) and device
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!configured[dev & 63]) {
+  const int which = a.qkv ? 1 : 0;
+  if (!configured[which][dev & 63]) {
     VQB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[dev & 63] = true;
+    configured[which][dev & 63] = true;
   }
   const int U = a.B * a.H * (a.len_ptr ? a.NT_cap : a.NT);  // a device length is bounded by the capacity
   int grid = balanced_grid(U, sm_count());
