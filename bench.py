@@ -364,14 +364,18 @@ def time_decode(torch, dev, batch=1, ctx=4096, reps=10, tp=False, fused=False):
         torch.cuda.empty_cache()
     world = dec.world
     dec.set_length(ctx - 1 - reps - 3)
-    dec.capture()
+    # (the gloo dry run of the multi-GPU path cannot capture its collectives: eager steps)
+    eager = tp and os.environ.get("VQB_BENCH_SHARED_GPU") == "1"
+    step = dec.run_step if eager else dec.replay
+    if not eager:
+        dec.capture()
     for _ in range(3):
-        dec.replay()
+        step()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
     for _ in range(reps):
-        dec.replay()
+        step()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
@@ -629,8 +633,13 @@ def run_impl(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # VQB_BENCH_SHARED_GPU=1 (dry run of the multi-GPU code path on a one-GPU box): every
+    # rank on cuda:0, collectives over gloo (NCCL refuses two ranks on one device)
+    shared = os.environ.get("VQB_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if shared else "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import __graft_entry__
