@@ -568,7 +568,10 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
         // software pipeline: the ldmatrix gathers of column-pair group g+1 are issued
         // before the MMAs of group g, so each MMA finds its A fragment landed instead of
         // waiting one shared-memory round trip per column pair
-        constexpr int QG = (R == 1 ? 4 : 2) < QW ? (R == 1 ? 4 : 2) : QW;  // column pairs per group
+        // column pairs per group (the grouped kernel's problem cursors leave no registers
+        // for a deeper pipeline: one pair at a time there)
+        constexpr int QG0 = GROUP ? 1 : (R == 1 ? 4 : 2);
+        constexpr int QG = QG0 < QW ? QG0 : QW;
         constexpr int NG = QW / QG;
         uint32_t af[2][QG][R][4];
         auto gather = [&](int g, uint32_t (&dst)[QG][R][4]) {
