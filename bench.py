@@ -720,6 +720,31 @@ def run_impl(args):
     torch.cuda.synchronize()
     ms_single = e0.elapsed_time(e1) / args.steps
     diff = float((single.y.float() - stack.y.float()).abs().max()) if world == 1 else None
+    # the headline step with fp32 accumulation of every product (VQB_FLAG_EXACT_ACCUM)
+    # instead of the 8-row fp16x2 windows, for comparison with the window numerics
+    exact = None
+    if world == 1 and not args.no_extra:
+        from paper_2503_02236_b200.ops import launch_struct
+        Lx = launch_struct()
+        Lx.flags |= 8
+        ex = VQLinearStack(stack.weights, rows=1, launches=[Lx] * len(stack.weights), grouped=True)
+        ex.x.copy_(stack.x)
+        ex.capture()
+        for _ in range(3):
+            ex.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            ex.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_ex = e0.elapsed_time(e1) / args.steps
+        exact = {"what": "the headline step (one grouped launch) with VQB_FLAG_EXACT_ACCUM: fp32 accumulation "
+                         "of every product instead of 8-row fp16x2 windows",
+                 "ms_per_step": ms_ex, "GB_s": step_bytes / (ms_ex * 1e-3) / 1e9,
+                 "max_abs_diff_vs_windows": float((ex.y.float() - stack.y.float()).abs().max()),
+                 "max_abs_output": float(stack.y.float().abs().max())}
+        del ex
     # e2e through the public API with pinned host buffers
     hx = torch.empty(stack.x.shape, dtype=stack.x.dtype, pin_memory=True)
     hx.copy_(stack.x)
@@ -764,6 +789,8 @@ def run_impl(args):
             "ms_per_step": ms_single, "GB_s": total_bytes / (ms_single * 1e-3) / 1e9,
             "frac": total_bytes / (ms_single * 1e-3) / 1e9 / world / hbm, "launches_per_step": single.n_launches,
             "max_abs_diff_vs_grouped": diff}
+        if exact:
+            extra["exact_accum_step"] = exact
         want = (lambda k: True) if not args.only else (lambda k: k in args.only.split(","))
         if not args.no_extra and world == 1:
             from paper_2503_02236_b200.codec import Sharing, VQConfig
