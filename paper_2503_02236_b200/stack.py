@@ -106,3 +106,46 @@ class VQLinearStack:
         self.x.copy_(host_x, non_blocking=True)
         self.replay()
         host_y.copy_(self.y, non_blocking=True)
+
+
+class StackPipeline:
+    """Serving-loop form of ``VQLinearStack.run``: two device buffer sets (each with its
+    own captured graph, sharing the weights) and separate host->device and
+    device->host copy streams, so step k's input copy and step k-1's result copy overlap
+    the neighbouring steps' compute. Every step still moves its inputs host->device and
+    its result device->host; only the waiting is hidden (PCIe is full duplex)."""
+
+    def __init__(self, stack: VQLinearStack):
+        twin = VQLinearStack(stack.weights, rows=stack.rows, act_dtype=stack.act_dtype, out_dtype=stack.out_dtype,
+                             launches=stack.launches, grouped=stack.grouped)
+        self.sets = [stack, twin]
+        for s in self.sets:
+            if s._graph is None:
+                s.capture()
+        dev = stack.device
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.in_ready = [torch.cuda.Event() for _ in range(2)]
+        self.out_ready = [torch.cuda.Event() for _ in range(2)]
+        self.set_free = [torch.cuda.Event() for _ in range(2)]
+
+    def run(self, host_xs, host_ys) -> None:
+        """One step per (pinned host input, pinned host output) pair, in order."""
+        comp = torch.cuda.current_stream(self.sets[0].device)
+        for k, (hx, hy) in enumerate(zip(host_xs, host_ys)):
+            i = k % 2
+            st = self.sets[i]
+            with torch.cuda.stream(self.h2d):
+                if k >= 2:
+                    self.h2d.wait_event(self.set_free[i])  # this set's previous result is read out
+                st.x.copy_(hx, non_blocking=True)
+                self.in_ready[i].record(self.h2d)
+            comp.wait_event(self.in_ready[i])
+            st.replay()
+            self.out_ready[i].record(comp)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.out_ready[i])
+                hy.copy_(st.y, non_blocking=True)
+                self.set_free[i].record(self.d2h)
+        comp.wait_stream(self.d2h)
+        comp.wait_stream(self.h2d)

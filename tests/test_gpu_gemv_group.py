@@ -110,3 +110,24 @@ def test_grouped_rejects_mixed_configs(dev):
     st = VQLinearStack([a, b], rows=1, grouped=True)
     with pytest.raises(ConfigError, match="grouped GEMV"):
         st.launch_all()
+
+
+def test_stack_pipeline_matches_serial_runs(dev):
+    """StackPipeline (double-buffered sets, H2D / D2H on their own streams) returns, per
+    step, exactly what the serial VQLinearStack.run returns for that step's input."""
+    from paper_2503_02236_b200.stack import StackPipeline, VQLinearStack
+    shapes = [(1024, 3072), (1024, 1024), (2752, 1024)]
+    ws, _ = zip(*[_weight(m, n, 60 + i, dev) for i, (m, n) in enumerate(shapes)])
+    st = VQLinearStack(ws, rows=1, grouped=True)
+    ref = VQLinearStack(ws, rows=1, grouped=True)
+    steps = 5
+    g = torch.Generator().manual_seed(3)
+    hxs = [torch.randn(st.x.shape, generator=g).half().pin_memory() for _ in range(steps)]
+    hys = [torch.empty(st.y.shape, dtype=st.y.dtype).pin_memory() for _ in range(steps)]
+    StackPipeline(st).run(hxs, hys)
+    torch.cuda.synchronize()
+    for hx, hy in zip(hxs, hys):
+        out = torch.empty_like(hy).pin_memory()
+        ref.run(hx, out)
+        torch.cuda.synchronize()
+        assert torch.equal(hy, out)
