@@ -690,11 +690,13 @@ constexpr int kGtThreads = (2 + kGtProd + kGtEpi) * 32;
 // consecutive stages concurrently (one group's latency chain — code LDS, gathers, STS,
 // proxy fence, barrier — no longer serialises the stages); the A / X ring has one slot
 // per group
-__host__ __device__ constexpr int gt_stages(int R) { return R == 1 ? 4 : 2; }
-__host__ __device__ constexpr int gt_code_stages(int BN) { return BN <= 32 ? 8 : 4; }  // code-word ring (HBM latency)
-__host__ __device__ constexpr int gt_x_stages(int BN) { return BN <= 32 ? 8 : 6; }     // X ring (its own depth)
-constexpr int kGtK = 64;                          // K rows per stage (one SW128 span)
-constexpr int kGtABytes = 256 * kGtK * 2;         // W^T tile: 256 output columns x 64 K (two 16 KB halves)
+// K rows per stage: 128 for one level (fewer, fatter stages: the per-stage hand-off
+// chain, not any one resource, bounds this kernel), 64 for two (shared-memory budget)
+__host__ __device__ constexpr int gt_k(int R) { return R == 1 ? 128 : 64; }
+__host__ __device__ constexpr int gt_stages(int R) { return 2; }
+__host__ __device__ constexpr int gt_code_stages(int BN) { return 4; }                     // code-word ring
+__host__ __device__ constexpr int gt_x_stages(int R, int BN) { return R == 1 && BN > 32 ? 2 : 4; }  // X ring
+__host__ __device__ constexpr int gt_a_bytes(int R) { return 256 * gt_k(R) * 2; }       // W^T tile, two halves
 
 struct GemvTcArgs {
   const uint8_t* codes;  // GEMV_IL, N % 256 == 0
@@ -707,11 +709,11 @@ struct GemvTcArgs {
   float* part;                    // (splits, B, N) fp32 partials when splits > 1
 };
 
-__host__ __device__ constexpr int gt_code_bytes(int cbytes, int R) { return R * (kGtK / (16 / cbytes)) * 512; }
+__host__ __device__ constexpr int gt_code_bytes(int cbytes, int R) { return R * (gt_k(R) / (16 / cbytes)) * 512; }
 __host__ __device__ constexpr size_t gt_smem(int cbytes, int R, int BN) {
-  return 1024 + (size_t)R * kBookBytes + (size_t)gt_stages(R) * kGtABytes + (size_t)gt_x_stages(BN) * BN * 128 +
-         (size_t)gt_code_stages(BN) * gt_code_bytes(cbytes, R) +
-         (2 * gt_stages(R) + 2 * gt_x_stages(BN) + 2 * gt_code_stages(BN) + 4) * 8 + 16;
+  return 1024 + (size_t)R * kBookBytes + (size_t)gt_stages(R) * gt_a_bytes(R) +
+         (size_t)gt_x_stages(R, BN) * BN * 2 * gt_k(R) + (size_t)gt_code_stages(BN) * gt_code_bytes(cbytes, R) +
+         (2 * gt_stages(R) + 2 * gt_x_stages(R, BN) + 2 * gt_code_stages(BN) + 4) * 8 + 16;
 }
 
 template <int CBYTES, int R, int BN>
@@ -719,13 +721,15 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, GemvTcArgs a) {
   constexpr int RPL = 16 / CBYTES;
   constexpr int CODEB = gt_code_bytes(CBYTES, R) / R;  // one level's code bytes per stage
-  constexpr int XB = BN * 128;                          // X tile bytes (BN rows x 64 K, SW128)
+  constexpr int GK = gt_k(R);
+  constexpr int ABYTES = gt_a_bytes(R);
+  constexpr int XB = BN * 2 * GK;                       // X tile bytes (GK / 64 SW128 boxes of BN rows)
   constexpr int STG = gt_stages(R);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  constexpr int CST = gt_code_stages(BN), XST = gt_x_stages(BN);
+  constexpr int CST = gt_code_stages(BN), XST = gt_x_stages(R, BN);
   uint8_t* sa = smem;                                   // STG x 32 KB (A: W^T tiles)
-  uint8_t* sx = sa + STG * kGtABytes;                   // XST x XB (B: X tiles)
+  uint8_t* sx = sa + STG * ABYTES;                   // XST x XB (B: X tiles)
   uint8_t* sc = sx + XST * XB;                          // CST x R x CODEB (code words)
   uint8_t* book = sc + CST * R * CODEB;                 // R x 256 entries x 128 B (replicated)
   uint64_t* bars = reinterpret_cast<uint64_t*>(book + R * kBookBytes);
@@ -790,7 +794,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         const int c = i % CST, ch = c_lo + i;
         if (i >= CST) mbar_wait(cempty0 + 8 * c, ((i / CST) & 1) ^ 1);
         mbar_arrive_expect_tx(cfull0 + 8 * c, (uint32_t)(R * CODEB));
-        const int64_t off = (int64_t)cb * 32 * (a.M / RPL) * 16 + (int64_t)ch * (kGtK / RPL) * 512;
+        const int64_t off = (int64_t)cb * 32 * (a.M / RPL) * 16 + (int64_t)ch * (GK / RPL) * 512;
 #pragma unroll
         for (int r = 0; r < R; ++r)
           tma_load_1d(smem_u32(sc + (c * R + r) * CODEB), a.codes + r * a.level_bytes + off, CODEB, cfull0 + 8 * c);
@@ -801,7 +805,9 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         const int x = i % XST;
         if (i >= XST) mbar_wait(xempty0 + 8 * x, ((i / XST) & 1) ^ 1);
         mbar_arrive_expect_tx(full0 + 8 * x, (uint32_t)XB);
-        tma_load_2d(smem_u32(sx + x * XB), &tmap_x, (c_lo + i) * kGtK, 0, full0 + 8 * x);
+#pragma unroll
+        for (int bx = 0; bx < GK / 64; ++bx)
+          tma_load_2d(smem_u32(sx + x * XB + bx * BN * 128), &tmap_x, (c_lo + i) * GK + bx * 64, 0, full0 + 8 * x);
       }
     }
   } else if (warp == 1) {
@@ -814,13 +820,14 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         mbar_wait(full0 + 8 * x, (i / XST) & 1);
         mbar_wait(afull0 + 8 * s, (i / STG) & 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sa + s * kGtABytes), x_base = smem_u32(sx + x * XB);
+        const uint32_t a_base = smem_u32(sa + s * ABYTES), x_base = smem_u32(sx + x * XB);
 #pragma unroll
-        for (int k = 0; k < kGtK / 16; ++k) {
-          const uint64_t bdesc = umma_desc(x_base + k * 32, 16, 1024);
+        for (int k = 0; k < GK / 16; ++k) {
+          // X: K-step k lies in SW128 box k / 4 (BN rows x 128 B), 32 B per K-step inside it
+          const uint64_t bdesc = umma_desc(x_base + (k >> 2) * BN * 128 + (k & 3) * 32, 16, 1024);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const uint64_t adesc = umma_desc(a_base + h * (kGtABytes / 2) + k * 4096, 1024, 2048);
+            const uint64_t adesc = umma_desc(a_base + h * (ABYTES / 2) + k * 4096, 1024, 2048);
             umma_f16(tmem_base + h * BN, adesc, bdesc, idesc, (i | k) != 0);
           }
         }
@@ -835,7 +842,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
     const int pw = warp - 2, grp = pw / GW;
     const int gtid = (pw % GW) * 32 + lane;
     constexpr int NPT = GW * 32;
-    constexpr int WORDS = (kGtK / RPL) * 32;        // code words per level per stage
+    constexpr int WORDS = (GK / RPL) * 32;          // code words per level per stage
     constexpr int TPW = NPT >= WORDS ? NPT / WORDS : 1;  // threads per word
     constexpr int WPT = NPT >= WORDS ? 1 : WORDS / NPT;  // words per thread
     constexpr int KR = RPL / TPW;                   // rows per thread per word
@@ -859,7 +866,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         const int w = idx % WORDS, part = (idx / WORDS) % TPW;
         const int gi = w % 32, rg = w / 32;
         const int h = gi >> 4, g16 = gi & 15, nb = g16 >> 3, c = g16 & 7;
-        uint8_t* at = sa + s * kGtABytes + h * (kGtABytes / 2);
+        uint8_t* at = sa + s * ABYTES + h * (ABYTES / 2);
 #pragma unroll
         for (int kk = 0; kk < KR; ++kk) {
           const int k = part * KR + kk;  // row within the word
@@ -1407,7 +1414,7 @@ static bool gemv_tc_covers(const Geom& g, const VqbTensor* w, int x_dtype, int r
   if (rows < 2 || rows > 64 || x_dtype != VQB_F16 || w->codebook_dtype != VQB_F16) return false;
   if (w->layout != VQB_LAYOUT_GEMV_IL || g.v != 8 || g.sharing != VQB_SHARE_WHOLE || g.ndim != 2) return false;
   if (!(g.R == 1 || g.R == 2) || !(g.bits == 8 || (g.bits == 16 && g.R == 1))) return false;
-  if (g.cols % 256 != 0 || g.rows % kGtK != 0) return false;
+  if (g.cols % 256 != 0 || g.rows % gt_k(g.R) != 0) return false;
   // every code must be resident in the 256-entry shared table
   if (!(g.K <= 256 || (w->max_code >= 0 && w->max_code < 256))) return false;
   // default: batches from kGemvTcMinRows, and every batch the CUDA-core / mma.sync
@@ -1417,7 +1424,7 @@ static bool gemv_tc_covers(const Geom& g, const VqbTensor* w, int x_dtype, int r
 
 int64_t gemv_tc_ws_bytes(const Geom& g, const VqbTensor* w, int rows, const VqbLaunch* L) {
   if (!gemv_tc_covers(g, w, VQB_F16, rows, L)) return 0;
-  const int sp = gemv_tc_splits((int)(g.cols / 256), (int)(g.rows / kGtK), rows, g.cols);
+  const int sp = gemv_tc_splits((int)(g.cols / 256), (int)(g.rows / gt_k(g.R)), rows, g.cols);
   return VQB_WS_COUNTER_BYTES + (sp > 1 ? (int64_t)sp * rows * g.cols * 4 : 0);
 }
 
@@ -1430,7 +1437,7 @@ int gemv_tc_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   const int BN = rows <= 8 ? 8 : rows <= 16 ? 16 : rows <= 32 ? 32 : 64;
   GemvTcArgs a;
   a.n_cblk = (int)(g.cols / 256);
-  a.n_chunks = (int)(g.rows / kGtK);
+  a.n_chunks = (int)(g.rows / gt_k(g.R));
   a.splits = gemv_tc_splits(a.n_cblk, a.n_chunks, rows, g.cols);
   const int64_t need = VQB_WS_COUNTER_BYTES + (a.splits > 1 ? (int64_t)a.splits * rows * g.cols * 4 : 0);
   if (!ws || (int64_t)ws_bytes < need)
@@ -1440,7 +1447,7 @@ int gemv_tc_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   CUtensorMap mx;
   const cuuint64_t dims[2] = {(cuuint64_t)g.rows, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)g.rows * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kGtK, (cuuint32_t)BN};
+  const cuuint32_t box[2] = {64u, (cuuint32_t)BN};
   const cuuint32_t estr[2] = {1, 1};
   CUresult cr = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
