@@ -281,6 +281,9 @@ int vqb_take_device_error(int32_t* out);
  *  VQB_XF_SILU_MUL: x = [gate | up] (2M halves), y = (silu(gate) * up) @ dequant(W) */
 #define VQB_XF_RMSNORM 1
 #define VQB_XF_SILU_MUL 2
+#define VQB_XF_SWIGLU_OUT 4 /* or-ed into mode: W's 256-column blocks hold [gate 128 | up 128] (the
+                               fused gate_up projection interleaved per 128 columns); the epilogue
+                               writes y = silu(gate) * up, N/2 fp16 columns (the silu_mul arithmetic) */
 int vqb_gemv_xf(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t mode, const void* d_res_in,
                 void* d_res_out, const void* d_weight, float eps, void* d_y, int32_t y_dtype,
                 const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream);

@@ -49,7 +49,7 @@ EXPORTS = (
     "vqb_tp_buffer_bytes", "vqb_ipc_get_handle", "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp",
     "vqb_tp_finish", "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append",
 )
-XF_RMSNORM, XF_SILU_MUL = 1, 2
+XF_RMSNORM, XF_SILU_MUL, XF_SWIGLU_OUT = 1, 2, 4
 
 
 class VqbTensor(ctypes.Structure):

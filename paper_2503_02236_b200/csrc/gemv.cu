@@ -105,6 +105,7 @@ struct GemvFastArgs {
   //    x' = w * rmsnorm(h) (the rmsnorm_kernel arithmetic, decode.cu)
   //  2 SiLU gate: x' = silu(x[:M]) * x[M:2M] for x = [gate | up] (silu_mul_kernel)
   int xf_mode;
+  int swiglu;  // XF kernels: W's 256-column blocks hold [gate 128 | up 128]; y = silu(gate) * up (N/2 columns)
   const __half* xf_add;  // RMSNorm: the input added to the residual (null: none)
   const __half* xf_res_in;
   __half* xf_res_out;
@@ -497,13 +498,30 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
 #pragma unroll
       for (int j = 0; j < 4; ++j) cacc[q][t][j] = 0.f;
 
+  // SwiGLU epilogue staging (XF kernels, batch 1): a block's 256 finished sums
+  float* swg = reinterpret_cast<float*>(xres + (XF ? (size_t)a.M * 2 : 0));
   // one finished output element: y, or (TP push) every rank's slot of this collective
   auto emit = [&](int b, int n, float v) {
-    if (a.tp_world == 0) {
+    if (XF && a.swiglu) {
+      swg[n & 255] = v;  // combined per column block after a barrier (swiglu_flush)
+    } else if (a.tp_world == 0) {
       store_from_f32(cc.y, a.y_dtype, (int64_t)b * cc.N + n, v);
     } else {
       tp_push(a.tp_peer, a.tp_world, tp_slot_offset(a.tp_mode, tp_par, a.tp_world, a.tp_rank, a.tp_slot_elems,
                                                      b, n, cc.N), v);
+    }
+  };
+  // silu(gate) * up of a finished column block, with the arithmetic of the unfused
+  // path (fp16 gate_up output, then silu_mul_kernel): called by every thread after a
+  // barrier that follows the block's emits
+  auto swiglu_flush = [&](int cbk) {
+    if constexpr (XF) {
+      if (tid < 128) {
+        const float g = __half2float(__float2half_rn(swg[tid]));
+        const float u = __half2float(__float2half_rn(swg[tid + 128]));
+        const __half sg = __float2half_rn(g / (1.0f + __expf(-g)));
+        store_from_f32(cc.y, a.y_dtype, (int64_t)cbk * 128 + tid, __half2float(sg) * u);
+      }
     }
   };
   int cur_buf = 0;
@@ -845,6 +863,10 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
         }
         __syncthreads();
       }
+      if (XF && a.swiglu && whole) {
+        swiglu_flush(cb);
+        __syncthreads();
+      }
       if (finisher) {
         // the later spans of this column block are the first spans of the CTAs
         // k in (blockIdx.x, k_end); their tagged partials are polled in parallel,
@@ -883,6 +905,11 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
           }
         }
         if (tid == 0) trace_at(a.trace, 5);
+        if (XF && a.swiglu) {
+          __syncthreads();
+          swiglu_flush(cb);
+          __syncthreads();
+        }
       }
 #pragma unroll
       for (int b = 0; b < (MMA ? 1 : B); ++b)
@@ -986,7 +1013,8 @@ int64_t gemv_tc_ws_bytes(const Geom& g, const VqbTensor* w, int rows, const VqbL
 
 // host-side description of a fused activation transform (vqb_gemv_xf)
 struct GemvXf {
-  int mode;  // VQB_XF_*
+  int mode;  // VQB_XF_* (without the SWIGLU bit)
+  int swiglu;
   const __half* add;
   const __half* res_in;
   __half* res_out;
@@ -1192,7 +1220,9 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     if (!kernel)
       return set_error(VQB_ECONFIG, "the fused-activation GEMV needs batch 1, v = 8, one level, whole-tensor "
                                     "books with every code < 256 and fp16 activations");
-    p.smem += (size_t)g.rows * 2;
+    p.smem += (size_t)g.rows * 2 + (xf->swiglu ? 1024 : 0);
+    if (xf->swiglu && (g.cols % 256 != 0 || y_dtype != VQB_F16))
+      return set_error(VQB_ECONFIG, "the SwiGLU epilogue needs N %% 256 == 0 ([gate 128 | up 128] blocks) and fp16 y");
   }
   if (used_fast) *used_fast = kernel != nullptr;
   if (tp && !kernel)
@@ -1230,6 +1260,7 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
     if (xf) {
       a.xf_mode = xf->mode;
+      a.swiglu = xf->swiglu;
       a.xf_add = xf->add;
       a.xf_res_in = xf->res_in;
       a.xf_res_out = xf->res_out;
@@ -1434,6 +1465,8 @@ extern "C" int vqb_gemv(const VqbTensor* w, const void* d_x, int32_t x_dtype, in
 extern "C" int vqb_gemv_xf(const VqbTensor* w, const void* d_x, int32_t x_dtype, int32_t mode, const void* d_res_in,
                            void* d_res_out, const void* d_weight, float eps, void* d_y, int32_t y_dtype,
                            const VqbLaunch* launch, void* d_ws, size_t ws_bytes, void* stream) {
+  const int swiglu = (mode & VQB_XF_SWIGLU_OUT) ? 1 : 0;
+  mode &= ~VQB_XF_SWIGLU_OUT;
   if (mode != VQB_XF_RMSNORM && mode != VQB_XF_SILU_MUL) return vqb::set_error(VQB_ECONFIG, "unknown activation transform %d", mode);
   if (x_dtype != VQB_F16) return vqb::set_error(VQB_ECONFIG, "the fused-activation GEMV takes fp16 activations");
   if (mode == VQB_XF_RMSNORM && (!d_res_in || !d_weight))
@@ -1441,7 +1474,7 @@ extern "C" int vqb_gemv_xf(const VqbTensor* w, const void* d_x, int32_t x_dtype,
   if (mode == VQB_XF_SILU_MUL && !d_x) return vqb::set_error(VQB_ECONFIG, "SiLU transform needs the gate|up input");
   for (const void* ptr : {d_x, d_res_in, (const void*)d_res_out, d_weight})
     if (reinterpret_cast<uintptr_t>(ptr) & 15) return vqb::set_error(VQB_ECONFIG, "activation buffers must be 16-byte aligned");
-  vqb::GemvXf xf{mode, mode == VQB_XF_RMSNORM ? reinterpret_cast<const __half*>(d_x) : nullptr,
+  vqb::GemvXf xf{mode, swiglu, mode == VQB_XF_RMSNORM ? reinterpret_cast<const __half*>(d_x) : nullptr,
                  reinterpret_cast<const __half*>(d_res_in), reinterpret_cast<__half*>(d_res_out),
                  reinterpret_cast<const __half*>(d_weight), eps};
   // x is read only by the transform (never by the TMA ring in this mode): the plan

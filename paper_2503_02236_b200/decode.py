@@ -79,8 +79,50 @@ class VQLlamaDecoder:
         self.length = 0  # host mirror of d_len (the step advances both)
         self.ws = ops.Workspace(self.device)  # private arena the captured graph keeps alive
         self.capacity = min(L.k_cache.shape[2] for L in self.layers) if self.layers else 0
+        # batch 1: the fused gate_up projection is stored interleaved per 128 columns,
+        # [gate 128 | up 128] in every 256-column block, so its GEMV epilogue emits
+        # silu(gate) * up directly (VQB_XF_SWIGLU_OUT) — one kernel less per layer
+        f_local = self.layers[0].gate_up.shape[1] // 2 if self.layers else 0
+        self.gu_il = (batch == 1 and self.layers and f_local % 128 == 0
+                      and all(L.gate_up.layout == "gemv" for L in self.layers))
+        if self.gu_il:
+            for L in self.layers:
+                L.gate_up = self._interleave_gate_up(L.gate_up)
 
     # -- construction -------------------------------------------------------------------------
+
+    @staticmethod
+    def _interleave_gate_up(w: DeviceVQTensor) -> DeviceVQTensor:
+        """[gate | up] (F + F columns) -> [gate 128 | up 128] per 256-column block."""
+        from .tp import device_shard
+        f = w.shape[1] // 2
+        ranges = []
+        for c0 in range(0, f, 128):
+            ranges += [(c0, c0 + 128), (f + c0, f + c0 + 128)]
+        return device_shard(w, col_ranges=ranges)
+
+    @staticmethod
+    def _gate_up_ranges(f: int, lo: int, hi: int, interleaved: bool):
+        """Column ranges of gate[lo:hi] then up[lo:hi] in a gate_up weight stored
+        [gate | up] or interleaved per 128 columns."""
+        if not interleaved:
+            return [(lo, hi), (f + lo, f + hi)]
+        gate, up = [], []
+        c = lo
+        while c < hi:
+            blk, off = divmod(c, 128)
+            n = min(hi - c, 128 - off)
+            gate.append((blk * 256 + off, blk * 256 + off + n))
+            up.append((blk * 256 + 128 + off, blk * 256 + 128 + off + n))
+            c += n
+        return gate + up
+
+    def _silu(self, gu: torch.Tensor) -> torch.Tensor:
+        """silu(gate) * up of a gate_up output in this decoder's column layout."""
+        if self.gu_il:
+            b, n = gu.shape
+            gu = gu.view(b, n // 256, 2, 128).permute(0, 2, 1, 3).reshape(b, n).contiguous()
+        return ops.silu_mul(gu)
 
     @staticmethod
     def synthetic(shape: LlamaShape, batch: int, capacity: int, device, seed: int = 0, working_entries: int = 256):
@@ -174,7 +216,7 @@ class VQLlamaDecoder:
 
             layers.append(DecoderLayer(
                 device_shard(L.qkv, col_ranges=hcols), device_shard(L.o, rows=(h0 * c, (h0 + hl) * c)),
-                device_shard(L.gate_up, col_ranges=[(f0, f0 + fl), (sh.ffn + f0, sh.ffn + f0 + fl)]),
+                device_shard(L.gate_up, col_ranges=cls._gate_up_ranges(sh.ffn, f0, f0 + fl, full.gu_il)),
                 device_shard(L.down, rows=(f0, f0 + fl)), L.attn_norm, L.ffn_norm, cache(L.k_cache),
                 cache(L.v_cache)))
         # the collectives run only in a real process group (rank / world given without
@@ -215,7 +257,7 @@ class VQLlamaDecoder:
             o = self._row_linear(L.o, a.view(b, hc))
             xn = ops.rmsnorm(o, self.res, L.ffn_norm, sh.eps)
             gu = self._linear(L.gate_up, xn)
-            x = self._row_linear(L.down, ops.silu_mul(gu))
+            x = self._row_linear(L.down, self._silu(gu))
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
         self.tokens.copy_(torch.argmax(self.logits, dim=-1))
@@ -237,12 +279,15 @@ class VQLlamaDecoder:
             cur ^= 1
             a = self._attend(L, qkv)
             o = self._row_linear(L.o, a.view(1, hc))
-            gu = ops.vq_gemv_rmsnorm(L.gate_up, o, res[cur], L.ffn_norm, sh.eps, residual_out=res[1 - cur])
+            if self.gu_il:
+                # ffn norm in the prologue, SiLU gating in the epilogue of the gate_up GEMV
+                h = ops.vq_gemv_rmsnorm(L.gate_up, o, res[cur], L.ffn_norm, sh.eps, residual_out=res[1 - cur],
+                                        swiglu=True)
+            else:
+                h = self._silu(ops.vq_gemv_rmsnorm(L.gate_up, o, res[cur], L.ffn_norm, sh.eps,
+                                                   residual_out=res[1 - cur]))
             cur ^= 1
-            # the SiLU gate stays a separate kernel: fused into the down GEMV every CTA
-            # would recompute all 11008 gated activations (measured 0.4 us slower per
-            # layer, tools/xf_bench.py); the norm fusion reads only 2 x 8 KB per CTA
-            x = self._row_linear(L.down, ops.silu_mul(gu))
+            x = self._row_linear(L.down, h)
         xn = ops.rmsnorm(x, res[cur], self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
         self.tokens.copy_(torch.argmax(self.logits, dim=-1))
@@ -275,7 +320,7 @@ class VQLlamaDecoder:
             if "linear" not in skip:
                 gu = self._linear(L.gate_up, xn)
             if "silu" not in skip:
-                hm = ops.silu_mul(gu)
+                hm = self._silu(gu)
             x = self._linear(L.down, hm) if "linear" not in skip else xn
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head

@@ -138,14 +138,16 @@ def vq_gemv(w: DeviceVQTensor, x: torch.Tensor, out_dtype=None, launch=None) -> 
 
 
 def vq_gemv_rmsnorm(w: DeviceVQTensor, x, residual: torch.Tensor, weight: torch.Tensor, eps: float,
-                    residual_out: torch.Tensor = None, out_dtype=torch.float16, launch=None) -> torch.Tensor:
+                    residual_out: torch.Tensor = None, out_dtype=torch.float16, launch=None,
+                    swiglu: bool = False) -> torch.Tensor:
     """Batch-1 decode GEMV with the residual add + RMSNorm fused into its prologue:
     h = residual + x (x may be None), residual_out = h, y = (weight * rmsnorm(h)) @ W.
     The same result as ``rmsnorm`` followed by ``vq_gemv``, one launch instead of two;
     ``residual_out`` must be a different buffer from ``residual`` (every CTA reads it)."""
     if residual_out is not None and residual_out.data_ptr() == residual.data_ptr():
         raise ConfigError("residual_out must not alias residual")
-    return _gemv_xf(w, x, N.XF_RMSNORM, residual, residual_out, weight, eps, out_dtype, launch)
+    mode = N.XF_RMSNORM | (N.XF_SWIGLU_OUT if swiglu else 0)
+    return _gemv_xf(w, x, mode, residual, residual_out, weight, eps, out_dtype, launch)
 
 
 def vq_gemv_silu(w: DeviceVQTensor, gate_up: torch.Tensor, out_dtype=torch.float16, launch=None) -> torch.Tensor:
@@ -158,13 +160,14 @@ def _gemv_xf(w, x, mode, res_in, res_out, weight, eps, out_dtype, launch):
     if len(w.shape) != 2:
         raise ShapeError(f"quantized weight must be 2-D, got {w.shape}")
     m, n = w.shape
-    want = 2 * m if mode == N.XF_SILU_MUL else m
+    swiglu = bool(mode & N.XF_SWIGLU_OUT)
+    want = 2 * m if (mode & ~N.XF_SWIGLU_OUT) == N.XF_SILU_MUL else m
     for t in (x, res_in, res_out, weight):
         if t is not None and (t.numel() != (want if t is x else m) or t.dtype != torch.float16):
             raise ShapeError(f"fused-activation GEMV operand of {t.numel()} {t.dtype} values, expected fp16 "
                              f"rows of {want if t is x else m}")
     od = torch_dtype(out_dtype or torch.float16)
-    y = torch.empty((1, n), dtype=od, device=w.device)
+    y = torch.empty((1, n // 2 if swiglu else n), dtype=od, device=w.device)
     L = launch if launch is not None else N.VqbLaunch()
     lib = N.lib()
     s = w.struct()

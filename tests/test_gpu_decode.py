@@ -426,3 +426,26 @@ def test_fused_append_attention_bit_identical(batch, dev):
         a.replay()
         b.replay()
         assert torch.equal(a.logits, b.logits)
+
+
+def test_swiglu_epilogue_matches_separate_kernels(dev):
+    """VQB_XF_SWIGLU_OUT: the gate_up GEMV stored [gate 128 | up 128] per 256-column
+    block emits silu(gate) * up from its epilogue — bit-identical to the fp16 gate_up
+    output followed by silu_mul, whole and split column blocks alike."""
+    N, DeviceVQTensor, ops = _mods()
+    from paper_2503_02236_b200.decode import WEIGHT_CFG
+    g = torch.Generator(device=dev).manual_seed(23)
+    for m, n in ((4096, 22016), (512, 1024)):
+        codes = torch.randint(0, 256, (1, m * n // 8), generator=g, device=dev, dtype=torch.int32)
+        books = (torch.randn((1, 65536, 8), generator=g, device=dev) * 0.05).half()
+        w = DeviceVQTensor.from_device_codes(codes, (m, n), WEIGHT_CFG, books).relayout("gemv")
+        res = torch.randn((1, m), generator=g, device=dev).half()
+        x = torch.randn((1, m), generator=g, device=dev).half()
+        nw = (1 + 0.1 * torch.randn(m, generator=g, device=dev)).half()
+        r_a, r_b = torch.empty_like(res), torch.empty_like(res)
+        gu = ops.vq_gemv_rmsnorm(w, x, res, nw, 1e-5, residual_out=r_a)
+        gu = gu.view(1, n // 256, 2, 128).permute(0, 2, 1, 3).reshape(1, n).contiguous()
+        ref = ops.silu_mul(gu)
+        h = ops.vq_gemv_rmsnorm(w, x, res, nw, 1e-5, residual_out=r_b, swiglu=True)
+        assert h.shape == (1, n // 2)
+        assert torch.equal(h, ref) and torch.equal(r_a, r_b)
