@@ -21,6 +21,7 @@
  *   vqb_cq_quantize  <- vqforge.codec.quantize / _nearest (codec.py:239-253, 367-389) for KV rows:
  *                       online nearest-centroid quantization of new tokens into a KV cache
  *   vqb_attn_decode_len, vqb_rmsnorm, vqb_qkv_rope, vqb_qkv_rope_append, vqb_silu_mul, vqb_add_len,
+ *   vqb_sample,
  *   vqb_take_device_error
  *                    <- the end-to-end decode step around the fused ops (
  *                       no vqforge counterpart: the reference stops at single fused kernels)
@@ -264,6 +265,14 @@ int vqb_qkv_rope_append(const void* d_qkv, void* d_q_out, const VqbTensor* k_cac
                         int32_t B, int32_t H, int32_t C, const int32_t* d_len, float theta, void* stream);
 /* out (rows, F) = silu(gate) * up for a fused [gate | up] (rows, 2F) input. */
 int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, int32_t ffn, void* stream);
+/* Next tokens of a decode step: d_tokens[b] (int64) drawn from softmax(logits[b] / T)
+ * restricted to the logits >= the top_k-th largest (top_k 0 = all) by the Gumbel-max
+ * trick with a counter-based hash of (seed, *d_step, b, i) as the noise (d_step may be
+ * NULL = step 0; pass the decode length so graph replays draw fresh noise);
+ * temperature 0 = greedy argmax. Ties resolve to the lowest index. logits (B, vocab)
+ * fp16 or fp32. */
+int vqb_sample(const void* d_logits, int32_t logits_dtype, int32_t B, int32_t vocab, float temperature,
+               int32_t top_k, uint64_t seed, const int32_t* d_step, int64_t* d_tokens, void* stream);
 /* d_len[0] += delta on the stream (advances a graph-replayed decode loop). */
 int vqb_add_len(int32_t* d_len, int32_t delta, void* stream);
 /* Read and clear the device error word (synchronises the device): bit 0 = a KV

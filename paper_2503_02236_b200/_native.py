@@ -47,7 +47,7 @@ EXPORTS = (
     "vqb_debug_smem_base", "vqb_attn_decode_len", "vqb_cq_quantize", "vqb_rmsnorm", "vqb_qkv_rope",
     "vqb_silu_mul", "vqb_add_len", "vqb_qkv_rope_append", "vqb_take_device_error", "vqb_gemv_grouped",
     "vqb_tp_buffer_bytes", "vqb_ipc_get_handle", "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp",
-    "vqb_tp_finish", "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append",
+    "vqb_tp_finish", "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append", "vqb_sample",
 )
 XF_RMSNORM, XF_SILU_MUL, XF_SWIGLU_OUT = 1, 2, 4
 
@@ -143,6 +143,7 @@ def lib():
             L.vqb_silu_mul.argtypes = [vp, vp, i32, i32, vp]
             L.vqb_qkv_rope_append.argtypes = [vp, vp, T, T, i32, i32, i32, vp, f32, vp]
             L.vqb_add_len.argtypes = [vp, i32, vp]
+            L.vqb_sample.argtypes = [vp, i32, i32, i32, f32, i32, ctypes.c_uint64, vp, vp, vp]
             L.vqb_take_device_error.argtypes = [P(i32)]
             L.vqb_cq_quantize.argtypes = [T, vp, i32, i64, i64, i64, i32, i32, vp, vp]
             L.vqb_layout_bytes.argtypes = [T, i32]
@@ -167,7 +168,7 @@ def lib():
                          "vqb_silu_mul", "vqb_add_len", "vqb_cq_quantize", "vqb_qkv_rope_append",
                          "vqb_take_device_error", "vqb_gemv_grouped", "vqb_ipc_get_handle",
                          "vqb_ipc_open_handle", "vqb_ipc_close_handle", "vqb_gemv_tp", "vqb_tp_finish",
-                         "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append"):
+                         "vqb_tp_take_error", "vqb_gemv_xf", "vqb_attn_decode_append", "vqb_sample"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib

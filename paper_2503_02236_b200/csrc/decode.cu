@@ -527,6 +527,132 @@ __global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* _
   }
 }
 
+// ---- token sampling (the decode loop's last step) ----
+// Gumbel-max: argmax_i (logit_i / T + g_i), g_i = -log(-log(u_i)), is an exact draw
+// from softmax(logit / T); u_i comes from a counter-based hash of (seed, step, row, i),
+// so a graph-replayed step draws fresh noise from the device length. top_k keeps the
+// logits >= the k-th largest (ties kept, the usual top-k warper's rule), found by a
+// 4-pass radix select over order-preserving 32-bit keys. T == 0 is greedy argmax.
+// Ties in the score resolve to the lowest index (torch.argmax's rule).
+__device__ __forceinline__ uint32_t order_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float sample_uniform(uint64_t seed, uint32_t step, uint32_t row, uint32_t i) {
+  uint64_t z = (seed ^ ((((uint64_t)step << 32) | row) * 0x9E3779B97F4A7C15ull)) + (uint64_t)(i + 1) * 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return ((float)(uint32_t)(z >> 41) + 0.5f) * 1.1920928955078125e-7f;  // (k + 0.5) / 2^23: exact, in (0, 1)
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict__ logits, int dtype, int V,
+                                                         float inv_temp, int top_k, uint64_t seed,
+                                                         const int* __restrict__ d_step, int64_t* __restrict__ out) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t sel[2];  // prefix, remaining
+  __shared__ float best_s[THREADS / 32];
+  __shared__ int best_i[THREADS / 32];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* lf = reinterpret_cast<const float*>(logits) + (int64_t)b * V;
+  const __half* lh = reinterpret_cast<const __half*>(logits) + (int64_t)b * V;
+  auto load = [&](int i) { return dtype == VQB_F32 ? __ldg(lf + i) : __half2float(lh[i]); };
+  const bool greedy = !(inv_temp > 0.f);
+  uint32_t thr = 0;  // keep keys >= thr
+  if (!greedy && top_k > 0 && top_k < V) {
+    uint32_t prefix = 0, mask = 0;
+    if (tid == 0) sel[1] = (uint32_t)top_k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += THREADS) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < V; i += THREADS) {
+        const uint32_t k = order_key(load(i));
+        if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) {  // the digit holding the remaining-th largest: scan bins from the top
+        uint32_t c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          c[j] = hist[255 - (lane * 8 + j)];
+          tot += c[j];
+        }
+        uint32_t incl = tot;  // inclusive prefix over lanes (lane 0 = the highest bins)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t rem = sel[1];
+        uint32_t run = incl - tot;
+        const bool mine = run < rem && incl >= rem;
+        if (mine) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (run + c[j] >= rem) {
+              sel[0] = (uint32_t)(255 - (lane * 8 + j));
+              sel[1] = rem - run;
+              break;
+            }
+            run += c[j];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= sel[0] << shift;
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+    thr = prefix;
+  }
+  const uint32_t step = d_step ? (uint32_t)__ldg(d_step) : 0u;
+  float bs = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = tid; i < V; i += THREADS) {
+    const float x = load(i);
+    if (order_key(x) < thr) continue;
+    const float s = greedy ? x : fmaf(x, inv_temp, -__logf(-__logf(sample_uniform(seed, step, (uint32_t)b, (uint32_t)i))));
+    if (s > bs || bi == 0x7fffffff) {  // ascending i per thread: strict > keeps the lowest index
+      bs = s;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (os > bs || (os == bs && oi < bi)) {
+      bs = os;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    best_s[warp] = bs;
+    best_i[warp] = bi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    bs = lane < THREADS / 32 ? best_s[lane] : -INFINITY;
+    bi = lane < THREADS / 32 ? best_i[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (os > bs || (os == bs && oi < bi)) {
+        bs = os;
+        bi = oi;
+      }
+    }
+    if (lane == 0) out[b] = bi;
+  }
+}
+
 }  // namespace vqb
 
 using namespace vqb;
@@ -614,6 +740,19 @@ extern "C" int vqb_take_device_error(int32_t* out) {
   VQB_CUDA_CHECK(cudaMemcpyFromSymbol(&v, vqb::g_append_oob, sizeof(v)));
   VQB_CUDA_CHECK(cudaMemcpyToSymbol(vqb::g_append_oob, &zero, sizeof(zero)));
   if (out) *out = (int32_t)v;
+  return VQB_OK;
+}
+
+extern "C" int vqb_sample(const void* d_logits, int32_t logits_dtype, int32_t B, int32_t vocab, float temperature,
+                          int32_t top_k, uint64_t seed, const int32_t* d_step, int64_t* d_tokens, void* stream) {
+  if (B < 1 || vocab < 1) return set_error(VQB_ESHAPE, "sample needs B >= 1 and vocab >= 1");
+  if (logits_dtype != VQB_F16 && logits_dtype != VQB_F32) return set_error(VQB_ECONFIG, "sample reads fp16 or fp32 logits");
+  if (!(temperature >= 0.f) || top_k < 0) return set_error(VQB_ECONFIG, "sample needs temperature >= 0 and top_k >= 0");
+  const float inv_temp = temperature > 0.f ? 1.0f / temperature : 0.f;
+  VQB_CUDA_CHECK(launch_pdl(sample_kernel<1024>, dim3(B), dim3(1024), 0, reinterpret_cast<cudaStream_t>(stream),
+                            d_logits, (int)logits_dtype, (int)vocab, inv_temp, (int)top_k, seed, d_step, d_tokens));
+  VQB_LAUNCH_CHECK("sample_kernel");
+  set_kernel("sample");
   return VQB_OK;
 }
 

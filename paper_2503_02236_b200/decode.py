@@ -8,10 +8,11 @@ step the paper evaluates end to end: per layer
     CQ cache -> VQ GEMV o -> RMSNorm(+residual) -> VQ GEMV gate|up -> SiLU*up ->
     VQ GEMV down
 
-then the final RMSNorm, a dense fp16 LM head (cuBLAS, a plain library GEMM) and
-greedy sampling. The current length lives in a device int32 that the step advances
+then the final RMSNorm, a dense fp16 LM head (cuBLAS, a plain library GEMM) and the
+next-token draw (`vqb_sample`: greedy, or temperature / top-k by Gumbel-max). The current length lives in a device int32 that the step advances
 itself, so one CUDA graph replays every decode step while the cache grows.
-Batches of 1-8 rows take the CUDA-core GEMV, larger batches the tcgen05 GEMM.
+Batches of up to 64 rows take the decode GEMV (CUDA cores, mma.sync or tcgen05 by batch
+size), larger batches the tcgen05 GEMM.
 """
 
 import os
@@ -78,6 +79,8 @@ class VQLlamaDecoder:
         self._graph = None
         self.length = 0  # host mirror of d_len (the step advances both)
         self.ws = ops.Workspace(self.device)  # private arena the captured graph keeps alive
+        # next-token rule (vqb_sample): greedy by default; set_sampling before capture()
+        self.temperature, self.top_k, self.seed = 0.0, 0, 0
         self.capacity = min(L.k_cache.shape[2] for L in self.layers) if self.layers else 0
         # batch 1: the fused gate_up projection is stored interleaved per 128 columns,
         # [gate 128 | up 128] in every 256-column block, so its GEMV epilogue emits
@@ -156,7 +159,7 @@ class VQLlamaDecoder:
 
     # -- the step -----------------------------------------------------------------------------
 
-    gemv_max_rows = 64  # batches up to this take the decode GEMV (CUDA cores 1-2, mma.sync 4-8, tcgen05 9-64)
+    gemv_max_rows = 64  # batches up to this take the decode GEMV (CUDA cores 1-3, mma.sync 4, tcgen05 5-64)
     fuse_norms = True  # batch 1: RMSNorm / SiLU gating fused into the following GEMV's prologue
     fuse_append = True  # RoPE + KV append inside the attention kernel (CQ-4 caches at C = 128, batch <= 8)
 
@@ -260,8 +263,7 @@ class VQLlamaDecoder:
             x = self._row_linear(L.down, self._silu(gu))
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
-        self.tokens.copy_(torch.argmax(self.logits, dim=-1))
-        return self.tokens
+        return self._sample()
 
     def _step_fused(self) -> torch.Tensor:
         """Batch-1 step with the norms and the SiLU gate fused into the GEMVs that
@@ -290,8 +292,7 @@ class VQLlamaDecoder:
             x = self._row_linear(L.down, h)
         xn = ops.rmsnorm(x, res[cur], self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
-        self.tokens.copy_(torch.argmax(self.logits, dim=-1))
-        return self.tokens
+        return self._sample()
 
     def _step_ablated(self, skip):
         sh, b = self.shape, self.batch
@@ -324,8 +325,19 @@ class VQLlamaDecoder:
             x = self._linear(L.down, hm) if "linear" not in skip else xn
         xn = ops.rmsnorm(x, self.res, self.final_norm, sh.eps)
         self.logits = xn @ self.lm_head
-        self.tokens.copy_(torch.argmax(self.logits, dim=-1))
-        return self.tokens
+        return self._sample()
+
+    def set_sampling(self, temperature: float = 0.0, top_k: int = 0, seed: int = 0) -> None:
+        """Temperature / top-k sampling of the next token (Gumbel-max over the logits,
+        noise hashed from the seed and the device length, so every replayed step draws
+        afresh and TP ranks draw identically). temperature 0 = greedy. A captured graph
+        keeps the rule it was captured with: call this before capture()."""
+        if temperature < 0 or top_k < 0:
+            raise ConfigError("sampling needs temperature >= 0 and top_k >= 0")
+        self.temperature, self.top_k, self.seed = float(temperature), int(top_k), int(seed)
+
+    def _sample(self) -> torch.Tensor:
+        return ops.sample(self.logits, self.temperature, self.top_k, self.seed, d_step=self.d_len, out=self.tokens)
 
     def capture(self) -> None:
         """Record one step as a CUDA graph. The warm-up step (on the capture stream)

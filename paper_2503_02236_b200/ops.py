@@ -273,6 +273,26 @@ def silu_mul(gate_up: torch.Tensor, out=None) -> torch.Tensor:
     return out
 
 
+def sample(logits: torch.Tensor, temperature: float = 0.0, top_k: int = 0, seed: int = 0,
+           d_step: torch.Tensor = None, out: torch.Tensor = None) -> torch.Tensor:
+    """Next tokens (B,) int64 from logits (B, vocab) fp16/fp32: a Gumbel-max draw from
+    softmax(logits / temperature) over the top_k largest logits (0 = all; ties at the
+    k-th value kept), noise hashed from (seed, d_step[0], row, index); temperature 0 is
+    greedy argmax (lowest index on ties, like torch.argmax)."""
+    if logits.dim() != 2 or logits.dtype not in (torch.float16, torch.float32) or not logits.is_contiguous():
+        raise ShapeError(f"logits {tuple(logits.shape)} {logits.dtype} must be a contiguous (B, vocab) fp16/fp32 tensor")
+    b, v = logits.shape
+    out = torch.empty(b, dtype=torch.int64, device=logits.device) if out is None else out
+    if out.dtype != torch.int64 or out.numel() != b or not out.is_contiguous():
+        raise ShapeError("sample writes a contiguous (B,) int64 tensor")
+    if d_step is not None and (d_step.dtype != torch.int32 or d_step.device != logits.device):
+        raise ShapeError("d_step must be a device int32 tensor")
+    N.check(N.lib().vqb_sample(logits.data_ptr(), dtype_enum(logits.dtype), b, v, float(temperature), int(top_k),
+                               int(seed) & 0xFFFFFFFFFFFFFFFF, None if d_step is None else d_step.data_ptr(),
+                               out.data_ptr(), _stream(logits.device)))
+    return out
+
+
 def add_len(d_len: torch.Tensor, delta: int = 1) -> None:
     N.check(N.lib().vqb_add_len(d_len.data_ptr(), int(delta), _stream(d_len.device)))
 

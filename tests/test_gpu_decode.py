@@ -449,3 +449,27 @@ def test_swiglu_epilogue_matches_separate_kernels(dev):
         h = ops.vq_gemv_rmsnorm(w, x, res, nw, 1e-5, residual_out=r_b, swiglu=True)
         assert h.shape == (1, n // 2)
         assert torch.equal(h, ref) and torch.equal(r_a, r_b)
+
+
+def test_decode_sampling_replay_matches_eager(dev):
+    """Temperature / top-k sampling inside the decode step: a replayed graph draws
+    the eager step's tokens (the noise is keyed on the device length), every token is
+    in the top-k set of its logits, and the draw is the oracle's Gumbel-max choice."""
+    from oracle import sample_oracle as SO
+    from paper_2503_02236_b200.decode import LlamaShape, VQLlamaDecoder
+    sh = LlamaShape(hidden=512, heads=4, head_dim=128, ffn=1024, layers=2, vocab=256)
+    a = VQLlamaDecoder.synthetic(sh, 4, 64, dev, seed=8)
+    b = VQLlamaDecoder.synthetic(sh, 4, 64, dev, seed=8)
+    for d in (a, b):
+        d.set_sampling(temperature=0.8, top_k=20, seed=77)
+        d.tokens.fill_(7)
+    b.capture()
+    for _ in range(4):
+        tok = a.run_step().clone()
+        b.replay()
+        assert torch.equal(tok, b.tokens)
+        lg = a.logits.float().cpu().numpy()
+        sc = SO.scores(lg, 0.8, 20, 77, int(a.d_len.item()))
+        t = tok.cpu().numpy()
+        got = sc[np.arange(4), t]
+        assert np.all(np.isfinite(got)) and np.all(got >= sc.max(axis=1) - 1e-4 * np.maximum(1, np.abs(sc.max(axis=1))))
