@@ -111,7 +111,10 @@ struct AttnSmem {
   // address is one PRMT of (column, code, region high bytes). The dynamic base is
   // only known at run time (1 KB on B200), hence the slack of one region.
   static constexpr size_t region = 65536;
-  static constexpr size_t scratch_bytes = ((size_t)kAttnWarps * (C + 2) + C + 1) * 4 + 16;
+  // merge scratch, then each warp's 32 token probabilities (fp16, the V phase's
+  // broadcast), then the book mbarrier
+  static constexpr size_t pbuf_off = ((((size_t)kAttnWarps * (C + 2) + C + 1) * 4) + 63) & ~(size_t)63;
+  static constexpr size_t scratch_bytes = pbuf_off + (size_t)kAttnWarps * 64 + 16;
   static constexpr size_t total = 3 * region + scratch_bytes;
   static_assert(256 * G * 4 <= region && 256 * G * EPB <= region, "region overflow");
 };
@@ -178,7 +181,7 @@ template <int V, int GPL, bool PRMT, bool APPEND>
 __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int bh, int tok0, int tok1, uint32_t lut_base,
                                                  uint32_t vbook_base, float& m_w, float& l_lane,
                                                  float (&acc)[GPL][V], uint4 (&ka)[2 * GPL],
-                                                 uint4 (&va)[2 * GPL], int fresh_t0) {
+                                                 uint4 (&va)[2 * GPL], int fresh_t0, uint32_t pbuf) {
   using SM = AttnSmem<V, GPL>;
   constexpr int G = SM::G, EPB = SM::EPB;
   constexpr int Q = 2 * GPL;  // 16-byte loads per lane per 32-token batch
@@ -205,9 +208,9 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vbase + off), "r"(Q * 512) : "memory");
     }
   };
-  // K phase + online-softmax update of one 32-token batch; returns this lane's
-  // token probability (fp16 bits) for the V phase
-  auto kphase = [&](const uint4 (&kc)[Q], int tb) -> uint32_t {
+  // K phase + online-softmax update of one 32-token batch; lane l stores token l's
+  // probability (fp16) in the warp's pbuf for the V phase
+  auto kphase = [&](const uint4 (&kc)[Q], int tb) {
     // lane partial logits for the 32 slots (slot i = token i ^ lane)
     auto partial = [&](int i) {
       float acc_s = 0.f;
@@ -235,27 +238,46 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
       for (int i = 0; i < off; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i + off], off);
     // tokens past the valid length (a partial last batch) get p = 0
     const float z = (tb + lane < T) ? s[0] : -INFINITY;
-    float mb = z;
+    // the running max moves only when some logit exceeds it (rarer as the span goes
+    // on): one vote instead of the 5-level max tree and the rescale. Bit-identical —
+    // the skipped path would compute corr = exp2(0) = 1.
+    float corr = 1.f;
+    if (__any_sync(0xffffffffu, z > m_w)) {
+      float mb = z;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
-    const float m_new = fmaxf(m_w, mb);
-    const float corr = fast_exp2(m_w - m_new);
-    const float p = fast_exp2(z - m_new);
+      for (int off = 16; off >= 1; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
+      const float m_new = fmaxf(m_w, mb);
+      corr = fast_exp2(m_w - m_new);
+      m_w = m_new;
+#pragma unroll
+      for (int j = 0; j < GPL; ++j)
+#pragma unroll
+        for (int c = 0; c < V; ++c) acc[j][c] *= corr;
+    }
+    const float p = fast_exp2(z - m_w);
     l_lane = l_lane * corr + p;
-    m_w = m_new;
-#pragma unroll
-    for (int j = 0; j < GPL; ++j)
-#pragma unroll
-      for (int c = 0; c < V; ++c) acc[j][c] *= corr;
-    const uint32_t ph = (uint32_t)__half_as_ushort(__float2half_rn(p));
-    return ph | (ph << 16);  // (p, p) for the fp16x2 V accumulation
+    __syncwarp();  // every lane has read the previous batch's probabilities
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(pbuf + lane * 2), "h"(__half_as_ushort(__float2half_rn(p))) : "memory");
+    __syncwarp();
   };
-  // V phase: slot i holds token i ^ lane, whose probability lives on that lane.
+  // V phase: slot i holds token i ^ lane. Slots 4k..4k+3 hold tokens
+  // 4(k ^ (lane >> 2)) + (r ^ (lane & 3)), so one 8-byte broadcast read of pbuf serves
+  // four slots and a PRMT (per-lane selector of half r ^ (lane & 3)) makes each slot's
+  // (p, p) pair: 8 LDS instead of 32 shuffles per batch — the MIO pipe (shared loads
+  // and shuffles) is what bounds this kernel.
   // p * V accumulates in packed fp16x2 windows of 8 tokens (HFMA2, full rate; the
   // mixed-precision fp32 FMA is quarter rate), flushed into the fp32 accumulators
   // with an exact widening FMA — the GEMV's windowing, at attention's 2e-3 bound.
-  auto vphase = [&](const uint4 (&vc)[Q], uint32_t ph) {
+  uint32_t psel[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t h2 = 2u * (uint32_t)(r ^ (lane & 3));
+    psel[r] = h2 | ((h2 + 1) << 4) | (h2 << 8) | ((h2 + 1) << 12);
+  }
+  const uint32_t pb_lane = pbuf + (uint32_t)(lane >> 2) * 8;  // pbuf is 64-byte aligned
+  auto vphase = [&](const uint4 (&vc)[Q]) {
     constexpr int HW = V / 2;  // fp16x2 words per entry
+    uint2 pv = make_uint2(0u, 0u);
 #pragma unroll
     for (int w8 = 0; w8 < 4; ++w8) {
       uint32_t hw[GPL][HW];
@@ -266,7 +288,8 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
 #pragma unroll
       for (int ii = 0; ii < 8; ++ii) {
         const int i = w8 * 8 + ii;
-        const uint32_t pp = (uint32_t)__shfl_sync(0xffffffffu, ph, i ^ lane);
+        if ((i & 3) == 0) pv = lds64(pb_lane ^ (uint32_t)((i >> 2) * 8));
+        const uint32_t pp = prmt(pv.x, pv.y, psel[i & 3]);
 #pragma unroll
         for (int j = 0; j < GPL; ++j) {
           const int byte = i * GPL + j;
@@ -316,9 +339,9 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
   for (; t0 < tok1; t0 += STRIDE) {
     const int tn = t0 + STRIDE;
     prefetch(t0 + (PF_AHEAD + 1) * STRIDE);
-    const uint32_t ph = kphase(ka, t0);
+    kphase(ka, t0);
     if (tn < tok1) load_k(ka, tn);
-    vphase(va, ph);
+    vphase(va);
     if (tn < tok1) load_v(va, tn);
   }
 }
@@ -407,6 +430,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   uint8_t* vbook_s = smem + lut_off + SM::region;
   float* lut_s = reinterpret_cast<float*>(smem + lut_off);
   float* scratch = reinterpret_cast<float*>(smem + scratch_off);
+  const uint32_t pbuf = smem_u32(smem + scratch_off + SM::pbuf_off) + (uint32_t)(threadIdx.x >> 5) * 64;
   // mbarrier for the bulk-copied books (8-byte aligned slot at the end of the scratch)
   const uint32_t book_bar = smem_u32(smem + ((scratch_off + SM::scratch_bytes - 8) & ~7u));
   const bool bulk_books = (V == 2) && a.kbt != nullptr && a.vbt != nullptr;
@@ -590,10 +614,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     if (tok0 + warp * 32 < tok1) attn_load_batch<V, GPL>(a, bh, tok0 + warp * 32, ka, va, APPEND && tok0 + warp * 32 == fresh_t0);
     if (aligned)
       attn_stream_span<V, GPL, true, APPEND>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va,
-                                              fresh_t0);
+                                              fresh_t0, pbuf);
     else
       attn_stream_span<V, GPL, false, APPEND>(a, T, bh, tok0, tok1, lut_base, vbook_base, m_w, l_lane, acc, ka, va,
-                                               fresh_t0);
+                                               fresh_t0, pbuf);
 
     ph.mark(a, 1);
     // ---- merge the warps of this span
