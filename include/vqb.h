@@ -77,9 +77,10 @@ extern "C" {
  *            rows per 16-byte load (8 rows of u16 codes, 16 rows of u8 codes).
  *            Levels are stored one after another (level-major, like the reference).
  * KV_IL    : KV-cache codes interleaved for the decode-attention kernel (u8 codes,
- *            G = C/v in {32, 64}), per level and per (b, h) row block of T tokens:
- *            [T/TPL][32][TPL][GPL] with GPL = G/32 groups per lane (lane l owns groups
- *            l + 32*j) and TPL = 16/GPL tokens per 16-byte lane load.
+ *            G = C/v in {32, 64}), per level and per (b, h) row block of T tokens,
+ *            per 32-token batch: [G/16 words][32 lanes][16 bytes]. Lane (h, ll) =
+ *            (lane >> 4, lane & 15) owns groups ll + 16*(j ^ h), j < G/16, and stores
+ *            token 16h + (i ^ ll) at slot i (0..15), byte i*(G/16) + j.
  * PLAIN    : the reference `codes` array (R, S) level-major in the narrowest unsigned
  *            type: u8 when log2_entries <= 8, else u16.
  */

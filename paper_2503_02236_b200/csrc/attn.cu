@@ -15,13 +15,16 @@
 //  * K side as a lookup table: q is fixed per (b, h), so the CTA builds
 //    LUT[e][g] = log2(e)/sqrt(C) * <q_g, K_book_g[e]> once per (b, h); a token's
 //    logit is sum_g LUT[code_g][g]: one LDS.32 + FADD per code, no dequantise.
-//  * bank-conflict-free by construction: lane l owns channel groups g = l + 32j;
-//    the LUT and the V book are stored [entry][group], so lane l always hits bank
-//    (l mod 32) whatever its code is. With a 256-byte row the shared address is
+//  * bank-conflict-free by construction: lane (h, ll) = (lane >> 4, lane & 15) owns
+//    channel groups g = ll + 16 (j ^ h); the LUT and the V book are stored
+//    [entry][group], so in every shared load the 32 lanes hit 32 distinct banks
+//    (g mod 32) whatever their codes are. With a 256-byte row the shared address is
 //    a single PRMT of the code byte and the lane's column (plus the region base).
-//  * select-free logit reduction: the KV_IL layout stores token (i ^ l) in lane
-//    l's slot i, so the 32x32 transpose-reduction across the warp is 31
-//    shuffle+add pairs with no selects, leaving lane l with token l's logit.
+//  * select-free logit reduction: in the KV_IL layout a half-warp spans a token's
+//    groups and lane (h, ll) stores token 16h + (i ^ ll) in slot i, so the 16x16
+//    transpose-reduction inside each half-warp is 15 shuffle+add pairs with no
+//    selects, leaving lane l with token l's logit (16 fewer shuffles per 32 tokens
+//    than spanning the groups over the whole warp).
 //  * online softmax (flash-decode) in the exp2 domain; V is dequantised in
 //    registers and fused into fp32 accumulators with fma.rn.f32.f16.
 //  * the next 32-token batch's K codes load during the V phase, its V codes during
@@ -180,21 +183,23 @@ __device__ __forceinline__ void attn_load_batch(const AttnArgs& a, int bh, int t
 template <int V, int GPL, bool PRMT, bool APPEND>
 __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int bh, int tok0, int tok1, uint32_t lut_base,
                                                  uint32_t vbook_base, float& m_w, float& l_lane,
-                                                 float (&acc)[GPL][V], uint4 (&ka)[2 * GPL],
+                                                 float (&acc)[2 * GPL][V], uint4 (&ka)[2 * GPL],
                                                  uint4 (&va)[2 * GPL], int fresh_t0, uint32_t pbuf) {
   using SM = AttnSmem<V, GPL>;
   constexpr int G = SM::G, EPB = SM::EPB;
-  constexpr int Q = 2 * GPL;  // 16-byte loads per lane per 32-token batch
+  constexpr int Q = 2 * GPL;    // 16-byte loads per lane per 32-token batch
+  constexpr int GPH = 2 * GPL;  // groups per lane (KV_IL: a half-warp spans the G groups)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hh = lane >> 4, ll = lane & 15;
   const int64_t TG = (int64_t)a.T_cap * G;
   const uint8_t* kbase = a.kc + (int64_t)bh * TG;
   const uint8_t* vbase = a.vc + (int64_t)bh * TG;
   // per-lane columns (and, for the single-prmt form, the region's high address bytes)
-  uint32_t colK[GPL], colV[GPL], cbK[GPL], cbV[GPL];
+  uint32_t colK[GPH], colV[GPH], cbK[GPH], cbV[GPH];
 #pragma unroll
-  for (int j = 0; j < GPL; ++j) {
-    colK[j] = (uint32_t)(lane + 32 * j) * 4;
-    colV[j] = (uint32_t)(lane + 32 * j) * EPB;
+  for (int j = 0; j < GPH; ++j) {
+    colK[j] = (uint32_t)(ll + 16 * (j ^ hh)) * 4;
+    colV[j] = (uint32_t)(ll + 16 * (j ^ hh)) * EPB;
     cbK[j] = (lut_base & 0xffff0000u) | colK[j];
     cbV[j] = (vbook_base & 0xffff0000u) | colV[j];
   }
@@ -211,29 +216,29 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
   // K phase + online-softmax update of one 32-token batch; lane l stores token l's
   // probability (fp16) in the warp's pbuf for the V phase
   auto kphase = [&](const uint4 (&kc)[Q], int tb) {
-    // lane partial logits for the 32 slots (slot i = token i ^ lane)
+    // lane partial logits for its 16 slots (slot i = token 16 hh + (i ^ ll))
     auto partial = [&](int i) {
       float acc_s = 0.f;
 #pragma unroll
-      for (int j = 0; j < GPL; ++j) {
-        const int byte = i * GPL + j;
+      for (int j = 0; j < GPH; ++j) {
+        const int byte = i * GPH + j;
         const uint32_t w = (&kc[byte / 16].x)[(byte % 16) / 4];
         const float lv = lds_f32(row_addr<G * 4, PRMT>(w, byte % 4, cbK[j], colK[j], lut_base));
         acc_s = (j == 0) ? lv : acc_s + lv;
       }
       return acc_s;
     };
-    // select-free transpose-reduction: afterwards s[0] on lane l is token l's logit.
-    // The first (offset 16) step is fused into the partial computation so only 16
-    // partial logits are ever live.
-    float s[16];
+    // select-free transpose-reduction inside each half-warp: afterwards s[0] on lane l
+    // is token l's logit. The first (offset 8) step is fused into the partial
+    // computation so only 8 partial logits are ever live; 15 shuffles per batch.
+    float s[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float lo = partial(i), hi = partial(i + 16);
-      s[i] = lo + __shfl_xor_sync(0xffffffffu, hi, 16);
+    for (int i = 0; i < 8; ++i) {
+      const float lo = partial(i), hi = partial(i + 8);
+      s[i] = lo + __shfl_xor_sync(0xffffffffu, hi, 8);
     }
 #pragma unroll
-    for (int off = 8; off >= 1; off >>= 1)
+    for (int off = 4; off >= 1; off >>= 1)
 #pragma unroll
       for (int i = 0; i < off; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i + off], off);
     // tokens past the valid length (a partial last batch) get p = 0
@@ -250,7 +255,7 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
       corr = fast_exp2(m_w - m_new);
       m_w = m_new;
 #pragma unroll
-      for (int j = 0; j < GPL; ++j)
+      for (int j = 0; j < GPH; ++j)
 #pragma unroll
         for (int c = 0; c < V; ++c) acc[j][c] *= corr;
     }
@@ -260,11 +265,11 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(pbuf + lane * 2), "h"(__half_as_ushort(__float2half_rn(p))) : "memory");
     __syncwarp();
   };
-  // V phase: slot i holds token i ^ lane. Slots 4k..4k+3 hold tokens
-  // 4(k ^ (lane >> 2)) + (r ^ (lane & 3)), so one 8-byte broadcast read of pbuf serves
-  // four slots and a PRMT (per-lane selector of half r ^ (lane & 3)) makes each slot's
-  // (p, p) pair: 8 LDS instead of 32 shuffles per batch — the MIO pipe (shared loads
-  // and shuffles) is what bounds this kernel.
+  // V phase: slot i holds token 16 hh + (i ^ ll). Slots 4k..4k+3 hold tokens
+  // 16 hh + 4(k ^ (ll >> 2)) + (r ^ (ll & 3)), so one 8-byte broadcast read of pbuf
+  // serves four slots and a PRMT (per-lane selector of half r ^ (ll & 3)) makes each
+  // slot's (p, p) pair: 4 LDS instead of 16 shuffles per batch — the MIO pipe (shared
+  // loads and shuffles) is what bounds this kernel.
   // p * V accumulates in packed fp16x2 windows of 8 tokens (HFMA2, full rate; the
   // mixed-precision fp32 FMA is quarter rate), flushed into the fp32 accumulators
   // with an exact widening FMA — the GEMV's windowing, at attention's 2e-3 bound.
@@ -274,15 +279,15 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     const uint32_t h2 = 2u * (uint32_t)(r ^ (lane & 3));
     psel[r] = h2 | ((h2 + 1) << 4) | (h2 << 8) | ((h2 + 1) << 12);
   }
-  const uint32_t pb_lane = pbuf + (uint32_t)(lane >> 2) * 8;  // pbuf is 64-byte aligned
+  const uint32_t pb_lane = pbuf + (uint32_t)hh * 32 + (uint32_t)(ll >> 2) * 8;  // pbuf is 64-byte aligned
   auto vphase = [&](const uint4 (&vc)[Q]) {
     constexpr int HW = V / 2;  // fp16x2 words per entry
     uint2 pv = make_uint2(0u, 0u);
 #pragma unroll
-    for (int w8 = 0; w8 < 4; ++w8) {
-      uint32_t hw[GPL][HW];
+    for (int w8 = 0; w8 < 2; ++w8) {
+      uint32_t hw[GPH][HW];
 #pragma unroll
-      for (int j = 0; j < GPL; ++j)
+      for (int j = 0; j < GPH; ++j)
 #pragma unroll
         for (int c = 0; c < HW; ++c) hw[j][c] = 0u;
 #pragma unroll
@@ -291,8 +296,8 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
         if ((i & 3) == 0) pv = lds64(pb_lane ^ (uint32_t)((i >> 2) * 8));
         const uint32_t pp = prmt(pv.x, pv.y, psel[i & 3]);
 #pragma unroll
-        for (int j = 0; j < GPL; ++j) {
-          const int byte = i * GPL + j;
+        for (int j = 0; j < GPH; ++j) {
+          const int byte = i * GPH + j;
           const uint32_t w = (&vc[byte / 16].x)[(byte % 16) / 4];
           const uint32_t addr = row_addr<G * EPB, PRMT>(w, byte % 4, cbV[j], colV[j], vbook_base);
           if constexpr (V == 2) {
@@ -306,7 +311,7 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
         }
       }
 #pragma unroll
-      for (int j = 0; j < GPL; ++j)
+      for (int j = 0; j < GPH; ++j)
 #pragma unroll
         for (int c = 0; c < HW; ++c) {
           acc[j][2 * c] = fma_h((uint16_t)(hw[j][c] & 0xffff), (uint16_t)0x3C00, acc[j][2 * c]);
@@ -533,11 +538,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
         }
         const uint8_t* bk = is_k ? reinterpret_cast<const uint8_t*>(lut_s) : vbook_s;
         const int code = cq_nearest_team<4>(bk + gg * 4, G * 4, p[0], p[1], split);
-        if (split == 0) {
-          const int l = gg & 31, jj = gg >> 5, slot = (pos & 31) ^ l, byte = slot * GPL + jj;
-          const int64_t off = (int64_t)bh * a.T_cap * G + (int64_t)(pos >> 5) * 32 * G + ((byte >> 4) * 32 + l) * 16 + (byte & 15);
-          (is_k ? a.kc_w : a.vc_w)[off] = (uint8_t)code;
-        }
+        if (split == 0) (is_k ? a.kc_w : a.vc_w)[(int64_t)bh * a.T_cap * G + kvil_offset(pos, gg, G)] = (uint8_t)code;
         __syncthreads();  // the codes are in global memory before any warp loads that batch
       }
       uint32_t* lw = reinterpret_cast<uint32_t*>(lut_s);
@@ -604,9 +605,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     }
     ph.mark(a, 0);
     float m_w = -INFINITY, l_lane = 0.f;
-    float acc[GPL][V];
+    float acc[2 * GPL][V];  // lane (h, ll): groups ll + 16 (j ^ h), j < 2 GPL
 #pragma unroll
-    for (int j = 0; j < GPL; ++j)
+    for (int j = 0; j < 2 * GPL; ++j)
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
     uint4 ka[2 * GPL], va[2 * GPL];
@@ -629,10 +630,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       my[0] = m_w;
       my[1] = l_w;
     }
+    // the two half-warps hold the same groups for different tokens: lane ll of the
+    // first half adds its partner's (ll + 16) sums for group ll + 16 j
 #pragma unroll
-    for (int j = 0; j < GPL; ++j)
+    for (int j = 0; j < 2 * GPL; ++j)
 #pragma unroll
-      for (int i = 0; i < V; ++i) my[2 + (lane + 32 * j) * V + i] = acc[j][i];
+      for (int i = 0; i < V; ++i) {
+        const float tot = acc[j][i] + __shfl_xor_sync(0xffffffffu, acc[j ^ 1][i], 16);
+        if (lane < 16) my[2 + (lane + 16 * j) * V + i] = tot;
+      }
     __syncthreads();
     // every warp is done with the LUT and the V book: fetch the next span's books now,
     // so the copy overlaps this span's merge

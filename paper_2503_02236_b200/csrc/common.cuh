@@ -100,6 +100,21 @@ __device__ __forceinline__ int region_of(const Geom& g, int64_t s) {
   return (int)((local_row / g.tile_rows) * n_tc + col / g.tile_cols);
 }
 
+// KV_IL inside one (b, h) block (G = C/v groups, 32 or 64), per 32-token batch:
+// [G/16 words][32 lanes][16 bytes]. Half-warp h = lane >> 4 holds tokens 16h..16h+15;
+// lane (h, ll = lane & 15) owns groups ll + 16 (j ^ h), j < G/16, and stores token
+// 16h + (i ^ ll) at slot i (0..15), byte i * (G/16) + j. The XOR orders make the
+// attention kernel's cross-lane logit reduction select-free (4 shuffle levels inside
+// each half-warp), and the (j ^ h) swap puts the two halves of every shared load on
+// distinct banks.
+__host__ __device__ __forceinline__ int64_t kvil_offset(int64_t t, int grp, int G) {
+  const int gph = G / 16;
+  const int h = (int)(t & 31) >> 4, ll = grp & 15, j = (grp >> 4) ^ h;
+  const int lane = h * 16 + ll, slot = (int)(t & 15) ^ ll;
+  const int byte = slot * gph + j;
+  return (t >> 5) * 32 * (int64_t)G + ((byte >> 4) * 32 + lane) * 16 + (byte & 15);
+}
+
 // Offset (in codes) of code (level r, sub-vector s) inside an interleaved layout.
 __device__ __forceinline__ int64_t il_offset(const Geom& g, int r, int64_t s) {
   if (g.layout == VQB_LAYOUT_GEMV_IL) {
@@ -112,17 +127,10 @@ __device__ __forceinline__ int64_t il_offset(const Geom& g, int r, int64_t s) {
     const int64_t wb = min(gcb, g.gpr - cb * gcb);
     return (int64_t)r * g.S + cb * gcb * g.rows + ((m / rpl) * wb + gi) * rpl + (m % rpl);
   }
-  // KV_IL: per (b,h), per 32-token batch: [Q = 2*GPL][32 lanes][16 bytes]; lane l owns
-  // groups l + 32j and stores token (i ^ l) of the batch at slot i, byte i*GPL + j
-  // (the XOR order makes the attention kernel's cross-lane logit reduction select-free).
   const int64_t T = g.d_T;
-  const int gpl = (int)(g.gpr / 32);
   const int64_t row = s / g.gpr, grp = s - (s / g.gpr) * g.gpr;
   const int64_t bh = row / T, t = row - (row / T) * T;
-  const int lane = (int)(grp % 32), j = (int)(grp / 32);
-  const int slot = (int)(t % 32) ^ lane;
-  const int byte = slot * gpl + j;
-  return (int64_t)r * g.S + bh * T * g.gpr + (t / 32) * 32 * g.gpr + ((byte / 16) * 32 + lane) * 16 + (byte % 16);
+  return (int64_t)r * g.S + bh * T * g.gpr + kvil_offset(t, (int)grp, (int)g.gpr);
 }
 
 // Code of level r for sub-vector s, from any layout.
