@@ -79,8 +79,8 @@ extern "C" {
  * KV_IL    : KV-cache codes interleaved for the decode-attention kernel (u8 codes,
  *            G = C/v in {32, 64}), per level and per (b, h) row block of T tokens,
  *            per 32-token batch: [G/16 words][32 lanes][16 bytes]. Lane (h, ll) =
- *            (lane >> 4, lane & 15) owns groups ll + 16*(j ^ h), j < G/16, and stores
- *            token 16h + (i ^ ll) at slot i (0..15), byte i*(G/16) + j.
+ *            (lane / 8, lane % 8) owns groups ll + 8*(j ^ h), j < G/8, and stores
+ *            token 8h + (i ^ ll) at slot i (0..7), byte i*(G/8) + j.
  * PLAIN    : the reference `codes` array (R, S) level-major in the narrowest unsigned
  *            type: u8 when log2_entries <= 8, else u16.
  */

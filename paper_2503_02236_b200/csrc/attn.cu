@@ -15,16 +15,16 @@
 //  * K side as a lookup table: q is fixed per (b, h), so the CTA builds
 //    LUT[e][g] = log2(e)/sqrt(C) * <q_g, K_book_g[e]> once per (b, h); a token's
 //    logit is sum_g LUT[code_g][g]: one LDS.32 + FADD per code, no dequantise.
-//  * bank-conflict-free by construction: lane (h, ll) = (lane >> 4, lane & 15) owns
-//    channel groups g = ll + 16 (j ^ h); the LUT and the V book are stored
+//  * bank-conflict-free by construction: lane (h, ll) = (lane / 8, lane % 8) owns
+//    channel groups g = ll + 8 (j ^ h); the LUT and the V book are stored
 //    [entry][group], so in every shared load the 32 lanes hit 32 distinct banks
 //    (g mod 32) whatever their codes are. With a 256-byte row the shared address is
 //    a single PRMT of the code byte and the lane's column (plus the region base).
-//  * select-free logit reduction: in the KV_IL layout a half-warp spans a token's
-//    groups and lane (h, ll) stores token 16h + (i ^ ll) in slot i, so the 16x16
-//    transpose-reduction inside each half-warp is 15 shuffle+add pairs with no
-//    selects, leaving lane l with token l's logit (16 fewer shuffles per 32 tokens
-//    than spanning the groups over the whole warp).
+//  * select-free logit reduction: in the KV_IL layout a set of 8 lanes spans a token's
+//    groups and lane (h, ll) stores token 8h + (i ^ ll) in slot i, so the 8x8
+//    transpose-reduction inside each set is 7 shuffle+add pairs with no selects,
+//    leaving lane l with token l's logit (24 fewer shuffles per 32 tokens than
+//    spanning the groups over the whole warp).
 //  * online softmax (flash-decode) in the exp2 domain; V is dequantised in
 //    registers and fused into fp32 accumulators with fma.rn.f32.f16.
 //  * the next 32-token batch's K codes load during the V phase, its V codes during
@@ -183,14 +183,17 @@ __device__ __forceinline__ void attn_load_batch(const AttnArgs& a, int bh, int t
 template <int V, int GPL, bool PRMT, bool APPEND>
 __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int bh, int tok0, int tok1, uint32_t lut_base,
                                                  uint32_t vbook_base, float& m_w, float& l_lane,
-                                                 float (&acc)[2 * GPL][V], uint4 (&ka)[2 * GPL],
+                                                 float (&acc)[32 * GPL / kKvLanes][V], uint4 (&ka)[2 * GPL],
                                                  uint4 (&va)[2 * GPL], int fresh_t0, uint32_t pbuf) {
   using SM = AttnSmem<V, GPL>;
   constexpr int G = SM::G, EPB = SM::EPB;
   constexpr int Q = 2 * GPL;    // 16-byte loads per lane per 32-token batch
-  constexpr int GPH = 2 * GPL;  // groups per lane (KV_IL: a half-warp spans the G groups)
+  constexpr int LPT = kKvLanes;  // lanes spanning one token's G groups (KV_IL)
+  constexpr int NS = LPT;        // slots (tokens) per lane per 32-token batch
+  constexpr int GPH = G / LPT;   // groups per lane
+  static_assert(GPH * 32 / LPT >= 32 / LPT && (GPH & (GPH - 1)) == 0 && GPH >= 32 / LPT, "KV_IL lane sets");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int hh = lane >> 4, ll = lane & 15;
+  const int hh = lane / LPT, ll = lane % LPT;
   const int64_t TG = (int64_t)a.T_cap * G;
   const uint8_t* kbase = a.kc + (int64_t)bh * TG;
   const uint8_t* vbase = a.vc + (int64_t)bh * TG;
@@ -198,8 +201,8 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
   uint32_t colK[GPH], colV[GPH], cbK[GPH], cbV[GPH];
 #pragma unroll
   for (int j = 0; j < GPH; ++j) {
-    colK[j] = (uint32_t)(ll + 16 * (j ^ hh)) * 4;
-    colV[j] = (uint32_t)(ll + 16 * (j ^ hh)) * EPB;
+    colK[j] = (uint32_t)(ll + LPT * (j ^ hh)) * 4;
+    colV[j] = (uint32_t)(ll + LPT * (j ^ hh)) * EPB;
     cbK[j] = (lut_base & 0xffff0000u) | colK[j];
     cbV[j] = (vbook_base & 0xffff0000u) | colV[j];
   }
@@ -216,7 +219,7 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
   // K phase + online-softmax update of one 32-token batch; lane l stores token l's
   // probability (fp16) in the warp's pbuf for the V phase
   auto kphase = [&](const uint4 (&kc)[Q], int tb) {
-    // lane partial logits for its 16 slots (slot i = token 16 hh + (i ^ ll))
+    // lane partial logits for its NS slots (slot i = token LPT hh + (i ^ ll))
     auto partial = [&](int i) {
       float acc_s = 0.f;
 #pragma unroll
@@ -228,17 +231,17 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
       }
       return acc_s;
     };
-    // select-free transpose-reduction inside each half-warp: afterwards s[0] on lane l
-    // is token l's logit. The first (offset 8) step is fused into the partial
-    // computation so only 8 partial logits are ever live; 15 shuffles per batch.
-    float s[8];
+    // select-free transpose-reduction inside each lane set: afterwards s[0] on lane l
+    // is token l's logit. The first (offset NS/2) step is fused into the partial
+    // computation so only NS/2 partial logits are ever live; NS-1 shuffles per batch.
+    float s[NS / 2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float lo = partial(i), hi = partial(i + 8);
-      s[i] = lo + __shfl_xor_sync(0xffffffffu, hi, 8);
+    for (int i = 0; i < NS / 2; ++i) {
+      const float lo = partial(i), hi = partial(i + NS / 2);
+      s[i] = lo + __shfl_xor_sync(0xffffffffu, hi, NS / 2);
     }
 #pragma unroll
-    for (int off = 4; off >= 1; off >>= 1)
+    for (int off = NS / 4; off >= 1; off >>= 1)
 #pragma unroll
       for (int i = 0; i < off; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i + off], off);
     // tokens past the valid length (a partial last batch) get p = 0
@@ -265,11 +268,11 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(pbuf + lane * 2), "h"(__half_as_ushort(__float2half_rn(p))) : "memory");
     __syncwarp();
   };
-  // V phase: slot i holds token 16 hh + (i ^ ll). Slots 4k..4k+3 hold tokens
-  // 16 hh + 4(k ^ (ll >> 2)) + (r ^ (ll & 3)), so one 8-byte broadcast read of pbuf
+  // V phase: slot i holds token LPT hh + (i ^ ll). Slots 4k..4k+3 hold tokens
+  // LPT hh + 4(k ^ (ll >> 2)) + (r ^ (ll & 3)), so one 8-byte broadcast read of pbuf
   // serves four slots and a PRMT (per-lane selector of half r ^ (ll & 3)) makes each
-  // slot's (p, p) pair: 4 LDS instead of 16 shuffles per batch — the MIO pipe (shared
-  // loads and shuffles) is what bounds this kernel.
+  // slot's (p, p) pair: NS/4 LDS instead of NS shuffles per batch — the MIO pipe
+  // (shared loads and shuffles) is what bounds this kernel.
   // p * V accumulates in packed fp16x2 windows of 8 tokens (HFMA2, full rate; the
   // mixed-precision fp32 FMA is quarter rate), flushed into the fp32 accumulators
   // with an exact widening FMA — the GEMV's windowing, at attention's 2e-3 bound.
@@ -279,12 +282,12 @@ __device__ __forceinline__ void attn_stream_span(const AttnArgs& a, int T, int b
     const uint32_t h2 = 2u * (uint32_t)(r ^ (lane & 3));
     psel[r] = h2 | ((h2 + 1) << 4) | (h2 << 8) | ((h2 + 1) << 12);
   }
-  const uint32_t pb_lane = pbuf + (uint32_t)hh * 32 + (uint32_t)(ll >> 2) * 8;  // pbuf is 64-byte aligned
+  const uint32_t pb_lane = pbuf + (uint32_t)hh * (2 * LPT) + (uint32_t)(ll >> 2) * 8;  // pbuf is 64-byte aligned
   auto vphase = [&](const uint4 (&vc)[Q]) {
     constexpr int HW = V / 2;  // fp16x2 words per entry
     uint2 pv = make_uint2(0u, 0u);
 #pragma unroll
-    for (int w8 = 0; w8 < 2; ++w8) {
+    for (int w8 = 0; w8 < NS / 8; ++w8) {
       uint32_t hw[GPH][HW];
 #pragma unroll
       for (int j = 0; j < GPH; ++j)
@@ -605,9 +608,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
     }
     ph.mark(a, 0);
     float m_w = -INFINITY, l_lane = 0.f;
-    float acc[2 * GPL][V];  // lane (h, ll): groups ll + 16 (j ^ h), j < 2 GPL
+    constexpr int GPH = G / kKvLanes;
+    float acc[GPH][V];  // lane (h, ll): groups ll + kKvLanes (j ^ h), j < GPH
 #pragma unroll
-    for (int j = 0; j < 2 * GPL; ++j)
+    for (int j = 0; j < GPH; ++j)
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
     uint4 ka[2 * GPL], va[2 * GPL];
@@ -630,15 +634,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
       my[0] = m_w;
       my[1] = l_w;
     }
-    // the two half-warps hold the same groups for different tokens: lane ll of the
-    // first half adds its partner's (ll + 16) sums for group ll + 16 j
+    // the lane sets hold the same groups for different tokens: a butterfly over the
+    // sets (set h's slot j is group ll + kKvLanes (j ^ h)) leaves set 0 with the sums
 #pragma unroll
-    for (int j = 0; j < 2 * GPL; ++j)
+    for (int o = kKvLanes; o < 32; o <<= 1) {
+      float nx[GPH][V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const float tot = acc[j][i] + __shfl_xor_sync(0xffffffffu, acc[j ^ 1][i], 16);
-        if (lane < 16) my[2 + (lane + 16 * j) * V + i] = tot;
-      }
+      for (int j = 0; j < GPH; ++j)
+#pragma unroll
+        for (int i = 0; i < V; ++i) nx[j][i] = acc[j][i] + __shfl_xor_sync(0xffffffffu, acc[j ^ (o / kKvLanes)][i], o);
+#pragma unroll
+      for (int j = 0; j < GPH; ++j)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[j][i] = nx[j][i];
+    }
+    if (lane < kKvLanes)
+#pragma unroll
+      for (int j = 0; j < GPH; ++j)
+#pragma unroll
+        for (int i = 0; i < V; ++i) my[2 + (lane + kKvLanes * j) * V + i] = acc[j][i];
     __syncthreads();
     // every warp is done with the LUT and the V book: fetch the next span's books now,
     // so the copy overlaps this span's merge

@@ -101,16 +101,18 @@ __device__ __forceinline__ int region_of(const Geom& g, int64_t s) {
 }
 
 // KV_IL inside one (b, h) block (G = C/v groups, 32 or 64), per 32-token batch:
-// [G/16 words][32 lanes][16 bytes]. Half-warp h = lane >> 4 holds tokens 16h..16h+15;
-// lane (h, ll = lane & 15) owns groups ll + 16 (j ^ h), j < G/16, and stores token
-// 16h + (i ^ ll) at slot i (0..15), byte i * (G/16) + j. The XOR orders make the
-// attention kernel's cross-lane logit reduction select-free (4 shuffle levels inside
-// each half-warp), and the (j ^ h) swap puts the two halves of every shared load on
+// [G/16 words][32 lanes][16 bytes]. The warp is cut into 32/kKvLanes lane sets; set h
+// = lane / kKvLanes holds tokens kKvLanes*h + (0..kKvLanes-1), and lane (h, ll = lane %
+// kKvLanes) owns groups ll + kKvLanes*(j ^ h), j < G/kKvLanes, storing token
+// kKvLanes*h + (i ^ ll) at slot i, byte i*(G/kKvLanes) + j. The XOR orders make the
+// attention kernel's cross-lane logit reduction select-free (log2(kKvLanes) shuffle
+// levels inside each set), and the (j ^ h) swap puts the sets of every shared load on
 // distinct banks.
+constexpr int kKvLanes = 8;
 __host__ __device__ __forceinline__ int64_t kvil_offset(int64_t t, int grp, int G) {
-  const int gph = G / 16;
-  const int h = (int)(t & 31) >> 4, ll = grp & 15, j = (grp >> 4) ^ h;
-  const int lane = h * 16 + ll, slot = (int)(t & 15) ^ ll;
+  const int gph = G / kKvLanes;
+  const int h = (int)(t & 31) / kKvLanes, ll = grp % kKvLanes, j = (grp / kKvLanes) ^ h;
+  const int lane = h * kKvLanes + ll, slot = (int)(t % kKvLanes) ^ ll;
   const int byte = slot * gph + j;
   return (t >> 5) * 32 * (int64_t)G + ((byte >> 4) * 32 + lane) * 16 + (byte & 15);
 }

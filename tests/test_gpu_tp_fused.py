@@ -12,7 +12,6 @@ its outputs into both ranks' slots and the finish kernel reduces / gathers them.
 """
 
 import os
-import socket
 
 import pytest
 
@@ -21,15 +20,14 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
+def _init_file():
+    # file rendezvous: no TCP port to race for between tests (a freed port can be
+    # taken again before the workers bind it)
+    import tempfile
+    return os.path.join(tempfile.mkdtemp(prefix="vqb_tp_"), "rendezvous")
 
 
-def _worker(rank, world, port, results):
+def _worker(rank, world, init_file, results):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for p in (root, os.path.join(root, "tests"), os.path.join(root, "tests", "golden")):
@@ -38,9 +36,7 @@ def _worker(rank, world, port, results):
     import torch
     import torch.distributed as dist
     from conftest import Case, O
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank, world_size=world)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     from paper_2503_02236_b200 import _native as N
@@ -97,11 +93,11 @@ def _worker(rank, world, port, results):
 
 def test_fused_peer_memory_collectives_world2():
     import torch.multiprocessing as mp
-    port = _free_port()
+    init_file = _init_file()
     ctx = mp.get_context("spawn")
     with ctx.Manager() as mgr:
         results = mgr.dict()
-        mp.spawn(_worker, args=(2, port, results), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, init_file, results), nprocs=2, join=True)
         res = dict(results)
     assert res, "rank 0 reported nothing"
     for key, (err, kern) in res.items():
