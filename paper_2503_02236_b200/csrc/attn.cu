@@ -713,13 +713,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
               wa[j] = ld_relaxed_u64(sp + 2 + tid);
             }
           }
+          for (;;) {  // re-poll every pending word per round (one L2 round trip per round)
+            bool pending = false;
+#pragma unroll
+            for (int j = 0; j < PF; ++j) pending |= ((wm[j] >> 32) == 0) | ((wl[j] >> 32) == 0) | ((wa[j] >> 32) == 0);
+            if (!pending) break;
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+              const unsigned long long* sp = slots + (int64_t)(blockIdx.x + 1 + j0 + j) * (C + 2);
+              if ((wm[j] >> 32) == 0) wm[j] = ld_relaxed_u64(sp);
+              if ((wl[j] >> 32) == 0) wl[j] = ld_relaxed_u64(sp + 1);
+              if ((wa[j] >> 32) == 0) wa[j] = ld_relaxed_u64(sp + 2 + tid);
+            }
+          }
 #pragma unroll
           for (int j = 0; j < PF; ++j) {
             if (j0 + j < n_later) {
               unsigned long long* sp = slots + (int64_t)(blockIdx.x + 1 + j0 + j) * (C + 2);
-              while ((wm[j] >> 32) == 0) wm[j] = ld_relaxed_u64(sp);
-              while ((wl[j] >> 32) == 0) wl[j] = ld_relaxed_u64(sp + 1);
-              while ((wa[j] >> 32) == 0) wa[j] = ld_relaxed_u64(sp + 2 + tid);
               const float mj = __uint_as_float((uint32_t)wm[j]);
               const float Mn = fmaxf(Mr, mj);
               const float s0 = fast_exp2(Mr - Mn);

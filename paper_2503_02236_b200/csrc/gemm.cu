@@ -396,19 +396,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 // (remote mbarrier arrive through mapa); tcgen05.commit multicasts "empty" and the
 // final "TMEM full" to both CTAs.
 
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
-  uint32_t d;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(addr), "r"(rank));
-  return d;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 // Remote arrive on the leader's barrier. Default (.release.cta) semantics like
 // CUTLASS's 2-SM transform pipeline: the data is consumed by the pair's tensor core
 // (async proxy), ordered by the preceding fence.proxy.async; a .release.cluster arrive

@@ -892,9 +892,20 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
                 pp[j] = a.part + ((int64_t)(blockIdx.x + 1 + j0 + j) * B + b) * COLS + col;
                 pv[j] = (j0 + j < n_later) ? ld_relaxed_u64(pp[j]) : (1ull << 32);
               }
+              // re-poll every pending slot per round: one L2 round trip per round, not
+              // one per slot (the publishers finish together, so a slot-by-slot wait
+              // serialised up to PF round trips into the launch's tail)
+              for (;;) {
+                bool pending = false;
+#pragma unroll
+                for (int j = 0; j < PF; ++j) pending |= (pv[j] >> 32) == 0;
+                if (!pending) break;
+#pragma unroll
+                for (int j = 0; j < PF; ++j)
+                  if ((pv[j] >> 32) == 0) pv[j] = ld_relaxed_u64(pp[j]);
+              }
 #pragma unroll
               for (int j = 0; j < PF; ++j) {
-                while ((pv[j] >> 32) == 0) pv[j] = ld_relaxed_u64(pp[j]);
                 if (j0 + j < n_later) {
                   sum += __uint_as_float((uint32_t)pv[j]);
                   st_relaxed_u64(pp[j], 0ull);
