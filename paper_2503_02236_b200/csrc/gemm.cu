@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(kGtThreads, 1)
         const int64_t off = (int64_t)cb * 32 * (a.M / RPL) * 16 + (int64_t)ch * (GK / RPL) * 512;
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          tma_load_1d(smem_u32(sc + (c * R + r) * CODEB), a.codes + r * a.level_bytes + off, CODEB, cfull0 + 8 * c);
+          tma_load_1d_hint(smem_u32(sc + (c * R + r) * CODEB), a.codes + r * a.level_bytes + off, CODEB, cfull0 + 8 * c, l2_evict_first());
       }
     } else if (lane == 1) {
       pdl_wait();

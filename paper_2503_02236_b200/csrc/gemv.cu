@@ -399,8 +399,8 @@ __device__ __forceinline__ void gemv_fast_body(const GemvFastArgs& a, const Gemv
     const int64_t off = (int64_t)cb * GC * (fc.M / RPL) * 16 + (int64_t)chunk * (CR / RPL) * rgb;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      tma_load_1d(smem_u32(stages + s * STG + r * LEVB), fc.codes + r * fc.level_bytes + off,
-                  (uint32_t)((rows / RPL) * rgb), full0 + 8 * s);
+      tma_load_1d_hint(smem_u32(stages + s * STG + r * LEVB), fc.codes + r * fc.level_bytes + off,
+                  (uint32_t)((rows / RPL) * rgb), full0 + 8 * s, l2_evict_first());
   };
   auto issue_x = [&](ProbCursor& c, int idx) {
     if constexpr (XF) return;  // x is resident in shared memory
