@@ -30,6 +30,7 @@ FLAG_GEMM_FUSED = 512  # GEMM: fused producers at prefill sizes
 FLAG_GEMM_TWO_PHASE = 1024  # GEMM: dequantise to an fp16 scratch, then the dense pair GEMM
 FLAG_GEMV_TC = 2048  # GEMV: the tcgen05 decode GEMV below its default batch range
 FLAG_NO_GEMV_TC = 4096  # GEMV: never the tcgen05 decode GEMV
+FLAG_NO_COLSPLIT = 8192  # GEMV batch 1: stream-K instead of the column-split kernel
 
 _ERRORS = {
     ESHAPE: ShapeError,

@@ -1199,6 +1199,9 @@ static GemvKernel fast_kernel_for(const FastPlan& p, int rows) {
   return nullptr;
 }
 
+int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
+                     const VqbLaunch* L, cudaStream_t st);
+
 int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void* y, int y_dtype,
                   const VqbLaunch* L, void* ws, size_t ws_bytes, cudaStream_t st, bool* used_fast,
                   const VqbPeerComm* tp, int tp_mode, const GemvXf* xf) {
@@ -1215,6 +1218,12 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     if (t <= 0) {
       if (used_fast && t == 0) *used_fast = true;
       return t;
+    }
+    // batch 1, 16 x 256-column outputs: the column-split kernel (csrc/gemv_cs.cu)
+    const int c = gemv_cs_dispatch(g, w, x, x_dtype, rows, y, y_dtype, L, st);
+    if (c <= 0) {
+      if (used_fast && c == 0) *used_fast = true;
+      return c;
     }
   }
   FastPlan p = plan_fast(g, w, rows, x_dtype, L);

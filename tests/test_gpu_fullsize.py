@@ -57,7 +57,7 @@ def test_full_size_gemv(label, shape, v, bits, r, sharing, work, dev):
     g = torch.Generator(device=dev).manual_seed(1)
     x = torch.randn((1, shape[0]), generator=g, device=dev).half()
     y = ops.vq_gemv(w, x, out_dtype=torch.float32)
-    assert N.last_kernel() == "gemv_fast"
+    assert N.last_kernel() in ("gemv_fast", "gemv_cs")  # column-split for 16-block outputs
     ref = x.float() @ dense
     assert _rel(y, ref) <= 1e-3, label
     # determinism of the split reduction and linearity in the activation

@@ -58,7 +58,9 @@ def test_full_size_gemv_vs_c_oracle(label, shape, v, bits, r, sharing, work, row
     w, codes, books, nreg, regions = _weight(dev, shape, v, bits, r, sharing, work)
     x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))
     y = ops.vq_gemv(w, torch.from_numpy(x).to(dev).half(), out_dtype=torch.float32)
-    want = "gemv_fast" if rows <= 4 or (rows <= 8 and sharing != "whole") else "gemv_tc" if sharing == "whole" else "gemv_generic"
+    colsplit = rows == 1 and sharing == "whole" and r == 1 and 111 <= shape[1] // 256 * 8 <= 148
+    want = ("gemv_cs" if colsplit else "gemv_fast") if rows <= 4 or (rows <= 8 and sharing != "whole") \
+        else "gemv_tc" if sharing == "whole" else "gemv_generic"
     assert N.last_kernel() == want, label
     ref = CO.gemv(codes, books, shape, v, nreg, regions, x)
     assert _rel(y, ref) <= 1e-3, label

@@ -155,8 +155,8 @@ def test_gemv_fast_kernel(label, shape, v, bits, r, sharing, tile, work, rows, d
     assert d.layout == "gemv"
     x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))
     L = ops.launch_struct()
-    L.flags |= N.FLAG_NO_GEMV_TC  # this kernel family (batch 8 defaults to the tcgen05 GEMV)
-    y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half(), launch=L)
+    L.flags |= N.FLAG_NO_GEMV_TC | N.FLAG_NO_COLSPLIT  # this kernel family (batch 8 defaults to the
+    y = ops.vq_gemv(d, torch.from_numpy(x).to(dev).half(), launch=L)  # tcgen05 GEMV, batch 1 at N = 4096
     assert N.last_kernel() == "gemv_fast"
     ref = O.matmul_ref(x, dense)
     assert O.rel_err(y.cpu().numpy(), ref) <= TOL_F16
