@@ -29,17 +29,18 @@ constexpr int kCsRep = 8;                     // codebook replicas (16-byte entr
 struct GemvCsArgs {
   const uint8_t* codes;  // GEMV_IL, u16 codes, one level
   const __half* books;   // (K, 8) fp16, entries [0, n_sh) used
-  const __half* x;       // (M,)
+  const __half* x;       // (B, M)
   void* y;
   int y_dtype;
   int M, N, n_sh;
 };
 
+template <int B>
 __global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* books_s = smem;                                            // n_sh x 128 B
-  __half* x_s = reinterpret_cast<__half*>(smem + 256 * 128);          // M halves
-  float* red = reinterpret_cast<float*>(smem + 256 * 128 + ((a.M * 2 + 15) & ~15));  // warps x 32
+  __half* x_s = reinterpret_cast<__half*>(smem + 256 * 128);          // B x M halves
+  float* red = reinterpret_cast<float*>(smem + 256 * 128 + ((B * a.M * 2 + 15) & ~15));  // warps x B x 32
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gl = lane % kCsGroups, rl = lane / kCsGroups;
@@ -69,15 +70,17 @@ __global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
       *reinterpret_cast<uint4*>(books_s + (size_t)e * 128 + ((r + e) % kCsRep) * 16) = q;
   }
   pdl_wait();  // x comes from the previous kernel
-  for (int i = tid; i < a.M / 8; i += kCsThreads)
+  for (int i = tid; i < B * a.M / 8; i += kCsThreads)
     reinterpret_cast<uint4*>(x_s)[i] = __ldg(reinterpret_cast<const uint4*>(a.x) + i);
   __syncthreads();
 
   const uint32_t bk = smem_u32(books_s) + (uint32_t)(lane % kCsRep) * 16;
   const uint32_t xb = smem_u32(x_s);
-  float acc[8];
+  float acc[B][8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
   for (int k0 = 0; k0 < n_mine; k0 += kCsDepth) {
 #pragma unroll
     for (int d = 0; d < kCsDepth; ++d) {
@@ -86,8 +89,14 @@ __global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
         const uint4 w = cw[d];
         if (k + kCsDepth < n_mine) cw[d] = ldg_stream_hint(base + (int64_t)(first + (k + kCsDepth) * stride) * 512, pol);
         const int rg = first + k * stride;
-        const uint4 xv = lds128(xb + (uint32_t)rg * 16);  // x rows 8rg .. 8rg+7
-        uint32_t hw[4] = {0u, 0u, 0u, 0u};
+        uint4 xv[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) xv[b] = lds128(xb + (uint32_t)(b * a.M * 2) + (uint32_t)rg * 16);  // rows 8rg..+7
+        uint32_t hw[B][4];
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) hw[b][j] = 0u;
 #pragma unroll
         for (int kr = 0; kr < 8; ++kr) {
           const uint32_t ww = (&w.x)[kr / 2];
@@ -95,16 +104,21 @@ __global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
           // every slot of a row holds the entry: lane l reads slot l % 8, so each
           // quarter-warp's eight 16-byte reads hit eight distinct bank groups
           const uint4 q = lds128(bk + code * 128);
-          const uint32_t xw = (&xv.x)[kr / 2];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            hw[j] = (kr & 1) ? hfma2_bcast<1>((&q.x)[j], xw, hw[j]) : hfma2_bcast<0>((&q.x)[j], xw, hw[j]);
+          for (int b = 0; b < B; ++b) {
+            const uint32_t xw = (&xv[b].x)[kr / 2];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              hw[b][j] = (kr & 1) ? hfma2_bcast<1>((&q.x)[j], xw, hw[b][j]) : hfma2_bcast<0>((&q.x)[j], xw, hw[b][j]);
+          }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {  // flush the 8-row window (exact widening)
-          acc[2 * j] = fma_h((uint16_t)(hw[j] & 0xffff), (uint16_t)0x3C00, acc[2 * j]);
-          acc[2 * j + 1] = fma_h((uint16_t)(hw[j] >> 16), (uint16_t)0x3C00, acc[2 * j + 1]);
-        }
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // flush the 8-row window (exact widening)
+            acc[b][2 * j] = fma_h((uint16_t)(hw[b][j] & 0xffff), (uint16_t)0x3C00, acc[b][2 * j]);
+            acc[b][2 * j + 1] = fma_h((uint16_t)(hw[b][j] >> 16), (uint16_t)0x3C00, acc[b][2 * j + 1]);
+          }
       }
     }
   }
@@ -112,16 +126,21 @@ __global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
 #pragma unroll
   for (int o = kCsGroups; o < 32; o <<= 1)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[b][j] += __shfl_xor_sync(0xffffffffu, acc[b][j], o);
   if (rl == 0)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) red[warp * 32 + gl * 8 + j] = acc[j];
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) red[(warp * B + b) * 32 + gl * 8 + j] = acc[b][j];
   __syncthreads();
-  if (tid < kCsGroups * 8) {
+  if (tid < B * kCsGroups * 8) {
+    const int b = tid / 32, c = tid % 32;
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kCsWarps; ++w) s += red[w * 32 + tid];
-    store_from_f32(a.y, a.y_dtype, (int64_t)cb * 256 + sl * kCsGroups * 8 + tid, s);
+    for (int w = 0; w < kCsWarps; ++w) s += red[(w * B + b) * 32 + c];
+    store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * 256 + sl * kCsGroups * 8 + c, s);
   }
 }
 
@@ -131,7 +150,7 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   if (L && (L->flags & (VQB_FLAG_FORCE_GENERIC | VQB_FLAG_NO_SHARED | VQB_FLAG_EXACT_ACCUM | VQB_FLAG_NO_COLSPLIT)))
     return 1;
   if (L && (L->split_factor > 0 || L->grid_limit > 0 || L->n_reg > 0)) return 1;  // planner-directed launches
-  if (rows != 1 || x_dtype != VQB_F16 || g.v != 8 || g.R != 1 || g.code_bytes != 2 || g.ndim != 2 ||
+  if ((rows != 1 && rows != 2 && rows != 4) || x_dtype != VQB_F16 || g.v != 8 || g.R != 1 || g.code_bytes != 2 || g.ndim != 2 ||
       g.sharing != VQB_SHARE_WHOLE || w->layout != VQB_LAYOUT_GEMV_IL || w->codebook_dtype != VQB_F16)
     return 1;
   const int n_sh = g.K <= 256 ? g.K : ((w->max_code >= 0 && w->max_code < 256) ? (int)w->max_code + 1 : -1);
@@ -150,14 +169,16 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   a.M = (int)g.rows;
   a.N = (int)g.cols;
   a.n_sh = n_sh;
-  const size_t smem = 256 * 128 + ((size_t)(g.rows * 2 + 15) & ~(size_t)15) + kCsWarps * 32 * 4;
+  const size_t smem = 256 * 128 + ((size_t)(rows * g.rows * 2 + 15) & ~(size_t)15) + (size_t)kCsWarps * rows * 32 * 4;
   if (smem > 232448) return 1;
-  static bool configured[64] = {};
+  auto kern = rows == 1 ? gemv_cs_kernel<1> : rows == 2 ? gemv_cs_kernel<2> : gemv_cs_kernel<4>;
+  static bool configured[3][64] = {};
+  const int ki = rows == 1 ? 0 : rows == 2 ? 1 : 2;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!configured[dev & 63]) {
-    VQB_CUDA_CHECK(cudaFuncSetAttribute(gemv_cs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
-    configured[dev & 63] = true;
+  if (!configured[ki][dev & 63]) {
+    VQB_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    configured[ki][dev & 63] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -167,7 +188,7 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   cudaLaunchAttribute attr[2];
   cfg.attrs = attr;
   cfg.numAttrs = persistent_attrs(attr, L ? (L->flags & ~VQB_FLAG_COOPERATIVE) : 0);
-  VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemv_cs_kernel, a));
+  VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
   set_kernel("gemv_cs");
   set_launch(grid, kCsThreads, n_sh, 0);
   return 0;

@@ -1,4 +1,4 @@
-"""Column-split batch-1 GEMV (csrc/gemv_cs.cu): every CTA owns a 32-column slice of a
+"""Column-split batch 1/2/4 GEMV (csrc/gemv_cs.cu): every CTA owns a 32-column slice of a
 256-column block for all M rows, so there is no cross-CTA split reduction. Parity
 against the C oracle (oracle/vq_oracle.c, V/codec.py:391-408 + V/sim.py:133-155) at the
 Llama-7B o / down shapes and a TP2 o shard, fp16 and fp32 outputs, a 65536-entry book
@@ -35,11 +35,12 @@ def _weight(dev, shape, entries, work, seed):
 
 @pytest.mark.parametrize("shape", [(4096, 4096), (11008, 4096), (2048, 4096)])
 @pytest.mark.parametrize("out", ["f16", "f32"])
-def test_colsplit_gemv_vs_c_oracle(shape, out, dev):
+@pytest.mark.parametrize("rows", [1, 2, 4])
+def test_colsplit_gemv_vs_c_oracle(shape, out, rows, dev):
     from paper_2503_02236_b200 import _native as N
     from paper_2503_02236_b200 import ops
     w, codes, books, = _weight(dev, shape, 65536, 256, seed=shape[0] % 97)
-    x = O.round_f16(O.synthetic_tensor((1, shape[0]), 3))
+    x = O.round_f16(O.synthetic_tensor((rows, shape[0]), 3))
     od = torch.float16 if out == "f16" else torch.float32
     y = ops.vq_gemv(w, torch.from_numpy(x).to(dev).half(), out_dtype=od)
     assert N.last_kernel() == "gemv_cs"

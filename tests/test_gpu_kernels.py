@@ -197,10 +197,10 @@ def test_gemv_cuda_core_path_at_mma_batches(label, shape, v, bits, r, sharing, t
     x = torch.from_numpy(O.round_f16(O.synthetic_tensor((rows, shape[0]), 7))).to(dev).half()
     ref = O.matmul_ref(x.float().cpu().numpy(), dense)
     L = ops.launch_struct()
-    L.flags = N.FLAG_NO_MMA | N.FLAG_NO_GEMV_TC
+    L.flags = N.FLAG_NO_MMA | N.FLAG_NO_GEMV_TC | N.FLAG_NO_COLSPLIT
     y_fma = ops.vq_gemv(d, x, launch=L)
     L2 = ops.launch_struct()
-    L2.flags = N.FLAG_NO_GEMV_TC
+    L2.flags = N.FLAG_NO_GEMV_TC | N.FLAG_NO_COLSPLIT
     y_mma = ops.vq_gemv(d, x, launch=L2)
     assert N.last_kernel() == "gemv_fast"
     assert O.rel_err(y_fma.cpu().numpy(), ref) <= TOL_F16
