@@ -19,10 +19,6 @@
 
 namespace vqb {
 
-constexpr int kCsThreads = 512;
-constexpr int kCsWarps = kCsThreads / 32;
-constexpr int kCsGroups = 4;                  // sub-vector groups (of 8 columns) per CTA
-constexpr int kCsRowLanes = 32 / kCsGroups;   // lanes along M in a warp
 constexpr int kCsDepth = 8;                   // 16-byte code words in flight per thread
 constexpr int kCsRep = 8;                     // codebook replicas (16-byte entries, 128-byte rows)
 
@@ -35,12 +31,14 @@ struct GemvCsArgs {
   int M, N, n_sh;
 };
 
-template <int B>
-__global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
+// B batch rows, SG sub-vector groups (of 8 columns) per CTA, NT threads
+template <int B, int SG, int NT>
+__global__ void __launch_bounds__(NT) gemv_cs_kernel(GemvCsArgs a) {
+  constexpr int kCsThreads = NT, kCsWarps = NT / 32, kCsGroups = SG, kCsRowLanes = 32 / SG, CPC = SG * 8;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* books_s = smem;                                            // n_sh x 128 B
   __half* x_s = reinterpret_cast<__half*>(smem + 256 * 128);          // B x M halves
-  float* red = reinterpret_cast<float*>(smem + 256 * 128 + ((B * a.M * 2 + 15) & ~15));  // warps x B x 32
+  float* red = reinterpret_cast<float*>(smem + 256 * 128 + ((B * a.M * 2 + 15) & ~15));  // warps x B x CPC
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gl = lane % kCsGroups, rl = lane / kCsGroups;
@@ -133,15 +131,20 @@ __global__ void __launch_bounds__(kCsThreads) gemv_cs_kernel(GemvCsArgs a) {
 #pragma unroll
     for (int b = 0; b < B; ++b)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) red[(warp * B + b) * 32 + gl * 8 + j] = acc[b][j];
+      for (int j = 0; j < 8; ++j) red[(warp * B + b) * CPC + gl * 8 + j] = acc[b][j];
   __syncthreads();
-  if (tid < B * kCsGroups * 8) {
-    const int b = tid / 32, c = tid % 32;
+  for (int i = tid; i < B * CPC; i += NT) {
+    const int b = i / CPC, c = i % CPC;
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kCsWarps; ++w) s += red[(w * B + b) * 32 + c];
-    store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * 256 + sl * kCsGroups * 8 + c, s);
+    for (int w = 0; w < kCsWarps; ++w) s += red[(w * B + b) * CPC + c];
+    store_from_f32(a.y, a.y_dtype, (int64_t)b * a.N + (int64_t)cb * 256 + sl * CPC + c, s);
   }
+}
+
+typedef void (*GemvCsKernel)(GemvCsArgs);
+static GemvCsKernel pick_cs(int rows) {
+  return rows == 1 ? gemv_cs_kernel<1, 4, 512> : rows == 2 ? gemv_cs_kernel<2, 4, 512> : gemv_cs_kernel<4, 4, 512>;
 }
 
 // 1 = not covered (the caller falls back to the stream-K kernels)
@@ -156,10 +159,14 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   const int n_sh = g.K <= 256 ? g.K : ((w->max_code >= 0 && w->max_code < 256) ? (int)w->max_code + 1 : -1);
   if (n_sh <= 0 || (g.cols % 256) != 0 || (g.rows % 8) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) return 1;
   const int n_cblk = (int)(g.cols / 256);
-  const int grid = n_cblk * (32 / kCsGroups);
-  // only where the stream-K kernel would split every column block several ways and
-  // the slices still fill the SMs in one wave
-  if (grid > sm_count() || grid < sm_count() * 3 / 4) return 1;
+  // one wave of n_cblk x 8 CTAs (o / down: 16 blocks). Measured: wider outputs with 8- or
+  // 16-group slices on 256-thread CTAs sharing SMs (qkv 192 CTAs, gate_up 172) are slower
+  // than the stream-K kernel (9.8 vs 8.6 us, 18.7 vs 11.5 us at batch 1).
+  const int sms = sm_count();
+  const int SG = 4;
+  if (n_cblk * 8 > sms || n_cblk * 8 < sms * 3 / 4) return 1;
+  const int NT = 512;
+  const int grid = n_cblk * (32 / SG);
   GemvCsArgs a;
   a.codes = reinterpret_cast<const uint8_t*>(w->d_codes);
   a.books = reinterpret_cast<const __half*>(w->d_codebooks);
@@ -169,11 +176,11 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   a.M = (int)g.rows;
   a.N = (int)g.cols;
   a.n_sh = n_sh;
-  const size_t smem = 256 * 128 + ((size_t)(rows * g.rows * 2 + 15) & ~(size_t)15) + (size_t)kCsWarps * rows * 32 * 4;
+  const size_t smem = 256 * 128 + ((size_t)(rows * g.rows * 2 + 15) & ~(size_t)15) + (size_t)(NT / 32) * rows * SG * 8 * 4;
   if (smem > 232448) return 1;
-  auto kern = rows == 1 ? gemv_cs_kernel<1> : rows == 2 ? gemv_cs_kernel<2> : gemv_cs_kernel<4>;
-  static bool configured[3][64] = {};
+  GemvCsKernel kern = pick_cs(rows);
   const int ki = rows == 1 ? 0 : rows == 2 ? 1 : 2;
+  static bool configured[3][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[ki][dev & 63]) {
@@ -182,7 +189,7 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kCsThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -190,7 +197,7 @@ int gemv_cs_dispatch(const Geom& g, const VqbTensor* w, const void* x, int x_dty
   cfg.numAttrs = persistent_attrs(attr, L ? (L->flags & ~VQB_FLAG_COOPERATIVE) : 0);
   VQB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a));
   set_kernel("gemv_cs");
-  set_launch(grid, kCsThreads, n_sh, 0);
+  set_launch(grid, NT, n_sh, 0);
   return 0;
 }
 
