@@ -796,7 +796,7 @@ def run_impl(args):
         if decode_tp:
             extra["decode_c5"] = decode_tp
         extra["step_per_launch"] = {
-            "what": "the same step as 128 single-linear gemv_fast launches (the per-call kernel of a decode loop)",
+            "what": "the same step as 128 single-linear vq_gemv launches (the per-call kernels of a decode loop)",
             "ms_per_step": ms_single, "GB_s": total_bytes / (ms_single * 1e-3) / 1e9,
             "frac": total_bytes / (ms_single * 1e-3) / 1e9 / world / hbm, "launches_per_step": single.n_launches,
             "max_abs_diff_vs_grouped": diff}

@@ -16,6 +16,7 @@ cap() {  # name, kernel regex, skip, command...: full capture -> raw CSV (the .n
 cap gemv_group gemv_group 0 python bench.py --steps 1 --warmup 3 --no-cpu --no-extra
 cap attn attn_cq 2 python tools/attn_bench.py
 cap gemv_tc gemv_tc 6 python tools/gemv_sweep.py --rows 16 --shapes 4096x12288 --copies 4
+cap gemv_cs gemv_cs 2 python tools/gemv_sweep.py --rows 1 --shapes 4096x4096 --copies 4
 cap gemm_dense gemm_dense 1 python tools/twophase_probe.py
 cap gemm_pair gemm_pair 1 python tools/twophase_probe.py
 timeout 300 python tools/decode_bench.py 1 2 4 8 16 32 64 > gpurun_out/decode_sweep.txt 2>&1; cat gpurun_out/decode_sweep.txt
