@@ -451,6 +451,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_cq_kernel(AttnArgs a) {
   }
   pdl_launch_dependents();
   attn_trace(a, 0);
+  if (threadIdx.x < 2) {
+    // L2 prefetch of the first unit's K / V codes while the preceding kernel drains (the
+    // work split depends on the device length, read speculatively: a stale value only
+    // misdirects a hint)
+    const int Ts = a.len_ptr ? max(1, min(*(volatile const int*)a.len_ptr, a.T_cap)) : a.T;
+    const int NTs = (Ts + kAttnChunk - 1) / kAttnChunk, Us = a.H * a.B * NTs;
+    const int GEs = min((int)gridDim.x, Us);
+    if ((int)blockIdx.x < GEs) {
+      const int u = (int)((int64_t)blockIdx.x * Us / GEs);
+      const int hh = u / (a.B * NTs), bb = (u / NTs) % a.B, tc = u % NTs;
+      const int64_t off = ((int64_t)(bb * a.H + hh) * a.T_cap + (int64_t)tc * kAttnChunk) * G;
+      const uint32_t bytes = (uint32_t)min(kAttnChunk, Ts - tc * kAttnChunk) * G;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((threadIdx.x ? a.vc : a.kc) + off),
+                   "r"((bytes + 15) & ~15u) : "memory");
+    }
+  }
   pdl_wait();  // q, the fresh KV codes and the length come from the preceding kernels
   attn_trace(a, 1);
   const uint32_t lut_base = smem_u32(lut_s);
