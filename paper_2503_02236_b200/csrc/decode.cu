@@ -549,6 +549,8 @@ __device__ __forceinline__ float sample_uniform(uint64_t seed, uint32_t step, ui
   return ((float)(uint32_t)(z >> 41) + 0.5f) * 1.1920928955078125e-7f;  // (k + 0.5) / 2^23: exact, in (0, 1)
 }
 
+constexpr int kSampleUnroll = 8;  // logits loaded per thread before they are used
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict__ logits, int dtype, int V,
                                                          float inv_temp, int top_k, uint64_t seed,
@@ -571,9 +573,15 @@ __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict_
     for (int shift = 24; shift >= 0; shift -= 8) {
       for (int i = tid; i < 256; i += THREADS) hist[i] = 0;
       __syncthreads();
-      for (int i = tid; i < V; i += THREADS) {
-        const uint32_t k = order_key(load(i));
-        if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
+      for (int i0 = tid; i0 < V; i0 += THREADS * kSampleUnroll) {
+        float xs[kSampleUnroll];  // independent loads first: one latency per kSampleUnroll elements
+#pragma unroll
+        for (int u = 0; u < kSampleUnroll; ++u) xs[u] = i0 + u * THREADS < V ? load(i0 + u * THREADS) : 0.f;
+#pragma unroll
+        for (int u = 0; u < kSampleUnroll; ++u) {
+          const uint32_t k = order_key(xs[u]);
+          if (i0 + u * THREADS < V && (k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
+        }
       }
       __syncthreads();
       if (warp == 0) {  // the digit holding the remaining-th largest: scan bins from the top
@@ -614,13 +622,20 @@ __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict_
   const uint32_t step = d_step ? (uint32_t)__ldg(d_step) : 0u;
   float bs = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = tid; i < V; i += THREADS) {
-    const float x = load(i);
-    if (order_key(x) < thr) continue;
-    const float s = greedy ? x : fmaf(x, inv_temp, -__logf(-__logf(sample_uniform(seed, step, (uint32_t)b, (uint32_t)i))));
-    if (s > bs || bi == 0x7fffffff) {  // ascending i per thread: strict > keeps the lowest index
-      bs = s;
-      bi = i;
+  for (int i0 = tid; i0 < V; i0 += THREADS * kSampleUnroll) {
+    float xs[kSampleUnroll];
+#pragma unroll
+    for (int u = 0; u < kSampleUnroll; ++u) xs[u] = i0 + u * THREADS < V ? load(i0 + u * THREADS) : 0.f;
+#pragma unroll
+    for (int u = 0; u < kSampleUnroll; ++u) {
+      const int i = i0 + u * THREADS;
+      const float x = xs[u];
+      if (i >= V || order_key(x) < thr) continue;
+      const float s = greedy ? x : fmaf(x, inv_temp, -__logf(-__logf(sample_uniform(seed, step, (uint32_t)b, (uint32_t)i))));
+      if (s > bs || bi == 0x7fffffff) {  // ascending i per thread: strict > keeps the lowest index
+        bs = s;
+        bi = i;
+      }
     }
   }
 #pragma unroll
