@@ -373,13 +373,10 @@ __device__ __forceinline__ int cq_nearest_team(const uint8_t* book, int stride, 
     const float cn = c0 * c0 + c1 * c1;
     cmax2 = fmaxf(cmax2, cn);
     const float d = fmaf(m0, c0, fmaf(m1, c1, cn));
-    if (d < d1) {
-      d2 = d1;
-      d1 = d;
-      e1 = e;
-    } else if (d < d2) {
-      d2 = d;
-    }
+    // branch-free best / second best (equal distances keep the earlier, lower index)
+    d2 = fminf(d2, fmaxf(d, d1));
+    e1 = d < d1 ? e : e1;
+    d1 = fminf(d1, d);
   }
 #pragma unroll
   for (int o = 1; o < TS; o <<= 1) {

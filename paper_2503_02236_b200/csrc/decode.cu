@@ -469,13 +469,10 @@ __global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* _
       const int e = i * S + split;
       const float4 c = bk[e];
       const float d = fmaf(m0, c.x, fmaf(m1, c.y, c.z));
-      if (d < d1) {
-        d2 = d1;
-        d1 = d;
-        e1 = e;
-      } else if (d < d2) {
-        d2 = d;
-      }
+      // branch-free best / second best (equal distances keep the earlier, lower index)
+      d2 = fminf(d2, fmaxf(d, d1));
+      e1 = d < d1 ? e : e1;
+      d1 = fminf(d1, d);
     }
     for (int o = 1; o < S; o <<= 1) {  // merge the row's lanes
       const float od1 = __shfl_xor_sync(0xffffffffu, d1, o), od2 = __shfl_xor_sync(0xffffffffu, d2, o);
