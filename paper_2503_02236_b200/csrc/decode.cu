@@ -373,6 +373,113 @@ __global__ void __launch_bounds__(256) qkv_rope_append_kernel(const __half* __re
 // second best per lane, merged over the row's lanes); only rows whose best two lie
 // within the fp32 error band rescore their candidates in float64 (the reference's
 // float64 argmin, lowest index on ties, is always among them).
+// Nearest-centroid codes of NR rows per lane (rows b0 + rl + r * rows) against one
+// group's book bk[e] = {c0, c1, |c|^2, 0}: fp32 screen keeping the best (lowest index
+// among equals) and second-best distance, S lanes per row merged, float64 rescoring of
+// near ties in the reference's operation order (V/codec.py:239-253).
+template <int NR>
+__device__ __forceinline__ void append_rows(const __half* __restrict__ qkv, int H, int C, bool is_k, int h, int gi,
+                                            const float (&cs)[2], const float (&sn)[2], const float4* bk,
+                                            float cmax2, int B, int rows, int S, int split, int rl, int n_e,
+                                            uint8_t* codes, int64_t bstride) {
+  for (int b0 = 0; b0 < B; b0 += rows * NR) {
+    float p0[NR], p1[NR], m0[NR], m1[NR], d1[NR], d2[NR];
+    int e1[NR];
+    bool valid[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int b = b0 + rl + r * rows;
+      valid[r] = b < B;
+      p0[r] = p1[r] = 0.f;
+      if (valid[r]) {
+        const __half* row = qkv + (int64_t)b * 3 * H * C + (int64_t)((is_k ? H : 2 * H) + h) * C;
+        float pj[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c = gi * 2 + j;
+          if (is_k) {
+            const int half = C / 2, i = c < half ? c : c - half;
+            const float x0 = __half2float(row[i]), x1 = __half2float(row[i + half]);
+            // the roped k is an fp16 tensor in the reference step
+            pj[j] = __half2float(__float2half_rn(c < half ? x0 * cs[j] - x1 * sn[j] : x1 * cs[j] + x0 * sn[j]));
+          } else {
+            pj[j] = __half2float(row[c]);
+          }
+        }
+        p0[r] = pj[0];
+        p1[r] = pj[1];
+      }
+      m0[r] = -2.f * p0[r];
+      m1[r] = -2.f * p1[r];
+      d1[r] = d2[r] = FLT_MAX;
+      e1[r] = 0x7fffffff;
+    }
+#pragma unroll 8
+    for (int i = 0; i < n_e; ++i) {
+      const int e = i * S + split;
+      const float4 c = bk[e];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const float d = fmaf(m0[r], c.x, fmaf(m1[r], c.y, c.z));
+        // branch-free best / second best (equal distances keep the earlier, lower index)
+        d2[r] = fminf(d2[r], fmaxf(d, d1[r]));
+        e1[r] = d < d1[r] ? e : e1[r];
+        d1[r] = fminf(d1[r], d);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      for (int o = 1; o < S; o <<= 1) {  // merge the row's lanes
+        const float od1 = __shfl_xor_sync(0xffffffffu, d1[r], o), od2 = __shfl_xor_sync(0xffffffffu, d2[r], o);
+        const int oe1 = __shfl_xor_sync(0xffffffffu, e1[r], o);
+        d2[r] = fminf(fmaxf(d1[r], od1), fminf(d2[r], od2));
+        if (od1 < d1[r] || (od1 == d1[r] && oe1 < e1[r])) {
+          d1[r] = od1;
+          e1[r] = oe1;
+        }
+      }
+      // screen tolerance: a bound on the fp32 rounding of |c|^2 - 2 p.c relative to the
+      // float64 distance (2 sqrt(|p|^2 |c|^2) <= |p|^2 + |c|^2 keeps it sqrt-free)
+      const float tol = 2e-5f * (cmax2 + p0[r] * p0[r] + p1[r] * p1[r]) + 1e-30f;
+      const bool need64 = valid[r] && (d2[r] - d1[r] <= tol);
+      int code = e1[r];
+      if (__any_sync(0xffffffffu, need64)) {
+        // several candidates: float64 distances in the reference's operation order
+        double best = DBL_MAX;
+        int be = 0x7fffffff;
+        if (need64) {
+          const double r0 = p0[r], r1 = p1[r];
+          const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
+          for (int i = 0; i < n_e; ++i) {
+            const int e = i * S + split;
+            const float4 c = bk[e];
+            if (fmaf(m0[r], c.x, fmaf(m1[r], c.y, c.z)) <= d1[r] + tol) {
+              const double a0 = c.x, a1 = c.y;
+              const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
+              const double cn = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
+              const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
+              if (d < best) {  // entries ascend: the first minimum is the lowest index
+                best = d;
+                be = e;
+              }
+            }
+          }
+        }
+        for (int o = 1; o < S; o <<= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+          if (ob < best || (ob == best && oe < be)) {
+            best = ob;
+            be = oe;
+          }
+        }
+        if (need64) code = be;
+      }
+      if (valid[r] && split == 0) codes[(int64_t)(b0 + rl + r * rows) * bstride] = (uint8_t)code;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* __restrict__ qkv,
                                                                __half* __restrict__ q_out, Geom gk,
                                                                void* __restrict__ kcodes,
@@ -438,90 +545,11 @@ __global__ void __launch_bounds__(256) qkv_rope_append_cq_kernel(const __half* _
   const int S = 32 / rows;  // lanes per row
   const int split = lane & (S - 1), rl = lane / S;
   const int n_e = 256 / S;
-  for (int b0 = 0; b0 < B; b0 += rows) {
-    const int b = b0 + rl;
-    const bool valid = b < B;
-    float p0 = 0.f, p1 = 0.f;
-    if (valid) {
-      const __half* row = qkv + (int64_t)b * 3 * H * C + (int64_t)((is_k ? H : 2 * H) + h) * C;
-      float pj[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = gi * 2 + j;
-        if (is_k) {
-          const int half = C / 2, i = c < half ? c : c - half;
-          const float x0 = __half2float(row[i]), x1 = __half2float(row[i + half]);
-          // the roped k is an fp16 tensor in the reference step
-          pj[j] = __half2float(__float2half_rn(c < half ? x0 * cs[j] - x1 * sn[j] : x1 * cs[j] + x0 * sn[j]));
-        } else {
-          pj[j] = __half2float(row[c]);
-        }
-      }
-      p0 = pj[0];
-      p1 = pj[1];
-    }
-    // fp32 screen: best (lowest index among equals) and second-best distance
-    const float m0 = -2.f * p0, m1 = -2.f * p1;
-    float d1 = FLT_MAX, d2 = FLT_MAX;
-    int e1 = 0x7fffffff;
-#pragma unroll 8
-    for (int i = 0; i < n_e; ++i) {
-      const int e = i * S + split;
-      const float4 c = bk[e];
-      const float d = fmaf(m0, c.x, fmaf(m1, c.y, c.z));
-      // branch-free best / second best (equal distances keep the earlier, lower index)
-      d2 = fminf(d2, fmaxf(d, d1));
-      e1 = d < d1 ? e : e1;
-      d1 = fminf(d1, d);
-    }
-    for (int o = 1; o < S; o <<= 1) {  // merge the row's lanes
-      const float od1 = __shfl_xor_sync(0xffffffffu, d1, o), od2 = __shfl_xor_sync(0xffffffffu, d2, o);
-      const int oe1 = __shfl_xor_sync(0xffffffffu, e1, o);
-      d2 = fminf(fmaxf(d1, od1), fminf(d2, od2));
-      if (od1 < d1 || (od1 == d1 && oe1 < e1)) {
-        d1 = od1;
-        e1 = oe1;
-      }
-    }
-    // screen tolerance: a bound on the fp32 rounding of |c|^2 - 2 p.c relative to the
-    // float64 distance (2 sqrt(|p|^2 |c|^2) <= |p|^2 + |c|^2 keeps it sqrt-free)
-    const float tol = 2e-5f * (cmax2 + p0 * p0 + p1 * p1) + 1e-30f;
-    const bool need64 = valid && (d2 - d1 <= tol);
-    int code = e1;
-    if (__any_sync(0xffffffffu, need64)) {
-      // several candidates: float64 distances in the reference's operation order
-      double best = DBL_MAX;
-      int be = 0x7fffffff;
-      if (need64) {
-        const double r0 = p0, r1 = p1;
-        const double pn = __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1));
-        for (int i = 0; i < n_e; ++i) {
-          const int e = i * S + split;
-          const float4 c = bk[e];
-          if (fmaf(m0, c.x, fmaf(m1, c.y, c.z)) <= d1 + tol) {
-            const double a0 = c.x, a1 = c.y;
-            const double dot = __dadd_rn(__dmul_rn(r0, a0), __dmul_rn(r1, a1));
-            const double cn = __dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1));
-            const double d = __dadd_rn(__dadd_rn(__dmul_rn(dot, -2.0), cn), pn);
-            if (d < best) {  // entries ascend: the first minimum is the lowest index
-              best = d;
-              be = e;
-            }
-          }
-        }
-      }
-      for (int o = 1; o < S; o <<= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-        if (ob < best || (ob == best && oe < be)) {
-          best = ob;
-          be = oe;
-        }
-      }
-      if (need64) code = be;
-    }
-    if (valid && split == 0) reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes)[off0 + (int64_t)b * bstride] = (uint8_t)code;
-  }
+  uint8_t* codes = reinterpret_cast<uint8_t*>(is_k ? kcodes : vcodes) + off0;
+  if (B > 32)  // two rows per lane: one broadcast read of each entry serves both
+    append_rows<2>(qkv, H, C, is_k, h, gi, cs, sn, bk, cmax2, B, rows, S, split, rl, n_e, codes, bstride);
+  else
+    append_rows<1>(qkv, H, C, is_k, h, gi, cs, sn, bk, cmax2, B, rows, S, split, rl, n_e, codes, bstride);
 }
 
 // ---- token sampling (the decode loop's last step) ----
