@@ -269,13 +269,14 @@ int vqb_qkv_rope_append(const void* d_qkv, void* d_q_out, const VqbTensor* k_cac
 /* out (rows, F) = silu(gate) * up for a fused [gate | up] (rows, 2F) input. */
 int vqb_silu_mul(const void* d_gate_up, void* d_out, int32_t rows, int32_t ffn, void* stream);
 /* Next tokens of a decode step: d_tokens[b] (int64) drawn from softmax(logits[b] / T)
- * restricted to the logits >= the top_k-th largest (top_k 0 = all) by the Gumbel-max
- * trick with a counter-based hash of (seed, *d_step, b, i) as the noise (d_step may be
- * NULL = step 0; pass the decode length so graph replays draw fresh noise);
- * temperature 0 = greedy argmax. Ties resolve to the lowest index. logits (B, vocab)
- * fp16 or fp32. */
+ * restricted to the logits >= the top_k-th largest (top_k 0 = all), then to the nucleus
+ * (the largest threshold whose kept probability mass is >= top_p; 1 = off; ties at the
+ * threshold kept), by the Gumbel-max trick with a counter-based hash of
+ * (seed, *d_step, b, i) as the noise (d_step may be NULL = step 0; pass the decode length
+ * so graph replays draw fresh noise); temperature 0 = greedy argmax. Ties resolve to the
+ * lowest index. logits (B, vocab) fp16 or fp32. */
 int vqb_sample(const void* d_logits, int32_t logits_dtype, int32_t B, int32_t vocab, float temperature,
-               int32_t top_k, uint64_t seed, const int32_t* d_step, int64_t* d_tokens, void* stream);
+               int32_t top_k, float top_p, uint64_t seed, const int32_t* d_step, int64_t* d_tokens, void* stream);
 /* d_len[0] += delta on the stream (advances a graph-replayed decode loop). */
 int vqb_add_len(int32_t* d_len, int32_t delta, void* stream);
 /* Read and clear the device error word (synchronises the device): bit 0 = a KV

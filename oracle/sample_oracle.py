@@ -37,18 +37,38 @@ def keep_mask(logits: np.ndarray, top_k: int) -> np.ndarray:
     return logits >= kth
 
 
-def scores(logits: np.ndarray, temperature: float, top_k: int, seed: int, step: int) -> np.ndarray:
-    """(B, V) float64 Gumbel-max scores, -inf outside the top-k set; temperature 0 =
-    the logits themselves (greedy)."""
+def nucleus_mask(logits: np.ndarray, temperature: float, keep: np.ndarray, top_p: float) -> np.ndarray:
+    """Within `keep`, the logits >= the largest threshold whose probability mass
+    (softmax(logits / T) over `keep`) is >= top_p (ties at the threshold kept)."""
+    if top_p >= 1.0:
+        return keep
+    out = np.zeros_like(keep)
+    for b in range(logits.shape[0]):
+        x = np.where(keep[b], logits[b].astype(np.float64), -np.inf)
+        w = np.exp((x - x.max()) / temperature)
+        order = np.argsort(-x, kind="stable")
+        cum = np.cumsum(w[order])
+        k = int(np.searchsorted(cum, top_p * cum[-1]))  # first prefix reaching the mass
+        tau = x[order[min(k, len(order) - 1)]]
+        out[b] = keep[b] & (x >= tau)
+    return out
+
+
+def scores(logits: np.ndarray, temperature: float, top_k: int, seed: int, step: int,
+           top_p: float = 1.0) -> np.ndarray:
+    """(B, V) float64 Gumbel-max scores, -inf outside the top-k / top-p set;
+    temperature 0 = the logits themselves (greedy)."""
     lg = np.asarray(logits, np.float64)
     if temperature <= 0:
         return lg.copy()
     idx = np.arange(lg.shape[1])
     g = np.stack([-np.log(-np.log(uniform(seed, step, b, idx))) for b in range(lg.shape[0])])
     s = lg / np.float64(np.float32(temperature)) + g
-    return np.where(keep_mask(lg, top_k), s, -np.inf)
+    keep = nucleus_mask(lg, float(np.float32(temperature)), keep_mask(lg, top_k), top_p)
+    return np.where(keep, s, -np.inf)
 
 
-def sample(logits: np.ndarray, temperature: float, top_k: int, seed: int, step: int) -> np.ndarray:
+def sample(logits: np.ndarray, temperature: float, top_k: int, seed: int, step: int,
+           top_p: float = 1.0) -> np.ndarray:
     """Next tokens (B,) int64: argmax of scores, lowest index on ties."""
-    return np.argmax(scores(logits, temperature, top_k, seed, step), axis=1).astype(np.int64)
+    return np.argmax(scores(logits, temperature, top_k, seed, step, top_p), axis=1).astype(np.int64)

@@ -144,7 +144,7 @@ def lib():
             L.vqb_silu_mul.argtypes = [vp, vp, i32, i32, vp]
             L.vqb_qkv_rope_append.argtypes = [vp, vp, T, T, i32, i32, i32, vp, f32, vp]
             L.vqb_add_len.argtypes = [vp, i32, vp]
-            L.vqb_sample.argtypes = [vp, i32, i32, i32, f32, i32, ctypes.c_uint64, vp, vp, vp]
+            L.vqb_sample.argtypes = [vp, i32, i32, i32, f32, i32, f32, ctypes.c_uint64, vp, vp, vp]
             L.vqb_take_device_error.argtypes = [P(i32)]
             L.vqb_cq_quantize.argtypes = [T, vp, i32, i64, i64, i64, i32, i32, vp, vp]
             L.vqb_layout_bytes.argtypes = [T, i32]

@@ -578,12 +578,14 @@ constexpr int kSampleUnroll = 8;  // logits loaded per thread before they are us
 
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict__ logits, int dtype, int V,
-                                                         float inv_temp, int top_k, uint64_t seed,
+                                                         float inv_temp, int top_k, float top_p, uint64_t seed,
                                                          const int* __restrict__ d_step, int64_t* __restrict__ out) {
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t sel[2];  // prefix, remaining
+  __shared__ unsigned long long hist[256];
+  __shared__ unsigned long long sel[2];  // digit, remaining weight
   __shared__ float best_s[THREADS / 32];
   __shared__ int best_i[THREADS / 32];
+  __shared__ float red_f[THREADS / 32];
+  __shared__ unsigned long long red_u[THREADS / 32];
   pdl_launch_dependents();
   pdl_wait();
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -591,12 +593,13 @@ __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict_
   const __half* lh = reinterpret_cast<const __half*>(logits) + (int64_t)b * V;
   auto load = [&](int i) { return dtype == VQB_F32 ? __ldg(lf + i) : __half2float(lh[i]); };
   const bool greedy = !(inv_temp > 0.f);
-  uint32_t thr = 0;  // keep keys >= thr
-  if (!greedy && top_k > 0 && top_k < V) {
+  // Radix select over order-preserving keys: the largest key t with weight(keys >= t,
+  // keys >= floor) >= target, weight(x) = 1 (top-k) or the fixed-point probability.
+  auto select = [&](unsigned long long target, uint32_t floor, auto weight) -> uint32_t {
     uint32_t prefix = 0, mask = 0;
-    if (tid == 0) sel[1] = (uint32_t)top_k;
+    if (tid == 0) sel[1] = target;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = tid; i < 256; i += THREADS) hist[i] = 0;
+      for (int i = tid; i < 256; i += THREADS) hist[i] = 0ull;
       __syncthreads();
       for (int i0 = tid; i0 < V; i0 += THREADS * kSampleUnroll) {
         float xs[kSampleUnroll];  // independent loads first: one latency per kSampleUnroll elements
@@ -605,31 +608,31 @@ __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict_
 #pragma unroll
         for (int u = 0; u < kSampleUnroll; ++u) {
           const uint32_t k = order_key(xs[u]);
-          if (i0 + u * THREADS < V && (k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
+          if (i0 + u * THREADS < V && k >= floor && (k & mask) == prefix)
+            atomicAdd(&hist[(k >> shift) & 255], weight(xs[u]));
         }
       }
       __syncthreads();
-      if (warp == 0) {  // the digit holding the remaining-th largest: scan bins from the top
-        uint32_t c[8], tot = 0;
+      if (warp == 0) {  // the digit holding the target: scan bins from the top
+        unsigned long long c[8], tot = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           c[j] = hist[255 - (lane * 8 + j)];
           tot += c[j];
         }
-        uint32_t incl = tot;  // inclusive prefix over lanes (lane 0 = the highest bins)
+        unsigned long long incl = tot;  // inclusive prefix over lanes (lane 0 = the highest bins)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += t;
         }
-        const uint32_t rem = sel[1];
-        uint32_t run = incl - tot;
-        const bool mine = run < rem && incl >= rem;
-        if (mine) {
+        const unsigned long long rem = sel[1];
+        unsigned long long run = incl - tot;
+        if (run < rem && incl >= rem) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             if (run + c[j] >= rem) {
-              sel[0] = (uint32_t)(255 - (lane * 8 + j));
+              sel[0] = (unsigned long long)(255 - (lane * 8 + j));
               sel[1] = rem - run;
               break;
             }
@@ -638,11 +641,46 @@ __global__ void __launch_bounds__(THREADS) sample_kernel(const void* __restrict_
         }
       }
       __syncthreads();
-      prefix |= sel[0] << shift;
+      prefix |= (uint32_t)sel[0] << shift;
       mask |= 255u << shift;
       __syncthreads();
     }
-    thr = prefix;
+    return prefix;
+  };
+  uint32_t thr = 0;  // keep keys >= thr
+  if (!greedy && top_k > 0 && top_k < V) thr = select((unsigned long long)top_k, 0u, [](float) { return 1ull; });
+  if (!greedy && top_p < 1.f) {
+    // nucleus over the (top-k) kept logits: weights exp((x - max) / T) in 2^32 fixed point
+    float mx = -INFINITY;
+    for (int i = tid; i < V; i += THREADS) {
+      const float x = load(i);
+      if (order_key(x) >= thr) mx = fmaxf(mx, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red_f[warp] = mx;
+    __syncthreads();
+    mx = red_f[0];
+    for (int w = 1; w < THREADS / 32; ++w) mx = fmaxf(mx, red_f[w]);
+    const float sc = inv_temp * 1.4426950408889634f;
+    auto weight = [&](float x) {
+      return (unsigned long long)(exp2f((x - mx) * sc) * 4294967296.0f);
+    };
+    unsigned long long tw = 0;
+    for (int i = tid; i < V; i += THREADS) {
+      const float x = load(i);
+      if (order_key(x) >= thr) tw += weight(x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tw += __shfl_xor_sync(0xffffffffu, tw, o);
+    if (lane == 0) red_u[warp] = tw;
+    __syncthreads();
+    tw = 0;
+    for (int w = 0; w < THREADS / 32; ++w) tw += red_u[w];
+    __syncthreads();
+    unsigned long long target = (unsigned long long)ceil((double)top_p * (double)tw);
+    if (target < 1) target = 1;
+    thr = max(thr, select(target, thr, weight));
   }
   const uint32_t step = d_step ? (uint32_t)__ldg(d_step) : 0u;
   float bs = -INFINITY;
@@ -784,13 +822,16 @@ extern "C" int vqb_take_device_error(int32_t* out) {
 }
 
 extern "C" int vqb_sample(const void* d_logits, int32_t logits_dtype, int32_t B, int32_t vocab, float temperature,
-                          int32_t top_k, uint64_t seed, const int32_t* d_step, int64_t* d_tokens, void* stream) {
+                          int32_t top_k, float top_p, uint64_t seed, const int32_t* d_step, int64_t* d_tokens,
+                          void* stream) {
   if (B < 1 || vocab < 1) return set_error(VQB_ESHAPE, "sample needs B >= 1 and vocab >= 1");
   if (logits_dtype != VQB_F16 && logits_dtype != VQB_F32) return set_error(VQB_ECONFIG, "sample reads fp16 or fp32 logits");
-  if (!(temperature >= 0.f) || top_k < 0) return set_error(VQB_ECONFIG, "sample needs temperature >= 0 and top_k >= 0");
+  if (!(temperature >= 0.f) || top_k < 0 || !(top_p > 0.f && top_p <= 1.f))
+    return set_error(VQB_ECONFIG, "sample needs temperature >= 0, top_k >= 0 and 0 < top_p <= 1");
   const float inv_temp = temperature > 0.f ? 1.0f / temperature : 0.f;
   VQB_CUDA_CHECK(launch_pdl(sample_kernel<1024>, dim3(B), dim3(1024), 0, reinterpret_cast<cudaStream_t>(stream),
-                            d_logits, (int)logits_dtype, (int)vocab, inv_temp, (int)top_k, seed, d_step, d_tokens));
+                            d_logits, (int)logits_dtype, (int)vocab, inv_temp, (int)top_k, top_p, seed, d_step,
+                            d_tokens));
   VQB_LAUNCH_CHECK("sample_kernel");
   set_kernel("sample");
   return VQB_OK;

@@ -80,7 +80,7 @@ class VQLlamaDecoder:
         self.length = 0  # host mirror of d_len (the step advances both)
         self.ws = ops.Workspace(self.device)  # private arena the captured graph keeps alive
         # next-token rule (vqb_sample): greedy by default; set_sampling before capture()
-        self.temperature, self.top_k, self.seed = 0.0, 0, 0
+        self.temperature, self.top_k, self.seed, self.top_p = 0.0, 0, 0, 1.0
         self.capacity = min(L.k_cache.shape[2] for L in self.layers) if self.layers else 0
         # batch 1: the fused gate_up projection is stored interleaved per 128 columns,
         # [gate 128 | up 128] in every 256-column block, so its GEMV epilogue emits
@@ -327,17 +327,18 @@ class VQLlamaDecoder:
         self.logits = xn @ self.lm_head
         return self._sample()
 
-    def set_sampling(self, temperature: float = 0.0, top_k: int = 0, seed: int = 0) -> None:
-        """Temperature / top-k sampling of the next token (Gumbel-max over the logits,
+    def set_sampling(self, temperature: float = 0.0, top_k: int = 0, seed: int = 0, top_p: float = 1.0) -> None:
+        """Temperature / top-k / top-p sampling of the next token (Gumbel-max over the logits,
         noise hashed from the seed and the device length, so every replayed step draws
         afresh and TP ranks draw identically). temperature 0 = greedy. A captured graph
         keeps the rule it was captured with: call this before capture()."""
-        if temperature < 0 or top_k < 0:
-            raise ConfigError("sampling needs temperature >= 0 and top_k >= 0")
-        self.temperature, self.top_k, self.seed = float(temperature), int(top_k), int(seed)
+        if temperature < 0 or top_k < 0 or not 0 < top_p <= 1:
+            raise ConfigError("sampling needs temperature >= 0, top_k >= 0 and 0 < top_p <= 1")
+        self.temperature, self.top_k, self.seed, self.top_p = float(temperature), int(top_k), int(seed), float(top_p)
 
     def _sample(self) -> torch.Tensor:
-        return ops.sample(self.logits, self.temperature, self.top_k, self.seed, d_step=self.d_len, out=self.tokens)
+        return ops.sample(self.logits, self.temperature, self.top_k, self.seed, d_step=self.d_len, out=self.tokens,
+                          top_p=self.top_p)
 
     def capture(self) -> None:
         """Record one step as a CUDA graph. The warm-up step (on the capture stream)

@@ -274,11 +274,12 @@ def silu_mul(gate_up: torch.Tensor, out=None) -> torch.Tensor:
 
 
 def sample(logits: torch.Tensor, temperature: float = 0.0, top_k: int = 0, seed: int = 0,
-           d_step: torch.Tensor = None, out: torch.Tensor = None) -> torch.Tensor:
+           d_step: torch.Tensor = None, out: torch.Tensor = None, top_p: float = 1.0) -> torch.Tensor:
     """Next tokens (B,) int64 from logits (B, vocab) fp16/fp32: a Gumbel-max draw from
     softmax(logits / temperature) over the top_k largest logits (0 = all; ties at the
-    k-th value kept), noise hashed from (seed, d_step[0], row, index); temperature 0 is
-    greedy argmax (lowest index on ties, like torch.argmax)."""
+    k-th value kept) and then the top_p nucleus (1.0 = off), noise hashed from
+    (seed, d_step[0], row, index); temperature 0 is greedy argmax (lowest index on ties,
+    like torch.argmax)."""
     if logits.dim() != 2 or logits.dtype not in (torch.float16, torch.float32) or not logits.is_contiguous():
         raise ShapeError(f"logits {tuple(logits.shape)} {logits.dtype} must be a contiguous (B, vocab) fp16/fp32 tensor")
     b, v = logits.shape
@@ -288,7 +289,7 @@ def sample(logits: torch.Tensor, temperature: float = 0.0, top_k: int = 0, seed:
     if d_step is not None and (d_step.dtype != torch.int32 or d_step.device != logits.device):
         raise ShapeError("d_step must be a device int32 tensor")
     N.check(N.lib().vqb_sample(logits.data_ptr(), dtype_enum(logits.dtype), b, v, float(temperature), int(top_k),
-                               int(seed) & 0xFFFFFFFFFFFFFFFF, None if d_step is None else d_step.data_ptr(),
+                               float(top_p), int(seed) & 0xFFFFFFFFFFFFFFFF, None if d_step is None else d_step.data_ptr(),
                                out.data_ptr(), _stream(logits.device)))
     return out
 

@@ -461,7 +461,7 @@ def test_decode_sampling_replay_matches_eager(dev):
     a = VQLlamaDecoder.synthetic(sh, 4, 64, dev, seed=8)
     b = VQLlamaDecoder.synthetic(sh, 4, 64, dev, seed=8)
     for d in (a, b):
-        d.set_sampling(temperature=0.8, top_k=20, seed=77)
+        d.set_sampling(temperature=0.8, top_k=20, seed=77, top_p=0.9)
         d.tokens.fill_(7)
     b.capture()
     for _ in range(4):
@@ -469,7 +469,7 @@ def test_decode_sampling_replay_matches_eager(dev):
         b.replay()
         assert torch.equal(tok, b.tokens)
         lg = a.logits.float().cpu().numpy()
-        sc = SO.scores(lg, 0.8, 20, 77, int(a.d_len.item()))
+        sc = SO.scores(lg, 0.8, 20, 77, int(a.d_len.item()), top_p=0.9 + 2e-3)
         t = tok.cpu().numpy()
         got = sc[np.arange(4), t]
         assert np.all(np.isfinite(got)) and np.all(got >= sc.max(axis=1) - 1e-4 * np.maximum(1, np.abs(sc.max(axis=1))))

@@ -2,7 +2,8 @@
 restatement in oracle/sample_oracle.py: greedy = torch.argmax (lowest index on
 ties), temperature / top-k Gumbel-max draws = the oracle's token up to fp32 score
 rounding (1e-4 on the oracle's float64 scores), the top-k set (ties at the k-th
-value kept), and the sampled distribution = softmax(logits / T) over that set."""
+value kept), the top-p nucleus (fp32 fixed-point weights: 2e-3 mass margin), and the
+sampled distribution = softmax(logits / T) over the kept set."""
 
 import numpy as np
 import pytest
@@ -121,3 +122,56 @@ def test_sample_errors(dev):
         ops.sample(lg, -1.0)
     with pytest.raises(ShapeError):
         ops.sample(lg.to(torch.int32))
+
+
+def test_oracle_nucleus_mask():
+    lg = np.array([[3.0, 2.0, 1.0, 0.0], [2.0, 2.0, 1.0, -5.0]])
+    keep = np.ones(lg.shape, bool)
+    assert SO.nucleus_mask(lg, 1.0, keep, 0.8)[0].tolist() == [True, True, False, False]
+    assert SO.nucleus_mask(lg, 1.0, keep, 0.5)[0].tolist() == [True, False, False, False]
+    assert SO.nucleus_mask(lg, 1.0, keep, 0.3)[1].tolist() == [True, True, False, False]  # ties kept
+    assert SO.nucleus_mask(lg, 1.0, keep, 1.0).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("temperature,top_k,top_p", [(1.0, 0, 0.9), (0.7, 50, 0.8), (1.3, 0, 0.5)])
+def test_nucleus_draw_matches_oracle(temperature, top_k, top_p, dev):
+    from paper_2503_02236_b200 import ops
+    g = torch.Generator(device=dev).manual_seed(12)
+    lg = (torch.randn((32, 32000), generator=g, device=dev) * 3).half()
+    step = torch.tensor([9], dtype=torch.int32, device=dev)
+    tok = ops.sample(lg, temperature, top_k, seed=5, d_step=step, top_p=top_p).cpu().numpy()
+    host = lg.float().cpu().numpy()
+    t32 = float(np.float32(temperature))
+    wide = SO.nucleus_mask(host, t32, SO.keep_mask(host, top_k), min(1.0, top_p + 2e-3))
+    assert wide[np.arange(32), tok].all()  # every draw inside the nucleus (fp32 weights: small margin)
+    want = SO.sample(host, temperature, top_k, 5, 9, top_p)
+    assert (tok == want).mean() >= 0.9
+
+
+@pytest.mark.gpu
+def test_nucleus_distribution(dev):
+    """Frequencies within 5 sigma of softmax renormalised over the nucleus."""
+    from paper_2503_02236_b200 import ops
+    l8 = torch.tensor([0.1, 1.5, -0.7, 0.9, 2.2, -2.0, 0.0, 1.1])
+    rows = 20000
+    lg = l8.repeat(rows, 1).to(dev)
+    for temperature, top_p in ((1.0, 0.7), (0.6, 0.9)):
+        tok = ops.sample(lg, temperature, 0, seed=17, top_p=top_p).cpu().numpy()
+        keep = SO.nucleus_mask(l8.numpy()[None].astype(np.float64), temperature, np.ones((1, 8), bool), top_p)[0]
+        p = torch.softmax(l8 / temperature, 0).numpy().astype(np.float64)
+        p = np.where(keep, p, 0.0)
+        p /= p.sum()
+        freq = np.bincount(tok, minlength=8) / rows
+        sigma = np.sqrt(p * (1 - p) / rows) + 1e-12
+        assert np.all(np.abs(freq - p) <= 5 * sigma + 1e-9), (temperature, top_p, freq, p)
+
+
+@pytest.mark.gpu
+def test_top_p_errors(dev):
+    from paper_2503_02236_b200 import ops
+    from paper_2503_02236_b200.errors import ConfigError
+    lg = torch.zeros((2, 10), device=dev)
+    for bad in (0.0, 1.5):
+        with pytest.raises(ConfigError):
+            ops.sample(lg, 1.0, top_p=bad)
