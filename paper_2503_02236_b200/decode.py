@@ -161,7 +161,8 @@ class VQLlamaDecoder:
 
     gemv_max_rows = 64  # batches up to this take the decode GEMV (CUDA cores 1-3, mma.sync 4, tcgen05 5-64)
     fuse_norms = True  # batch 1: RMSNorm / SiLU gating fused into the following GEMV's prologue
-    fuse_append = True  # RoPE + KV append inside the attention kernel (CQ-4 caches at C = 128, batch <= 8)
+    fuse_append = True  # RoPE + KV append inside the attention kernel (CQ-4 caches at C = 128)
+    fuse_append_max_batch = 8  # measured: the separate append kernel wins from batch 16
 
     def _attend(self, L: DecoderLayer, qkv: torch.Tensor) -> torch.Tensor:
         """RoPE, online KV quantization of the new token and decode attention: one fused
@@ -169,7 +170,7 @@ class VQLlamaDecoder:
         sh = self.shape
         # measured: fused wins at batch 1-8 (1.83 vs 1.88 ms at 1, 3.07 vs 3.19 at 4); from 16
         # rows the CTA holding each (b, h)'s last chunk serialises too many quantizations
-        if (self.fuse_append and self.batch <= 8 and L.k_cache.shape[3] == 128 and L.k_cache.config == KV_CFG
+        if (self.fuse_append and self.batch <= self.fuse_append_max_batch and L.k_cache.shape[3] == 128 and L.k_cache.config == KV_CFG
                 and L.k_cache.layout == "kv"):
             return ops.vq_attention_append(L.k_cache, L.v_cache, qkv, self.d_len, sh.rope_theta)
         q = ops.qkv_rope_append(qkv, L.k_cache, L.v_cache, self.d_len, sh.rope_theta)
