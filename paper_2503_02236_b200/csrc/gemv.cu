@@ -1274,7 +1274,7 @@ int gemv_dispatch(const VqbTensor* w, const void* x, int x_dtype, int rows, void
     a.n_reg = p.n_reg;
     const int grid = (int)std::min<int64_t>(units, sm_count());  // upper bound for the slot check
     // head layout: [0, 64 KB) split-arrival counters (attention), then the GEMV slots
-    if ((int64_t)grid * rows * (32 * p.WG * p.V) * 8 > VQB_WS_COUNTER_BYTES - 65536)
+    if ((int64_t)grid * rows * (32 * p.WG * p.V) * 8 > VQB_WS_COUNTER_BYTES - 2 * 65536)
       return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
     a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
     a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
@@ -1407,7 +1407,7 @@ int gemv_grouped_dispatch(const VqbTensor* ws_t, int n, const void* const* xs, i
   uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
   int grid = balanced_grid(units, sm_count());
   if (L && L->grid_limit > 0) grid = std::min(grid, L->grid_limit);
-  if ((int64_t)grid * rows * 256 * 8 > VQB_WS_COUNTER_BYTES - 65536)
+  if ((int64_t)grid * rows * 256 * 8 > VQB_WS_COUNTER_BYTES - 2 * 65536)
     return set_error(VQB_ECAPACITY, "GEMV partial slots exceed the workspace head");
   a.part = reinterpret_cast<unsigned long long*>(wsb + 65536);
   a.trace = (L && (L->flags & 32)) ? reinterpret_cast<unsigned long long*>(wsb + VQB_WS_COUNTER_BYTES) : nullptr;
