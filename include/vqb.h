@@ -136,8 +136,8 @@ typedef struct VqbLaunch {
 #define VQB_FLAG_GEMV_TC 2048    /* GEMV: the tcgen05 decode GEMV (batch as the UMMA N) also below its
                                     default batch range */
 #define VQB_FLAG_NO_GEMV_TC 4096 /* GEMV: never the tcgen05 decode GEMV (mma.sync / CUDA-core kernels) */
-#define VQB_FLAG_NO_COLSPLIT 8192 /* GEMV batch 1: the stream-K kernel (split over M) instead of the
-                                     column-split kernel for N = 16 x 256-column outputs */
+#define VQB_FLAG_NO_COLSPLIT 8192 /* GEMV batch 1/2/4: the stream-K kernel (split over M) instead of
+                                     the column-split kernel for N = 16 x 256-column outputs */
 #define VQB_FLAG_GEMM_FUSED 512  /* GEMM: keep the fused (dequantise-in-the-producers) kernels at
                                     prefill sizes where the two-phase path is the default */
 #define VQB_FLAG_GEMM_TWO_PHASE 1024 /* GEMM (rows > 256, v = 8, N % 256 == 0): dequantise W to an fp16
