@@ -76,3 +76,19 @@ def test_colsplit_not_taken_outside_its_shapes(dev):
     w, _, _ = _weight(dev, (4096, 4096), 65536, 65536, seed=8)  # codes beyond 256: global tier
     ops.vq_gemv(w, torch.randn((1, 4096), device=dev).half())
     assert N.last_kernel() != "gemv_cs"
+
+
+@pytest.mark.parametrize("m", [4104, 1032, 8])  # row groups not a multiple of the 128 row lanes
+@pytest.mark.parametrize("rows", [1, 4])
+def test_colsplit_ragged_rows(m, rows, dev):
+    from paper_2503_02236_b200 import _native as N
+    from paper_2503_02236_b200 import ops
+    shape = (m, 4096)
+    w, codes, books = _weight(dev, shape, 256, 256, seed=m)
+    x = O.round_f16(O.synthetic_tensor((rows, m), 4))
+    y = ops.vq_gemv(w, torch.from_numpy(x).to(dev).half(), out_dtype=torch.float32)
+    assert N.last_kernel() == "gemv_cs"
+    regions = O.region_ids(shape, 8, "whole", (256, 256), 0)
+    ref = CO.gemv(codes, books, shape, 8, 1, regions, x)
+    got = y.float().cpu().numpy()
+    assert float(np.abs(got - ref).max() / np.abs(ref).max()) <= 1e-3
