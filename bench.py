@@ -812,7 +812,7 @@ def run_impl(args):
                     torch, dev, ops, N, "C1 gptvq2 VQ<4,8,1> tile256 4096x4096 b1",
                     (4, 8, 1, Sharing.per_tile(256, 256)), (4096, 4096))
             if want("decode_c5"):
-                extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 4, 8, 16, 32, 64)]  # BASELINE C5 sweep
+                extra["decode_c5"] = [time_decode(torch, dev, b) for b in (1, 2, 4, 8, 16, 32, 64)]  # BASELINE C5 sweep
             if want("gemm_c2"):
                 extra["gemm_c2_prefill"] = time_gemm(
                     torch, dev, N, "C2 quip2 VQ<8,16,1> ws256 llama7b prefill rows 1024", VQConfig(8, 16, 1),
